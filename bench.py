@@ -1,0 +1,400 @@
+"""Benchmark: voxel-ADMM-iterations/s (fp64) of the outer iteration.
+
+Default workload (N=1): SURVEY §8(d) config 2 inputs at the metric's 256^3 —
+3D two-phase neo-Hookean laminate (Mooney-Rivlin, mu in {1, 0.05},
+kappa = 9.8 mu, layers normal to x_1), fully strain-controlled
+<F> = diag(0.95, 1, 1), F perturbed once by 1e-4 N(0,1) (seed 0),
+RatioToDual(0.3) local policy, default SolverParams.  A step is one ADMM
+outer iteration (solver.outer_iteration): local step, projection, multiplier
+ascent, residuals, penalty update.  W warm-up iterations from init_state,
+then K timed iterations.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--n 256] [--impl ours|reference]
+
+Under torchrun (N > 1) every rank runs its own replica (weak scaling); the
+timed region is bracketed by a barrier + synchronize and the max over ranks
+is reported.  ``--impl reference`` times the CPU restatement of the
+reference (oracle/, the "port") on the host cores on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B_ALG_MR3 = 952.0  # algorithmic bytes per voxel-iteration, 3D MR
+WORD = 8.0
+
+
+def laminate(n, dim=3):
+    """Config-2 inputs: phase = (x_1 + L)/(2L) < 0.5, composite_moduli(1, 20, 9.8)."""
+    L = 0.5
+    h = 2 * L / n
+    x = -L + h * np.arange(n)
+    chi = ((x + L) / (2 * L) < 0.5).astype(float)
+    chi = np.broadcast_to(chi.reshape((n,) + (1,) * (dim - 1)), (n,) * dim).ravel()
+    mu = 1.0 + (1.0 / 20.0 - 1.0) * chi
+    return mu, 9.8 * mu
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index=0):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        if self.th:
+            self.th.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def stage_bytes(n, dim=3):
+    """Algorithmic bytes per launch of each pipeline stage."""
+    M = n ** dim
+    nh = n // 2 + 1
+    D = dim * dim
+    spec = dim * (M // n) * nh * 16.0  # d-component half spectrum
+    return {
+        "local": (3 * D + 2 + D) * WORD * M,            # read F,G,lam,mu,kappa, write F
+        "row_fwd": 2 * D * WORD * M + spec,              # read F,lam, write spectrum
+        "col_fwd": 2 * spec,
+        "col_solve": 2 * spec,
+        "col_inv": 2 * spec,
+        "row_inv": spec + dim * WORD * M,                # read spectrum, write u_tilde
+        "grad": (dim + 3 * D) * WORD * M + 2 * D * WORD * M,  # read u,F,lam,G; write G,lam
+    }
+
+
+def setup_problem(mm, n, device_params=None):
+    dim = 3
+    grid = mm.Grid(dim, n, 0.5)
+    mu, kap = laminate(n, dim)
+    model = mm.MooneyRivlin(mu, kap, dim=dim, mu_rep=1.0)
+    bc = mm.MacroBC.strain(np.diag([0.95, 1.0, 1.0]))
+    params = mm.SolverParams()
+    st = mm.solver.init_state(grid, model, bc, params)
+    st.F = st.F + 1e-4 * np.random.default_rng(0).standard_normal(st.F.shape)
+    return grid, model, bc, params, st
+
+
+def run_ours(args, rank, world, dist):
+    import torch
+
+    import paper_2010_06697_b200 as mm
+    from paper_2010_06697_b200 import _lib
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    n = args.n
+    M = n ** 3
+    grid, model, bc, params, st = setup_problem(mm, n)
+    pol = mm.RatioToDual(0.3)
+    t_setup = time.perf_counter()
+    for _ in range(args.warmup):
+        mm.solver.outer_iteration(grid, model, st, params, bc, pol)
+    eng = st._engine
+    ctx = eng.ctx
+    ctx.synchronize()
+    ctx.profile_read(reset=True)
+    ctx.profile_enable(True)
+    sampler = ClockSampler(dev)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    # the library runs on its own stream; bracket it from the torch stream with
+    # full synchronisation on both sides (outer_iteration ends in a host sync)
+    t0.record()
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    hist = []
+    for _ in range(args.steps):
+        hist.append(mm.solver.outer_iteration(grid, model, st, params, bc, pol))
+    ctx.synchronize()
+    w1 = time.perf_counter()
+    t1.record()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms_total = max(t0.elapsed_time(t1), (w1 - w0) * 1e3)
+    ctx.profile_enable(False)
+    stage_ms, stage_launch = ctx.profile_read(reset=True)
+    if dist is not None:
+        t = torch.tensor([ms_total], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    sweeps = st.total_sweeps
+
+    # ---- e2e through the public API with host buffers: solve() on a host
+    # state (fresh engine: H2D of F, grad_u, lam, moduli), K iterations, then
+    # read F, grad_u, lam, u_tilde back to the host.
+    host = dict(F=st.F.copy(), grad_u=st.grad_u.copy(), lam=st.lam.copy(),
+                u_tilde=st.u_tilde.copy(), u_mean=st.u_mean.copy())
+    pinned = {}
+    for k in ("F", "grad_u", "lam"):
+        t = torch.empty(host[k].shape, dtype=torch.float64, pin_memory=True)
+        t.numpy()[...] = host[k]
+        pinned[k] = t
+    rho, r_d_prev, oi = st.rho, st.r_d_prev, st.outer_iter
+    del st, eng, ctx
+    import gc
+    gc.collect()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0 = time.perf_counter()
+    hs = mm.ADMMState(u_mean=host["u_mean"], u_tilde=host["u_tilde"],
+                      grad_u=pinned["grad_u"].numpy(), F=pinned["F"].numpy(),
+                      lam=pinned["lam"].numpy(), internal={}, rho=rho, outer_iter=oi,
+                      r_d_prev=r_d_prev)
+    p_e2e = mm.SolverParams(max_outer=args.steps)
+    hs, _ = mm.solve(grid, model, bc, p_e2e, policy=pol, state=hs, raise_on_max=False)
+    outs = [hs.F, hs.grad_u, hs.lam, hs.u_tilde]
+    hs._engine.ctx.synchronize()
+    e1 = time.perf_counter()
+    e2e_ms = (e1 - e0) * 1e3
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    h2d = sum(pinned[k].numel() * 8 for k in pinned) + host["u_tilde"].nbytes + 2 * M * 8
+    d2h = sum(o.nbytes for o in outs)
+
+    value = world * M * args.steps / (ms_total / 1e3)
+    e2e_value = world * M * args.steps / (e2e_ms / 1e3)
+    peak, peak_kind = measured_peak()
+    sb = stage_bytes(n)
+    per_stage = {}
+    for s_name, ms in stage_ms.items():
+        nl = stage_launch.get(s_name, 0)
+        if nl and s_name in sb:
+            avg = ms / nl
+            per_stage[s_name] = {"ms_total": round(ms, 4), "launches": nl,
+                                 "ms_per_launch": round(avg, 5),
+                                 "GBps": round(sb[s_name] / (avg / 1e3) / 1e9, 1)}
+    dom = max(per_stage, key=lambda k: per_stage[k]["ms_total"]) if per_stage else None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(dom)
+    except Exception:
+        pass
+    roof = None
+    if dom:
+        ach = per_stage[dom]["GBps"]
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": traffic,
+                "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"
+                if peak_kind == "measured" else "fallback B200_PROFILING.md"}
+    it_ms = ms_total / args.steps
+    roof_it = {"bound": "hbm", "B_alg_per_voxel": B_ALG_MR3,
+               "achieved": round(B_ALG_MR3 * M / (it_ms / 1e3) / 1e9, 1), "peak": peak,
+               "unit": "GB/s", "frac": round(B_ALG_MR3 * M / (it_ms / 1e3) / 1e9 / peak, 4)}
+    line = {
+        "metric": "voxel-ADMM-iterations/sec (fp64)",
+        "value": value,
+        "unit": "voxel-iter/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": it_ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (config-2 laminate inputs, seeded)",
+        "config": {"workload": f"3D neo-Hookean laminate {n}^3 (SURVEY 8(d) config 2 inputs at "
+                               f"the metric's {n}^3), one replica per GPU",
+                   "grid": n, "material": "MooneyRivlin mu in {1, 0.05}, kappa = 9.8 mu",
+                   "bc": "strain diag(0.95,1,1)", "policy": "RatioToDual(0.3)",
+                   "steps_are": f"outer iterations {args.warmup + 1}..{args.warmup + args.steps}"
+                                f" from init_state",
+                   "l2": "inputs larger than L2 (state 3.6 GB at 256^3)",
+                   "parallelism": f"replicas x{world}"},
+        "local_sweeps_total": int(sweeps),
+        "residuals_last": {"r_p": hist[-1].r_p, "r_d": hist[-1].r_d, "r_l": hist[-1].r_l,
+                           "rho": hist[-1].rho},
+        "stages": per_stage,
+        "roofline": roof,
+        "roofline_iteration": roof_it,
+        "gpu_launches": int(sum(stage_launch.values())),
+        "clocks": clocks,
+        "e2e": {"value": e2e_value, "unit": "voxel-iter/s", "h2d_bytes_per_step": h2d / args.steps,
+                "d2h_bytes_per_step": d2h / args.steps,
+                "how": "solve(max_outer=K) on a host (pinned) state: engine creation, H2D of F, "
+                       "grad_u, lam, u_tilde, moduli, K iterations, D2H of F, grad_u, lam, "
+                       "u_tilde; wall clock"},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.cpu_n, args.cpu_steps)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(n, steps, warm=1):
+    """Oracle port on the host cores, bounded sample of the same workload."""
+    import oracle
+
+    cores = len(os.sched_getaffinity(0))
+    oracle.set_threads(cores)
+    mu, kap = laminate(n, 3)
+    om = oracle.MR(mu, kap, dim=3, mu_rep=1.0)
+    mask = np.ones((3, 3), bool)
+    val = np.diag([0.95, 1.0, 1.0])
+    params = oracle.Params()
+    st = oracle.init_state(3, n, om, mask, val, params)
+    st.F = st.F + 1e-4 * np.random.default_rng(0).standard_normal(st.F.shape)
+    sym = oracle.symbols(3, n, 0.5)
+    pol = oracle.RatioToDual(0.3)
+    for _ in range(warm):
+        oracle.outer_iteration(3, n, 0.5, om, st, params, mask, val, pol, sym=sym)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        oracle.outer_iteration(3, n, 0.5, om, st, params, mask, val, pol, sym=sym)
+    dt = time.perf_counter() - t0
+    return {"value": n ** 3 * steps / dt, "unit": "voxel-iter/s", "cores": cores, "kind": "port",
+            "sample": f"oracle port (C local kernels + numpy FFT), same laminate at {n}^3, "
+                      f"outer iterations {warm + 1}..{warm + steps}, {dt:.1f} s"}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    import oracle
+
+    n = args.cpu_n
+    cores = len(os.sched_getaffinity(0))
+    oracle.set_threads(cores)
+    mu, kap = laminate(n, 3)
+    om = oracle.MR(mu, kap, dim=3, mu_rep=1.0)
+    mask = np.ones((3, 3), bool)
+    val = np.diag([0.95, 1.0, 1.0])
+    params = oracle.Params()
+    st = oracle.init_state(3, n, om, mask, val, params)
+    st.F = st.F + 1e-4 * np.random.default_rng(0).standard_normal(st.F.shape)
+    sym = oracle.symbols(3, n, 0.5)
+    pol = oracle.RatioToDual(0.3)
+    for _ in range(args.warmup):
+        oracle.outer_iteration(3, n, 0.5, om, st, params, mask, val, pol, sym=sym)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.outer_iteration(3, n, 0.5, om, st, params, mask, val, pol, sym=sym)
+    dt = time.perf_counter() - t0
+    v = n ** 3 * args.steps / dt
+    sample = (f"oracle port (C local kernels + numpy FFT) of the same laminate workload at {n}^3, "
+              f"outer iterations {args.warmup + 1}..{args.warmup + args.steps}")
+    print(json.dumps({
+        "impl": "reference", "metric": "voxel-ADMM-iterations/sec (fp64)", "value": v,
+        "unit": "voxel-iter/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (config-2 laminate inputs, seeded)",
+        "config": {"workload": f"3D neo-Hookean laminate (SURVEY 8(d) config 2 inputs), CPU "
+                               f"sample at {n}^3", "grid": n},
+        "cpu_baseline": {"value": v, "unit": "voxel-iter/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "voxel-iter/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-n", type=int, default=128)
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else max(args.warmup, 1)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        if args.impl == "ours":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        tdist.init_process_group(backend=backend)
+        dist = tdist
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank)
+        else:
+            run_ours(args, rank, world, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

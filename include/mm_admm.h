@@ -1,0 +1,192 @@
+/*
+ * mm_admm.h — C-ABI of the B200-native ADMM outer iteration (arXiv 2010.06697).
+ *
+ * Drop-in boundary for the hot path of the reference package `micromech`
+ * (paths relative to /root/reference/pkg/src/micromech).  Every entry point
+ * names the reference interface it replaces.  Plain pointers, sizes and
+ * doubles only; host arrays are C-order float64 in the reference's own
+ * layout (grid axes first, tensor components innermost: "AoS"), borrowed for
+ * the duration of the call.  Device fields are owned by the context and
+ * kept component-major ("SoA") in HBM.
+ *
+ * Error convention (errors.py:21-69): every int-returning call returns one
+ * of the MM_* status codes below; mm_last_error() gives the message.
+ * Status -> Python exception mapping used by the host package:
+ *   MM_ERR_PARAM        -> ParameterError
+ *   MM_ERR_CONFIG       -> ConfigurationError
+ *   MM_ERR_INADMISSIBLE -> InadmissibleStateError
+ *   MM_ERR_DIVERGED     -> DivergenceError
+ *   MM_ERR_CUDA         -> RuntimeError (device / driver failure)
+ *
+ * Threading: one context per GPU, not re-entrant; all work is issued on the
+ * context's stream (solver.py runs a single orchestrating thread).
+ */
+#ifndef MM_ADMM_H
+#define MM_ADMM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MM_ABI_VERSION 1
+
+enum mm_status {
+    MM_OK = 0,
+    MM_ERR_PARAM = 1,
+    MM_ERR_CONFIG = 2,
+    MM_ERR_INADMISSIBLE = 3,
+    MM_ERR_DIVERGED = 4,
+    MM_ERR_CUDA = 5
+};
+
+/* Field identifiers for mm_upload / mm_download / mm_field_sums.
+ * "ncomp" is the number of doubles per grid point in the host AoS array. */
+enum mm_field {
+    MM_FIELD_F = 0,      /* ADMMState.F      grid+(d,d)  solver.py:112 */
+    MM_FIELD_G = 1,      /* ADMMState.grad_u grid+(d,d)  solver.py:111 */
+    MM_FIELD_LAM = 2,    /* ADMMState.lam    grid+(d,d)  solver.py:113 */
+    MM_FIELD_UT = 3,     /* ADMMState.u_tilde grid+(d,)  solver.py:110 */
+    MM_FIELD_PREV_F = 4, /* ADMMState.prev_F grid+(d,d)  solver.py:120 */
+    MM_FIELD_MOD_A = 5,  /* per-point modulus: mu (MR) or c (quadratic), (npts,) */
+    MM_FIELD_MOD_B = 6,  /* per-point modulus: kappa (MR), (npts,) */
+    MM_FIELD_ANG = 7,    /* LCE internal["angles"]  (npts,) 2D / (npts,2) 3D  lce.py:116-124 */
+    MM_FIELD_CHART = 8,  /* LCE internal["chart"]   (npts,3,3) 3D only */
+    MM_FIELD_PINC = 9,   /* LCE internal["p_inc"]   (npts,) */
+    MM_FIELD_N0 = 10,    /* LCE imprinted director n0 (npts,d)  lce.py:96 */
+    MM_FIELD_FF = 11,    /* LCE frozen Frank force (npts,d)      lce.py:223-229 */
+    MM_FIELD_PREV_ANG = 12,   /* prev_internal["angles"] */
+    MM_FIELD_PREV_CHART = 13, /* prev_internal["chart"] */
+    MM_FIELD_COUNT = 14
+};
+
+/* Materials for mm_local_sweeps. */
+enum mm_material {
+    MM_MAT_MR = 0,        /* MooneyRivlin, mooney_rivlin.py:56 */
+    MM_MAT_QUADRATIC = 1, /* QuadraticMaterial, quadratic.py:22 */
+    MM_MAT_LCE = 2,       /* LiquidCrystalElastomer, lce.py:73 */
+    MM_MAT_MR_DESCENT = 3 /* MooneyRivlin through the vectorised-descent algorithm in any
+                             dim (MooneyRivlin._sweeps_numpy, mooney_rivlin.py:126-162) */
+};
+
+typedef struct mm_ctx mm_ctx;
+
+/* Outcome of one metered batch (LocalStats, base.py:44-55) plus the sums the
+ * solver needs afterwards.  sum_F holds sum over points of F_ij (d*d, the
+ * numerator of mean_field(F), grid.py:266). */
+typedef struct {
+    int64_t sweeps;       /* LocalStats.sweeps (max over points) */
+    int64_t n_conv;       /* points counted as converged (converged_frac * npts) */
+    double sum_res2;      /* sum of res_pts^2 (solver.py:266 r_l numerator) */
+    double sum_F[9];
+} mm_local_stats;
+
+/* Solver tail: projection + r_d + multiplier ascent + r_p (solver.py:268-279). */
+typedef struct {
+    double sum_dG2;       /* sum |grad_u_new - grad_u_old|^2  (r_d, solver.py:271) */
+    double sum_mis2;      /* sum |grad_u_new - F|^2           (r_p, solver.py:278) */
+    double sum_lam[9];    /* sum of lam after the ascent (next mean_field(lam)) */
+} mm_update_stats;
+
+/* Pipeline stages for mm_profile_read (one outer iteration runs them in
+ * this order). */
+enum mm_stage {
+    MM_STAGE_LOCAL = 0,     /* local constitutive step (all chunks) */
+    MM_STAGE_ROW_FWD = 1,   /* divergence + R2C along the contiguous axis */
+    MM_STAGE_COL_FWD = 2,   /* FFT along axis 1 (3D) */
+    MM_STAGE_COL_SOLVE = 3, /* FFT + solve + inverse FFT along axis 0 */
+    MM_STAGE_COL_INV = 4,   /* inverse FFT along axis 1 (3D) */
+    MM_STAGE_ROW_INV = 5,   /* C2R along the contiguous axis -> u_tilde */
+    MM_STAGE_GRAD = 6,      /* gradient + multiplier ascent + residual sums */
+    MM_STAGE_FROZEN = 7,    /* LCE director + Frank stencil */
+    MM_STAGE_OTHER = 8,     /* transfers, sums, checks */
+    MM_NSTAGE = 9
+};
+
+typedef struct {
+    double ms[MM_NSTAGE];          /* device time per stage (CUDA events), since reset */
+    int64_t launches[MM_NSTAGE];   /* kernels launched per stage, since reset */
+} mm_profile;
+
+/* LCE scalar parameters (lce.py:78-107, 233-275). */
+typedef struct {
+    double mu, r1d, rr, alpha, gamma_inc, vis_F, vis_n, det_tol;
+    double phiF_scale, phin_scale, frank_kappa;
+} mm_lce_params;
+
+int mm_abi_version(void);
+
+/* Context = one periodic grid on one device (Grid, grid.py:55-122).
+ * dim in {2,3}, n >= 4, length > 0 (half edge L). */
+int mm_create(int dim, int n, double length, int device, mm_ctx **out);
+/* Point-set context for the pointwise operator alone (local_sweeps called on
+ * (npts, d, d) arrays that are not a grid, as in materials tests): only the
+ * per-point fields exist; projection calls fail with MM_ERR_CONFIG. */
+int mm_create_points(int dim, int64_t npts, int device, mm_ctx **out);
+void mm_destroy(mm_ctx *ctx);
+const char *mm_last_error(const mm_ctx *ctx);
+int mm_synchronize(mm_ctx *ctx);
+/* Bytes of device memory currently held by the context. */
+int64_t mm_device_bytes(const mm_ctx *ctx);
+
+/* Host AoS <-> device SoA.  count = number of doubles in the host array
+ * (npts * ncomp of the field); a mismatch is MM_ERR_CONFIG. */
+int mm_upload(mm_ctx *ctx, int field, const double *host, int64_t count);
+int mm_download(mm_ctx *ctx, int field, double *host, int64_t count);
+/* Device-to-device copy of a whole field (e.g. begin_time_step, solver.py:230-233). */
+int mm_copy_field(mm_ctx *ctx, int dst_field, int src_field);
+/* Per-component sums over all points (mean_field numerator, grid.py:266). */
+int mm_field_sums(mm_ctx *ctx, int field, double *out);
+
+/* Modified central-difference symbols (grid.py:161-184): per-axis tables of
+ * |g_j(m)|^2 = (sin(h xi_m)/h)^2 in FFT order, axis_tab[j*n + m], the last
+ * axis holding only m = 0..n/2; `threshold` = 1e-14 * max |g|^2 (the live
+ * mask of projection.py:155-157).  Tables are built on the host exactly as
+ * the reference builds them and uploaded once per grid. */
+int mm_set_symbols(mm_ctx *ctx, const double *axis_tab, double threshold);
+
+/* One metered batch of local sweeps, MaterialModel.local_sweeps
+ * (base.py:104-112): MR -> mooney_rivlin.py:108-124 (2D kernel :169-255,
+ * 3D descent :126-162 + base.py:124-230); quadratic -> quadratic.py:46-69;
+ * LCE -> lce.py:233-275 (2D :371-584, 3D :676-995).
+ * tol is absolute (point_tol * mu_rep).  phi_scale: MR/quadratic energy
+ * scale (max mu + max kappa, resp. max c).  want_points != 0 keeps per-point
+ * res / nsw / ok for mm_download_points.  F (and LCE internals) are updated
+ * in place on the device.  Returns MM_ERR_INADMISSIBLE when the 3D MR
+ * gradient meets det F <= 0 (base.py:116-121); F is then unchanged. */
+int mm_local_sweeps(mm_ctx *ctx, int material, double rho, double tol, int64_t max_sweeps,
+                    double phi_scale, int want_points, mm_local_stats *out);
+int mm_set_lce(mm_ctx *ctx, const mm_lce_params *p);
+int mm_download_points(mm_ctx *ctx, double *res, int64_t *nsw, uint8_t *ok, int64_t npts);
+
+/* LCE frozen data (lce.py:223-229): director from angles/chart, then the
+ * Frank force 2 kappa (D^T D) n as the exact radius-2 real-space stencil
+ * (equal to the reference's spectral form, lce.py:213-221). */
+int mm_prepare_frozen(mm_ctx *ctx);
+
+/* Helmholtz projection of (F, lam) (projection.py:132-168): writes
+ * u_tilde and grad_u = u_mean + D u_tilde on the device.  u_mean (d*d,
+ * from macro_gradient, projection.py:125-129) is supplied by the host. */
+int mm_project(mm_ctx *ctx, double rho, const double *u_mean);
+
+/* Fused solver tail (solver.py:268-279): projection, then one pass that
+ * forms grad_u_new, accumulates |dG|^2 for r_d, misfit^2 for r_p, applies
+ * lam += rho (grad_u_new - F) and sums lam for the next macro control. */
+int mm_project_update(mm_ctx *ctx, double rho, const double *u_mean, mm_update_stats *out);
+
+/* Stage profiling: when on, each stage is bracketed by CUDA events on the
+ * context stream; mm_profile_read returns accumulated device milliseconds and
+ * kernel-launch counts (launch counts are kept even when off). */
+int mm_profile_enable(mm_ctx *ctx, int on);
+int mm_profile_read(mm_ctx *ctx, mm_profile *out, int reset);
+
+/* Central-difference stencils on the grid fields (grid.py:227-249):
+ * op 0: grad_u = D u_tilde (discrete_grad);  op 1: u_tilde = div F
+ * (discrete_div).  Both equal the reference's spectral forms to roundoff. */
+int mm_stencil(mm_ctx *ctx, int op);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MM_ADMM_H */

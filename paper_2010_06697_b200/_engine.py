@@ -1,0 +1,87 @@
+"""Device engine: one libmm_admm grid context plus the bookkeeping that keeps
+an ADMMState's host views and its device-resident fields consistent.
+
+Ownership model: during solve() the fields live in HBM in SoA
+layout; ADMMState attributes materialise host numpy views on demand (D2H),
+and assigning (or reading, since the caller may mutate the returned array in
+place) marks the field for re-upload before the next device operation.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .grid import Grid, axis_symbol_tables
+
+# ADMMState attribute -> (device field id, rank of the per-point tensor)
+STATE_FIELDS = {
+    "F": (_lib.FIELD_F, 2),
+    "grad_u": (_lib.FIELD_G, 2),
+    "lam": (_lib.FIELD_LAM, 2),
+    "u_tilde": (_lib.FIELD_UT, 1),
+    "prev_F": (_lib.FIELD_PREV_F, 2),
+}
+
+
+class Engine:
+    """Device context for one grid (mm_create) with symbols uploaded."""
+
+    def __init__(self, grid: Grid, device=None):
+        self.grid = grid
+        self.ctx = _lib.Context(grid.dim, n=grid.n, length=grid.length, device=device)
+        tab, thresh = axis_symbol_tables(grid)
+        self.ctx.set_symbols(tab, thresh)
+        self.model = None          # model whose parameters are on the device
+        self.model_version = None
+        self.lam_sum = None        # device-side sum of lam (None: recompute)
+
+    def matches(self, grid: Grid) -> bool:
+        return self.grid == grid
+
+    def bind_model(self, model):
+        ver = getattr(model, "_device_version", 0)
+        if self.model is model and self.model_version == ver:
+            return
+        model._device_bind(self.ctx, self.grid.npoints)
+        self.model = model
+        self.model_version = ver
+
+    def lam_mean(self):
+        d = self.grid.dim
+        if self.lam_sum is None:
+            self.lam_sum = self.ctx.field_sums(_lib.FIELD_LAM, d * d)
+        return (self.lam_sum / self.grid.npoints).reshape(d, d)
+
+
+def field_shape(grid: Grid, rank: int):
+    return grid.shape + (grid.dim,) * rank
+
+
+_GRID_ENGINES = {}
+
+
+def scratch_engine(grid: Grid) -> Engine:
+    """A cached engine per grid for the stateless helpers (projection,
+    stencils) that take host arrays."""
+    eng = _GRID_ENGINES.get(grid)
+    if eng is None:
+        if len(_GRID_ENGINES) > 8:
+            _GRID_ENGINES.clear()
+        eng = Engine(grid)
+        _GRID_ENGINES[grid] = eng
+    return eng
+
+
+def device_discrete_grad(grid: Grid, u: np.ndarray) -> np.ndarray:
+    eng = scratch_engine(grid)
+    eng.ctx.upload(_lib.FIELD_UT, u)
+    eng.ctx.stencil(0)
+    return eng.ctx.download(_lib.FIELD_G, field_shape(grid, 2))
+
+
+def device_discrete_div(grid: Grid, T: np.ndarray) -> np.ndarray:
+    eng = scratch_engine(grid)
+    eng.ctx.upload(_lib.FIELD_F, T)
+    eng.ctx.stencil(1)
+    return eng.ctx.download(_lib.FIELD_UT, field_shape(grid, 1))

@@ -1,0 +1,258 @@
+"""ctypes binding of libmm_admm.so (include/mm_admm.h) and the device
+context wrapper used by the host package.
+
+There is no CPU fallback: if the extension is missing or no CUDA device is
+visible, every call that needs the device raises RuntimeError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .errors import (
+    ConfigurationError,
+    DivergenceError,
+    InadmissibleStateError,
+    ParameterError,
+)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libmm_admm.so")
+
+MM_OK, MM_ERR_PARAM, MM_ERR_CONFIG, MM_ERR_INADMISSIBLE, MM_ERR_DIVERGED, MM_ERR_CUDA = range(6)
+
+FIELD_F, FIELD_G, FIELD_LAM, FIELD_UT, FIELD_PREV_F, FIELD_MOD_A, FIELD_MOD_B = range(7)
+FIELD_ANG, FIELD_CHART, FIELD_PINC, FIELD_N0, FIELD_FF, FIELD_PREV_ANG, FIELD_PREV_CHART = range(7, 14)
+
+MAT_MR, MAT_QUADRATIC, MAT_LCE, MAT_MR_DESCENT = range(4)
+
+# every symbol include/mm_admm.h declares (checked by the CPU test suite)
+EXPORTS = (
+    "mm_abi_version", "mm_create", "mm_create_points", "mm_destroy", "mm_last_error",
+    "mm_synchronize", "mm_device_bytes", "mm_upload", "mm_download", "mm_copy_field",
+    "mm_field_sums", "mm_set_symbols", "mm_local_sweeps", "mm_set_lce", "mm_download_points",
+    "mm_prepare_frozen", "mm_project", "mm_project_update", "mm_stencil",
+    "mm_profile_enable", "mm_profile_read",
+)
+
+STAGES = ("local", "row_fwd", "col_fwd", "col_solve", "col_inv", "row_inv", "grad", "frozen",
+          "other")
+
+
+class LocalStatsC(ctypes.Structure):
+    _fields_ = [("sweeps", ctypes.c_int64), ("n_conv", ctypes.c_int64),
+                ("sum_res2", ctypes.c_double), ("sum_F", ctypes.c_double * 9)]
+
+
+class UpdateStatsC(ctypes.Structure):
+    _fields_ = [("sum_dG2", ctypes.c_double), ("sum_mis2", ctypes.c_double),
+                ("sum_lam", ctypes.c_double * 9)]
+
+
+class ProfileC(ctypes.Structure):
+    _fields_ = [("ms", ctypes.c_double * 9), ("launches", ctypes.c_int64 * 9)]
+
+
+class LCEParamsC(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_double) for name in
+                ("mu", "r1d", "rr", "alpha", "gamma_inc", "vis_F", "vis_n", "det_tol",
+                 "phiF_scale", "phin_scale", "frank_kappa")]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library():
+    """Load the CUDA extension (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"CUDA extension not built: {LIB_PATH} is missing "
+                "(run `python -m paper_2010_06697_b200.build`); there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        P, D, I64, I = ctypes.c_void_p, ctypes.c_double, ctypes.c_int64, ctypes.c_int
+        PP = ctypes.POINTER(ctypes.c_void_p)
+        sig = {
+            "mm_abi_version": ([], I),
+            "mm_create": ([I, I, D, I, PP], I),
+            "mm_create_points": ([I, I64, I, PP], I),
+            "mm_destroy": ([P], None),
+            "mm_last_error": ([P], ctypes.c_char_p),
+            "mm_synchronize": ([P], I),
+            "mm_device_bytes": ([P], I64),
+            "mm_upload": ([P, I, P, I64], I),
+            "mm_download": ([P, I, P, I64], I),
+            "mm_copy_field": ([P, I, I], I),
+            "mm_field_sums": ([P, I, P], I),
+            "mm_set_symbols": ([P, P, D], I),
+            "mm_local_sweeps": ([P, I, D, D, I64, D, I, ctypes.POINTER(LocalStatsC)], I),
+            "mm_set_lce": ([P, ctypes.POINTER(LCEParamsC)], I),
+            "mm_download_points": ([P, P, P, P, I64], I),
+            "mm_prepare_frozen": ([P], I),
+            "mm_project": ([P, D, P], I),
+            "mm_project_update": ([P, D, P, ctypes.POINTER(UpdateStatsC)], I),
+            "mm_stencil": ([P, I], I),
+            "mm_profile_enable": ([P, I], I),
+            "mm_profile_read": ([P, ctypes.POINTER(ProfileC), I], I),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+        return L
+
+
+_EXC = {
+    MM_ERR_PARAM: ParameterError,
+    MM_ERR_CONFIG: ConfigurationError,
+    MM_ERR_INADMISSIBLE: InadmissibleStateError,
+    MM_ERR_DIVERGED: DivergenceError,
+}
+
+
+def _ptr(a):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _require_device(device):
+    import torch  # noqa: PLC0415  (plumbing only: device discovery)
+    if not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device visible: the B200 path has no CPU fallback")
+    return int(device if device is not None else torch.cuda.current_device())
+
+
+class Context:
+    """One device context (mm_ctx): a periodic grid, or a bare point set."""
+
+    def __init__(self, dim, n=None, length=None, npts=None, device=None):
+        self.lib = load_library()
+        self.device = _require_device(device)
+        self.dim = int(dim)
+        h = ctypes.c_void_p()
+        if n is not None:
+            rc = self.lib.mm_create(self.dim, int(n), float(length), self.device, ctypes.byref(h))
+            self.npts = int(n) ** self.dim
+            self.n = int(n)
+        else:
+            rc = self.lib.mm_create_points(self.dim, int(npts), self.device, ctypes.byref(h))
+            self.npts = int(npts)
+            self.n = None
+        self.h = h
+        if rc != MM_OK:
+            msg = self.lib.mm_last_error(h).decode() if h.value else "context creation failed"
+            if h.value:
+                self.lib.mm_destroy(h)
+            self.h = None
+            self._raise(rc, msg)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value and _lib is not None:
+            try:
+                _lib.mm_destroy(h)
+            except Exception:
+                pass
+            self.h = None
+
+    def close(self):
+        self.__del__()
+
+    @staticmethod
+    def _raise(rc, msg):
+        exc = _EXC.get(rc)
+        if exc is None:
+            raise RuntimeError(f"libmm_admm: {msg}")
+        raise exc(msg)
+
+    def check(self, rc):
+        if rc != MM_OK:
+            self._raise(rc, self.lib.mm_last_error(self.h).decode())
+
+    # -- transfers -------------------------------------------------------
+    def upload(self, field, arr):
+        a = np.ascontiguousarray(arr, dtype=np.float64)
+        self.check(self.lib.mm_upload(self.h, field, _ptr(a), a.size))
+
+    def download(self, field, shape):
+        out = np.empty(shape, dtype=np.float64)
+        self.check(self.lib.mm_download(self.h, field, _ptr(out), out.size))
+        return out
+
+    def download_into(self, field, out):
+        assert out.flags.c_contiguous and out.dtype == np.float64
+        self.check(self.lib.mm_download(self.h, field, _ptr(out), out.size))
+        return out
+
+    def copy_field(self, dst, src):
+        self.check(self.lib.mm_copy_field(self.h, dst, src))
+
+    def field_sums(self, field, ncomp):
+        out = np.zeros(max(ncomp, 9))
+        self.check(self.lib.mm_field_sums(self.h, field, _ptr(out)))
+        return out[:ncomp].copy()
+
+    def synchronize(self):
+        self.check(self.lib.mm_synchronize(self.h))
+
+    def device_bytes(self):
+        return int(self.lib.mm_device_bytes(self.h))
+
+    # -- compute -----------------------------------------------------------
+    def set_symbols(self, axis_tab, threshold):
+        t = np.ascontiguousarray(axis_tab, dtype=np.float64)
+        self.check(self.lib.mm_set_symbols(self.h, _ptr(t), float(threshold)))
+
+    def local_sweeps(self, material, rho, tol, max_sweeps, phi_scale, want_points=False):
+        st = LocalStatsC()
+        self.check(self.lib.mm_local_sweeps(self.h, int(material), float(rho), float(tol),
+                                            int(max_sweeps), float(phi_scale),
+                                            1 if want_points else 0, ctypes.byref(st)))
+        return st
+
+    def download_points(self):
+        res = np.empty(self.npts)
+        nsw = np.empty(self.npts, dtype=np.int64)
+        ok = np.empty(self.npts, dtype=np.uint8)
+        self.check(self.lib.mm_download_points(self.h, _ptr(res), _ptr(nsw), _ptr(ok),
+                                               self.npts))
+        return res, nsw, ok.astype(bool)
+
+    def set_lce(self, **kw):
+        p = LCEParamsC(**kw)
+        self.check(self.lib.mm_set_lce(self.h, ctypes.byref(p)))
+
+    def prepare_frozen(self):
+        self.check(self.lib.mm_prepare_frozen(self.h))
+
+    def project(self, rho, u_mean):
+        um = np.ascontiguousarray(u_mean, dtype=np.float64).reshape(-1)
+        self.check(self.lib.mm_project(self.h, float(rho), _ptr(um)))
+
+    def project_update(self, rho, u_mean):
+        um = np.ascontiguousarray(u_mean, dtype=np.float64).reshape(-1)
+        st = UpdateStatsC()
+        self.check(self.lib.mm_project_update(self.h, float(rho), _ptr(um), ctypes.byref(st)))
+        return st
+
+    def stencil(self, op):
+        self.check(self.lib.mm_stencil(self.h, int(op)))
+
+    def profile_enable(self, on=True):
+        self.check(self.lib.mm_profile_enable(self.h, 1 if on else 0))
+
+    def profile_read(self, reset=False):
+        p = ProfileC()
+        self.check(self.lib.mm_profile_read(self.h, ctypes.byref(p), 1 if reset else 0))
+        return ({s: p.ms[i] for i, s in enumerate(STAGES)},
+                {s: int(p.launches[i]) for i, s in enumerate(STAGES)})

@@ -1,0 +1,544 @@
+// Context lifetime, host<->device transfers (AoS <-> SoA) and the C-ABI
+// entry points of libmm_admm (declared in include/mm_admm.h).
+#include <math.h>
+
+#include <algorithm>
+#include <stdarg.h>
+
+#include <vector>
+
+#include "mm_internal.cuh"
+
+int mm_fail(mm_ctx *ctx, int code, const char *fmt, ...) {
+    if (ctx) {
+        char buf[1024];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        ctx->err = buf;
+    }
+    return code;
+}
+
+int mm_alloc(mm_ctx *ctx, void **ptr, size_t bytes) {
+    if (bytes == 0) bytes = 8;
+    cudaError_t e = cudaMalloc(ptr, bytes);
+    if (e != cudaSuccess)
+        return mm_fail(ctx, MM_ERR_CUDA, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    ctx->bytes += (int64_t)bytes;
+    return MM_OK;
+}
+
+int mm_ensure_partials(mm_ctx *ctx, int64_t nblocks) {
+    if (nblocks <= ctx->partials_cap) return MM_OK;
+    if (ctx->partials) {
+        cudaFree(ctx->partials);
+        ctx->bytes -= ctx->partials_cap * MM_MAX_PARTIALS * (int64_t)sizeof(double);
+    }
+    ctx->partials = nullptr;
+    int rc = mm_alloc(ctx, (void **)&ctx->partials, sizeof(double) * MM_MAX_PARTIALS * nblocks);
+    if (rc) return rc;
+    ctx->partials_cap = nblocks;
+    return MM_OK;
+}
+
+int mm_fetch_reduction(mm_ctx *ctx, int K, double *out) {
+    MM_CUDA(ctx, cudaMemcpyAsync(ctx->host_out, ctx->red_out, sizeof(double) * K,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    memcpy(out, ctx->host_out, sizeof(double) * K);
+    mm_drain_timings(ctx);
+    return MM_OK;
+}
+
+static cudaEvent_t pool_get(mm_ctx *ctx) {
+    if (!ctx->event_pool.empty()) {
+        cudaEvent_t e = ctx->event_pool.back();
+        ctx->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void mm_stage_begin(mm_ctx *ctx, int stage, cudaEvent_t *ev) {
+    *ev = nullptr;
+    if (!ctx->prof_on) return;
+    *ev = pool_get(ctx);
+    cudaEventRecord(*ev, ctx->stream);
+}
+
+void mm_stage_end(mm_ctx *ctx, int stage, cudaEvent_t ev, int nlaunch) {
+    ctx->launches[stage] += nlaunch;
+    if (!ctx->prof_on || !ev) return;
+    cudaEvent_t b = pool_get(ctx);
+    cudaEventRecord(b, ctx->stream);
+    ctx->pending.push_back({stage, ev, b});
+    ctx->prof_launches[stage] += nlaunch;
+}
+
+void mm_drain_timings(mm_ctx *ctx) {
+    for (auto &p : ctx->pending) {
+        float ms = 0.f;
+        if (cudaEventSynchronize(p.b) == cudaSuccess && cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess)
+            ctx->prof_ms[p.stage] += ms;
+        ctx->event_pool.push_back(p.a);
+        ctx->event_pool.push_back(p.b);
+    }
+    ctx->pending.clear();
+}
+
+// ---------------------------------------------------------------------------
+// AoS <-> SoA
+// ---------------------------------------------------------------------------
+__global__ void k_aos_to_soa(const double *__restrict__ src, double *__restrict__ dst,
+                             int64_t p0, int64_t np, int ncomp, int64_t M) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t tot = np * ncomp;
+    for (; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t p = i / ncomp;
+        int c = (int)(i - p * ncomp);
+        dst[(int64_t)c * M + p0 + p] = src[i];
+    }
+}
+
+__global__ void k_soa_to_aos(const double *__restrict__ src, double *__restrict__ dst,
+                             int64_t p0, int64_t np, int ncomp, int64_t M) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t tot = np * ncomp;
+    for (; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t p = i / ncomp;
+        int c = (int)(i - p * ncomp);
+        dst[i] = src[(int64_t)c * M + p0 + p];
+    }
+}
+
+static int field_info(mm_ctx *ctx, int field, double ***slot, int *ncomp) {
+    const int d = ctx->dim, D = ctx->D;
+    switch (field) {
+        case MM_FIELD_F: *slot = &ctx->F; *ncomp = D; break;
+        case MM_FIELD_G: *slot = &ctx->G; *ncomp = D; break;
+        case MM_FIELD_LAM: *slot = &ctx->Lam; *ncomp = D; break;
+        case MM_FIELD_UT: *slot = &ctx->Ut; *ncomp = d; break;
+        case MM_FIELD_PREV_F: *slot = &ctx->prevF; *ncomp = D; break;
+        case MM_FIELD_MOD_A: *slot = &ctx->modA; *ncomp = 1; break;
+        case MM_FIELD_MOD_B: *slot = &ctx->modB; *ncomp = 1; break;
+        case MM_FIELD_ANG: *slot = &ctx->ang; *ncomp = d == 2 ? 1 : 2; break;
+        case MM_FIELD_CHART:
+            if (d != 3) return mm_fail(ctx, MM_ERR_CONFIG, "chart exists only in 3D");
+            *slot = &ctx->chart; *ncomp = 9; break;
+        case MM_FIELD_PINC: *slot = &ctx->pinc; *ncomp = 1; break;
+        case MM_FIELD_N0: *slot = &ctx->n0; *ncomp = d; break;
+        case MM_FIELD_FF: *slot = &ctx->ff; *ncomp = d; break;
+        case MM_FIELD_PREV_ANG: *slot = &ctx->prevAng; *ncomp = d == 2 ? 1 : 2; break;
+        case MM_FIELD_PREV_CHART:
+            if (d != 3) return mm_fail(ctx, MM_ERR_CONFIG, "chart exists only in 3D");
+            *slot = &ctx->prevChart; *ncomp = 9; break;
+        default: return mm_fail(ctx, MM_ERR_CONFIG, "unknown field id %d", field);
+    }
+    return MM_OK;
+}
+
+static int ensure_field(mm_ctx *ctx, double **slot, int ncomp) {
+    if (*slot) return MM_OK;
+    int rc = mm_alloc(ctx, (void **)slot, sizeof(double) * ncomp * ctx->M);
+    if (rc) return rc;
+    MM_CUDA(ctx, cudaMemsetAsync(*slot, 0, sizeof(double) * ncomp * ctx->M, ctx->stream));
+    return MM_OK;
+}
+
+static int ensure_stage(mm_ctx *ctx, int64_t ndoubles) {
+    if (ndoubles <= ctx->stage_cap) return MM_OK;
+    if (ctx->stage) {
+        cudaFree(ctx->stage);
+        ctx->bytes -= ctx->stage_cap * 8;
+    }
+    if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
+    ctx->stage = nullptr;
+    ctx->host_stage = nullptr;
+    int rc = mm_alloc(ctx, (void **)&ctx->stage, sizeof(double) * ndoubles);
+    if (rc) return rc;
+    MM_CUDA(ctx, cudaMallocHost((void **)&ctx->host_stage, sizeof(double) * ndoubles));
+    ctx->stage_cap = ndoubles;
+    ctx->host_stage_cap = ndoubles;
+    return MM_OK;
+}
+
+static bool is_pinned(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+static int transfer(mm_ctx *ctx, double *dev, int ncomp, const double *hsrc, double *hdst) {
+    const int64_t M = ctx->M;
+    const int64_t chunk_pts = std::max<int64_t>(1, std::min<int64_t>(M, (int64_t)(1 << 22)));
+    int rc = ensure_stage(ctx, chunk_pts * ncomp);
+    if (rc) return rc;
+    const bool pinned = is_pinned(hsrc ? (const void *)hsrc : (const void *)hdst);
+    for (int64_t p0 = 0; p0 < M; p0 += chunk_pts) {
+        int64_t np = std::min(chunk_pts, M - p0);
+        size_t bytes = sizeof(double) * np * ncomp;
+        int threads = 256;
+        int blocks = (int)std::min<int64_t>((np * ncomp + threads - 1) / threads, 148 * 32);
+        if (hsrc) {
+            const double *src = hsrc + p0 * ncomp;
+            if (!pinned) {
+                // pageable host memory: bounce through the pinned stage
+                memcpy(ctx->host_stage, src, bytes);
+                src = ctx->host_stage;
+            }
+            MM_CUDA(ctx, cudaMemcpyAsync(ctx->stage, src, bytes, cudaMemcpyHostToDevice,
+                                         ctx->stream));
+            k_aos_to_soa<<<blocks, threads, 0, ctx->stream>>>(ctx->stage, dev, p0, np, ncomp, M);
+            MM_LAUNCH_CHECK(ctx);
+            if (!pinned) MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        } else {
+            k_soa_to_aos<<<blocks, threads, 0, ctx->stream>>>(dev, ctx->stage, p0, np, ncomp, M);
+            MM_LAUNCH_CHECK(ctx);
+            double *dst = pinned ? hdst + p0 * ncomp : ctx->host_stage;
+            MM_CUDA(ctx, cudaMemcpyAsync(dst, ctx->stage, bytes, cudaMemcpyDeviceToHost,
+                                         ctx->stream));
+            MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+            if (!pinned) memcpy(hdst + p0 * ncomp, ctx->host_stage, bytes);
+        }
+    }
+    if (hsrc) MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return MM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// twiddles (long double on the host, rounded once)
+// ---------------------------------------------------------------------------
+static std::vector<double2> twiddle_table(int N) {
+    std::vector<double2> t(N > 0 ? N : 1);
+    for (int k = 0; k < N; ++k) {
+        long double a = -2.0L * 3.141592653589793238462643383279502884L * (long double)k / N;
+        t[k].x = (double)cosl(a);
+        t[k].y = (double)sinl(a);
+    }
+    return t;
+}
+
+static int upload_tw(mm_ctx *ctx, double2 **dst, int N) {
+    std::vector<double2> t = twiddle_table(N);
+    int rc = mm_alloc(ctx, (void **)dst, sizeof(double2) * t.size());
+    if (rc) return rc;
+    MM_CUDA(ctx, cudaMemcpy(*dst, t.data(), sizeof(double2) * t.size(), cudaMemcpyHostToDevice));
+    return MM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int mm_abi_version(void) { return MM_ABI_VERSION; }
+
+const char *mm_last_error(const mm_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t mm_device_bytes(const mm_ctx *ctx) { return ctx ? ctx->bytes : 0; }
+
+int mm_create(int dim, int n, double length, int device, mm_ctx **out) {
+    if (!out) return MM_ERR_PARAM;
+    *out = nullptr;
+    if (dim != 2 && dim != 3) return MM_ERR_CONFIG;
+    if (n < 4) return MM_ERR_CONFIG;
+    if (!(length > 0.0)) return MM_ERR_CONFIG;
+    mm_ctx *ctx = new mm_ctx();
+    ctx->dim = dim;
+    ctx->n = n;
+    ctx->L = length;
+    ctx->h = 2.0 * length / n;  // grid.py:84-86
+    ctx->M = 1;
+    for (int i = 0; i < dim; ++i) ctx->M *= n;
+    ctx->D = dim * dim;
+    ctx->nh = n / 2 + 1;
+    ctx->P = (ctx->nh + 7) / 8 * 8;
+    ctx->nrows = ctx->M / n;
+    ctx->device = device;
+    *out = ctx;
+    int rc;
+#define TRY(x)                 \
+    do {                       \
+        rc = (x);              \
+        if (rc) return rc;     \
+    } while (0)
+    MM_CUDA(ctx, cudaSetDevice(device));
+    MM_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    const int64_t M = ctx->M;
+    TRY(mm_alloc(ctx, (void **)&ctx->F, sizeof(double) * ctx->D * M));
+    TRY(mm_alloc(ctx, (void **)&ctx->G, sizeof(double) * ctx->D * M));
+    TRY(mm_alloc(ctx, (void **)&ctx->Lam, sizeof(double) * ctx->D * M));
+    TRY(mm_alloc(ctx, (void **)&ctx->Ut, sizeof(double) * dim * M));
+    TRY(mm_alloc(ctx, (void **)&ctx->spec, sizeof(double2) * dim * ctx->nrows * ctx->P));
+    TRY(mm_alloc(ctx, (void **)&ctx->sym, sizeof(double) * dim * n));
+    TRY(mm_alloc(ctx, (void **)&ctx->red_out, sizeof(double) * MM_MAX_PARTIALS));
+    TRY(mm_alloc(ctx, (void **)&ctx->red_count, sizeof(unsigned int) * 4));
+    MM_CUDA(ctx, cudaMemset(ctx->red_count, 0, sizeof(unsigned int) * 4));
+    MM_CUDA(ctx, cudaMallocHost((void **)&ctx->host_out, sizeof(double) * MM_MAX_PARTIALS));
+    MM_CUDA(ctx, cudaMemsetAsync(ctx->F, 0, sizeof(double) * ctx->D * M, ctx->stream));
+    MM_CUDA(ctx, cudaMemsetAsync(ctx->G, 0, sizeof(double) * ctx->D * M, ctx->stream));
+    MM_CUDA(ctx, cudaMemsetAsync(ctx->Lam, 0, sizeof(double) * ctx->D * M, ctx->stream));
+    MM_CUDA(ctx, cudaMemsetAsync(ctx->Ut, 0, sizeof(double) * dim * M, ctx->stream));
+    MM_CUDA(ctx, cudaMemsetAsync(ctx->spec, 0, sizeof(double2) * dim * ctx->nrows * ctx->P,
+                                 ctx->stream));
+    TRY(upload_tw(ctx, &ctx->tw_full, n));
+    TRY(upload_tw(ctx, &ctx->tw_half, n / 2));
+    TRY(upload_tw(ctx, &ctx->tw_r2c, n));
+    TRY(mm_ensure_partials(ctx, 4096));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+#undef TRY
+    return MM_OK;
+}
+
+int mm_create_points(int dim, int64_t npts, int device, mm_ctx **out) {
+    if (!out) return MM_ERR_PARAM;
+    *out = nullptr;
+    if (dim != 2 && dim != 3) return MM_ERR_CONFIG;
+    if (npts < 0) return MM_ERR_CONFIG;
+    mm_ctx *ctx = new mm_ctx();
+    ctx->dim = dim;
+    ctx->n = 0;
+    ctx->M = npts;
+    ctx->D = dim * dim;
+    ctx->device = device;
+    ctx->points_only = true;
+    *out = ctx;
+    int rc;
+    MM_CUDA(ctx, cudaSetDevice(device));
+    MM_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    const int64_t M = npts > 0 ? npts : 1;
+    if ((rc = mm_alloc(ctx, (void **)&ctx->F, sizeof(double) * ctx->D * M))) return rc;
+    if ((rc = mm_alloc(ctx, (void **)&ctx->G, sizeof(double) * ctx->D * M))) return rc;
+    if ((rc = mm_alloc(ctx, (void **)&ctx->Lam, sizeof(double) * ctx->D * M))) return rc;
+    if ((rc = mm_alloc(ctx, (void **)&ctx->red_out, sizeof(double) * MM_MAX_PARTIALS))) return rc;
+    if ((rc = mm_alloc(ctx, (void **)&ctx->red_count, sizeof(unsigned int) * 4))) return rc;
+    MM_CUDA(ctx, cudaMemset(ctx->red_count, 0, sizeof(unsigned int) * 4));
+    MM_CUDA(ctx, cudaMallocHost((void **)&ctx->host_out, sizeof(double) * MM_MAX_PARTIALS));
+    if ((rc = mm_ensure_partials(ctx, 4096))) return rc;
+    return MM_OK;
+}
+
+void mm_destroy(mm_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    mm_drain_timings(ctx);
+    for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+    double *ptrs[] = {ctx->F, ctx->G, ctx->Lam, ctx->Ut, ctx->prevF, ctx->modA, ctx->modB,
+                      ctx->ang, ctx->chart, ctx->pinc, ctx->n0, ctx->ff, ctx->prevAng,
+                      ctx->prevChart, ctx->nk, ctx->sym, ctx->partials, ctx->red_out,
+                      ctx->res, ctx->tstate, ctx->stage};
+    for (double *p : ptrs)
+        if (p) cudaFree(p);
+    if (ctx->spec) cudaFree(ctx->spec);
+    if (ctx->tw_full) cudaFree(ctx->tw_full);
+    if (ctx->tw_half) cudaFree(ctx->tw_half);
+    if (ctx->tw_r2c) cudaFree(ctx->tw_r2c);
+    if (ctx->red_count) cudaFree(ctx->red_count);
+    if (ctx->nsw) cudaFree(ctx->nsw);
+    if (ctx->ok) cudaFree(ctx->ok);
+    if (ctx->freestate) cudaFree(ctx->freestate);
+    if (ctx->host_out) cudaFreeHost(ctx->host_out);
+    if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int mm_synchronize(mm_ctx *ctx) {
+    if (!ctx) return MM_ERR_PARAM;
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    mm_drain_timings(ctx);
+    return MM_OK;
+}
+
+int mm_profile_enable(mm_ctx *ctx, int on) {
+    if (!ctx) return MM_ERR_PARAM;
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    mm_drain_timings(ctx);
+    ctx->prof_on = on != 0;
+    return MM_OK;
+}
+
+int mm_profile_read(mm_ctx *ctx, mm_profile *out, int reset) {
+    if (!ctx || !out) return MM_ERR_PARAM;
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    mm_drain_timings(ctx);
+    for (int i = 0; i < MM_NSTAGE; ++i) {
+        out->ms[i] = ctx->prof_ms[i];
+        out->launches[i] = ctx->launches[i];
+        if (reset) {
+            ctx->prof_ms[i] = 0.0;
+            ctx->launches[i] = 0;
+            ctx->prof_launches[i] = 0;
+        }
+    }
+    return MM_OK;
+}
+
+int mm_upload(mm_ctx *ctx, int field, const double *host, int64_t count) {
+    if (!ctx || !host) return MM_ERR_PARAM;
+    double **slot;
+    int ncomp;
+    int rc = field_info(ctx, field, &slot, &ncomp);
+    if (rc) return rc;
+    if (count != ctx->M * ncomp)
+        return mm_fail(ctx, MM_ERR_CONFIG, "field %d: got %lld doubles, expected %lld", field,
+                       (long long)count, (long long)(ctx->M * ncomp));
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    rc = ensure_field(ctx, slot, ncomp);
+    if (rc) return rc;
+    if (field == MM_FIELD_F) ctx->F_checked = false;
+    if (field == MM_FIELD_PREV_F) ctx->have_prev_F = true;
+    if (field == MM_FIELD_PREV_ANG) ctx->have_prev_int = true;
+    return transfer(ctx, *slot, ncomp, host, nullptr);
+}
+
+int mm_download(mm_ctx *ctx, int field, double *host, int64_t count) {
+    if (!ctx || !host) return MM_ERR_PARAM;
+    double **slot;
+    int ncomp;
+    int rc = field_info(ctx, field, &slot, &ncomp);
+    if (rc) return rc;
+    if (count != ctx->M * ncomp)
+        return mm_fail(ctx, MM_ERR_CONFIG, "field %d: got %lld doubles, expected %lld", field,
+                       (long long)count, (long long)(ctx->M * ncomp));
+    if (!*slot) return mm_fail(ctx, MM_ERR_CONFIG, "field %d was never set", field);
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    return transfer(ctx, *slot, ncomp, nullptr, host);
+}
+
+int mm_copy_field(mm_ctx *ctx, int dst_field, int src_field) {
+    if (!ctx) return MM_ERR_PARAM;
+    double **ds, **ss;
+    int nd, ns;
+    int rc = field_info(ctx, dst_field, &ds, &nd);
+    if (rc) return rc;
+    rc = field_info(ctx, src_field, &ss, &ns);
+    if (rc) return rc;
+    if (nd != ns) return mm_fail(ctx, MM_ERR_CONFIG, "field shapes differ");
+    if (!*ss) return mm_fail(ctx, MM_ERR_CONFIG, "source field %d was never set", src_field);
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    rc = ensure_field(ctx, ds, nd);
+    if (rc) return rc;
+    MM_CUDA(ctx, cudaMemcpyAsync(*ds, *ss, sizeof(double) * nd * ctx->M,
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+    if (dst_field == MM_FIELD_PREV_F) ctx->have_prev_F = true;
+    if (dst_field == MM_FIELD_PREV_ANG) ctx->have_prev_int = true;
+    if (dst_field == MM_FIELD_F) ctx->F_checked = false;
+    return MM_OK;
+}
+
+int mm_field_sums(mm_ctx *ctx, int field, double *out) {
+    if (!ctx || !out) return MM_ERR_PARAM;
+    double **slot;
+    int ncomp;
+    int rc = field_info(ctx, field, &slot, &ncomp);
+    if (rc) return rc;
+    if (!*slot) return mm_fail(ctx, MM_ERR_CONFIG, "field %d was never set", field);
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    return mm_run_field_sums(ctx, *slot, ncomp, out);
+}
+
+int mm_set_symbols(mm_ctx *ctx, const double *axis_tab, double threshold) {
+    if (!ctx || !axis_tab) return MM_ERR_PARAM;
+    if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    MM_CUDA(ctx, cudaMemcpy(ctx->sym, axis_tab, sizeof(double) * ctx->dim * ctx->n,
+                            cudaMemcpyHostToDevice));
+    ctx->sym_thresh = threshold;
+    ctx->have_sym = true;
+    return MM_OK;
+}
+
+int mm_set_lce(mm_ctx *ctx, const mm_lce_params *p) {
+    if (!ctx || !p) return MM_ERR_PARAM;
+    ctx->lce = *p;
+    ctx->have_lce = true;
+    return MM_OK;
+}
+
+int mm_local_sweeps(mm_ctx *ctx, int material, double rho, double tol, int64_t max_sweeps,
+                    double phi_scale, int want_points, mm_local_stats *out) {
+    if (!ctx || !out) return MM_ERR_PARAM;
+    if (!(rho > 0.0) || !isfinite(rho))
+        return mm_fail(ctx, MM_ERR_PARAM, "rho must be positive and finite, got %g", rho);
+    if (max_sweeps < 0) return mm_fail(ctx, MM_ERR_PARAM, "max_sweeps must be >= 0");
+    if ((material == MM_MAT_MR || material == MM_MAT_QUADRATIC) && !ctx->modA)
+        return mm_fail(ctx, MM_ERR_CONFIG, "material moduli were never uploaded");
+    if (material == MM_MAT_MR && !ctx->modB)
+        return mm_fail(ctx, MM_ERR_CONFIG, "kappa was never uploaded");
+    if (material == MM_MAT_LCE && !ctx->have_lce)
+        return mm_fail(ctx, MM_ERR_CONFIG, "LCE parameters were never set");
+    if (material < 0 || material > 3) return mm_fail(ctx, MM_ERR_CONFIG, "unknown material");
+    if (material == MM_MAT_MR_DESCENT && (!ctx->modA || !ctx->modB))
+        return mm_fail(ctx, MM_ERR_CONFIG, "material moduli were never uploaded");
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    return mm_run_local(ctx, material, rho, tol, max_sweeps, phi_scale, want_points, out);
+}
+
+int mm_download_points(mm_ctx *ctx, double *res, int64_t *nsw, uint8_t *ok, int64_t npts) {
+    if (!ctx) return MM_ERR_PARAM;
+    if (npts != ctx->M) return mm_fail(ctx, MM_ERR_CONFIG, "npts mismatch");
+    if (!ctx->res) return mm_fail(ctx, MM_ERR_CONFIG, "no per-point results kept");
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    if (res)
+        MM_CUDA(ctx, cudaMemcpyAsync(res, ctx->res, sizeof(double) * npts, cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+    std::vector<int32_t> tmp;
+    if (nsw) {
+        tmp.resize(npts);
+        MM_CUDA(ctx, cudaMemcpyAsync(tmp.data(), ctx->nsw, sizeof(int32_t) * npts,
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    if (ok)
+        MM_CUDA(ctx, cudaMemcpyAsync(ok, ctx->ok, npts, cudaMemcpyDeviceToHost, ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (nsw)
+        for (int64_t i = 0; i < npts; ++i) nsw[i] = tmp[i];
+    return MM_OK;
+}
+
+int mm_prepare_frozen(mm_ctx *ctx) {
+    if (!ctx) return MM_ERR_PARAM;
+    if (!ctx->have_lce) return mm_fail(ctx, MM_ERR_CONFIG, "LCE parameters were never set");
+    if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    return mm_run_frozen(ctx);
+}
+
+int mm_project(mm_ctx *ctx, double rho, const double *u_mean) {
+    if (!ctx || !u_mean) return MM_ERR_PARAM;
+    if (!(rho > 0.0) || !isfinite(rho))
+        return mm_fail(ctx, MM_ERR_PARAM, "rho must be positive and finite, got %g", rho);
+    if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
+    if (!ctx->have_sym) return mm_fail(ctx, MM_ERR_CONFIG, "symbols were never set");
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    return mm_run_project(ctx, rho, u_mean, 0, nullptr);
+}
+
+int mm_project_update(mm_ctx *ctx, double rho, const double *u_mean, mm_update_stats *out) {
+    if (!ctx || !u_mean || !out) return MM_ERR_PARAM;
+    if (!(rho > 0.0) || !isfinite(rho))
+        return mm_fail(ctx, MM_ERR_PARAM, "rho must be positive and finite, got %g", rho);
+    if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
+    if (!ctx->have_sym) return mm_fail(ctx, MM_ERR_CONFIG, "symbols were never set");
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    return mm_run_project(ctx, rho, u_mean, 1, out);
+}
+
+int mm_stencil(mm_ctx *ctx, int op) {
+    if (!ctx) return MM_ERR_PARAM;
+    if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
+    if (op != 0 && op != 1) return mm_fail(ctx, MM_ERR_PARAM, "unknown stencil op %d", op);
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    return mm_run_stencil(ctx, op);
+}
+
+}  // extern "C"

@@ -1,0 +1,209 @@
+// Internal definitions shared by the CUDA translation units of libmm_admm.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/mm_admm.h"
+
+#define MM_MAX_PARTIALS 16  // doubles reduced per block by any kernel
+
+struct mm_ctx {
+    int dim = 0, n = 0;
+    double L = 0.0, h = 0.0;
+    int64_t M = 0;       // grid points n^dim
+    int D = 0;           // tensor components dim*dim
+    int nh = 0;          // n/2 + 1 (half-spectrum length, last axis)
+    int P = 0;           // spectral row pitch (complex), multiple of 8
+    int64_t nrows = 0;   // M / n rows along the contiguous axis
+    int device = 0;
+    cudaStream_t stream = nullptr;
+
+    // device fields, SoA (component-major): comp c of point p at c*M + p
+    double *F = nullptr, *G = nullptr, *Lam = nullptr, *Ut = nullptr, *prevF = nullptr;
+    double *modA = nullptr, *modB = nullptr;
+    // LCE internal / frozen
+    double *ang = nullptr, *chart = nullptr, *pinc = nullptr, *n0 = nullptr, *ff = nullptr;
+    double *prevAng = nullptr, *prevChart = nullptr, *nk = nullptr;
+    bool have_prev_F = false, have_prev_int = false;
+    mm_lce_params lce{};
+    bool have_lce = false;
+    // spectral workspace: dim comps x nrows x P complex
+    double2 *spec = nullptr;
+    // symbols
+    double *sym = nullptr;   // dim * n
+    double sym_thresh = 0.0;
+    bool have_sym = false;
+    // twiddles: tw_half (N = n/2 complex FFT of the packed real rows),
+    // tw_full (N = n), tw_r2c (W_n^k, k < n/2 + 1)
+    double2 *tw_full = nullptr, *tw_half = nullptr, *tw_r2c = nullptr;
+    // reductions
+    double *partials = nullptr;  // [max_blocks][MM_MAX_PARTIALS]
+    int64_t partials_cap = 0;
+    double *red_out = nullptr;   // MM_MAX_PARTIALS results
+    unsigned int *red_count = nullptr;
+    double *host_out = nullptr;  // pinned MM_MAX_PARTIALS
+    // per-point local outputs / persistent descent state
+    double *res = nullptr;
+    int32_t *nsw = nullptr;
+    uint8_t *ok = nullptr;
+    double *tstate = nullptr;
+    uint8_t *freestate = nullptr;
+    // staging for AoS <-> SoA
+    double *stage = nullptr;
+    int64_t stage_cap = 0;     // doubles
+    double *host_stage = nullptr;  // pinned
+    int64_t host_stage_cap = 0;
+    // stage profiling (CUDA events on ctx->stream) and launch counting
+    bool prof_on = false;
+    double prof_ms[MM_NSTAGE] = {0};
+    int64_t prof_launches[MM_NSTAGE] = {0};
+    int64_t launches[MM_NSTAGE] = {0};
+    struct PendingTiming {
+        int stage;
+        cudaEvent_t a, b;
+    };
+    std::vector<PendingTiming> pending;
+    std::vector<cudaEvent_t> event_pool;
+    bool F_checked = false;
+    bool points_only = false;    // F verified admissible since the last upload
+    int64_t bytes = 0;
+    std::string err;
+};
+
+// set error + return code
+int mm_fail(mm_ctx *ctx, int code, const char *fmt, ...);
+
+#define MM_CUDA(ctx, call)                                                                 \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return mm_fail((ctx), MM_ERR_CUDA, "%s failed: %s (%s:%d)", #call,             \
+                           cudaGetErrorString(e_), __FILE__, __LINE__);                    \
+    } while (0)
+
+#define MM_LAUNCH_CHECK(ctx)                                                               \
+    do {                                                                                   \
+        cudaError_t e_ = cudaGetLastError();                                               \
+        if (e_ != cudaSuccess)                                                             \
+            return mm_fail((ctx), MM_ERR_CUDA, "kernel launch failed: %s (%s:%d)",         \
+                           cudaGetErrorString(e_), __FILE__, __LINE__);                    \
+    } while (0)
+
+int mm_alloc(mm_ctx *ctx, void **ptr, size_t bytes);
+int mm_ensure_partials(mm_ctx *ctx, int64_t nblocks);
+// copy the finalized reduction results (K doubles) back to host
+int mm_fetch_reduction(mm_ctx *ctx, int K, double *out);
+
+// ---------------------------------------------------------------------------
+// deterministic block reductions
+// ---------------------------------------------------------------------------
+// Kinds of per-slot combination.
+enum { RED_SUM = 0, RED_MAX = 1 };
+
+__device__ __forceinline__ double red_op(int op, double a, double b) {
+    return op == RED_MAX ? fmax(a, b) : a + b;
+}
+
+// Reduce K per-thread values over the block in a fixed order (xor-shuffle
+// tree inside warps, then warps in index order); thread 0 gets the result.
+// smem: >= 32 * K doubles.
+template <int K>
+__device__ __forceinline__ void block_reduce(double (&vals)[K], const int (&ops)[K],
+                                             double *smem) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double v = vals[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = red_op(ops[k], v, __shfl_xor_sync(0xffffffffu, v, o));
+        vals[k] = v;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+    __syncthreads();
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) smem[warp * K + k] = vals[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double s = smem[k];
+            for (int w = 1; w < nw; ++w) s = red_op(ops[k], s, smem[w * K + k]);
+            vals[k] = s;
+        }
+    }
+    __syncthreads();
+}
+
+// Write this block's partial (thread 0's vals, already block-reduced) and let
+// the last block to finish reduce all partials.  Each thread of the last block
+// folds a contiguous range of blocks in order, then block_reduce combines the
+// threads in a fixed order => deterministic run to run.
+template <int K>
+__device__ void grid_finalize(const double (&vals)[K], const int (&ops)[K], double *partials,
+                              double *out, unsigned int *count, double *smem) {
+    __shared__ bool is_last;
+    const int nb = gridDim.x * gridDim.y * gridDim.z;
+    const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) partials[(int64_t)bid * K + k] = vals[k];
+        __threadfence();
+        unsigned int t = atomicAdd(count, 1u);
+        is_last = (t == (unsigned int)(nb - 1));
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    const int nt = blockDim.x;
+    const int per = (nb + nt - 1) / nt;
+    double acc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = ops[k] == RED_MAX ? -1e308 : 0.0;
+    const int b0 = threadIdx.x * per;
+    const int b1 = min(nb, b0 + per);
+    for (int b = b0; b < b1; ++b) {
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            acc[k] = red_op(ops[k], acc[k], ((volatile double *)partials)[(int64_t)b * K + k]);
+    }
+    block_reduce<K>(acc, ops, smem);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) out[k] = acc[k];
+        *count = 0u;
+    }
+}
+
+// stage timing: brackets the kernel launches of one pipeline stage with CUDA
+// events on the context stream when profiling is on, and counts launches.
+void mm_stage_begin(mm_ctx *ctx, int stage, cudaEvent_t *ev);
+void mm_stage_end(mm_ctx *ctx, int stage, cudaEvent_t ev, int nlaunch);
+void mm_drain_timings(mm_ctx *ctx);
+struct StageScope {
+    mm_ctx *ctx;
+    int stage;
+    int nlaunch;
+    cudaEvent_t ev = nullptr;
+    StageScope(mm_ctx *c, int s, int n = 1) : ctx(c), stage(s), nlaunch(n) {
+        mm_stage_begin(ctx, stage, &ev);
+    }
+    ~StageScope() { mm_stage_end(ctx, stage, ev, nlaunch); }
+};
+
+// launch helpers implemented per translation unit
+int mm_run_local(mm_ctx *ctx, int material, double rho, double tol, int64_t max_sweeps,
+                 double phi_scale, int want_points, mm_local_stats *out);
+int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
+                   mm_update_stats *out);
+int mm_run_frozen(mm_ctx *ctx);
+int mm_run_field_sums(mm_ctx *ctx, const double *field, int ncomp, double *out);
+int mm_check_det(mm_ctx *ctx, int *bad);
+int mm_run_stencil(mm_ctx *ctx, int op);

@@ -1,0 +1,583 @@
+// Local (per-voxel) constitutive step for the Mooney-Rivlin and quadratic
+// materials: ADMM step 1 of solver.py:252-265.
+//
+// One thread per voxel, fields SoA in HBM (coalesced 8-byte loads per
+// component), all per-point state in registers.  Two algorithms, each a
+// faithful restatement of the reference's:
+//   * k_mr2d      — the compiled 2D kernel, mooney_rivlin.py:169-255
+//   * k_descent   — the vectorised numpy descent used by 3D Mooney-Rivlin
+//                   (mooney_rivlin.py:126-162) and the quadratic material
+//                   (quadratic.py:46-69), base.py:124-230.  Its only
+//                   cross-point coupling (the stall guard every 32 sweeps,
+//                   base.py:224-229) is honoured by running the sweep loop in
+//                   32-sweep segments with a host check in between, and only
+//                   when the call may exceed 64 sweeps (below that the guard
+//                   cannot fire).
+// Each launch ends with a deterministic block + grid reduction of the batch
+// statistics (sum res^2, converged count, max sweeps, guard sum, sum F).
+#include <math.h>
+
+#include <algorithm>
+
+#include "mm_internal.cuh"
+
+namespace {
+
+constexpr double BT_DECREASE = 1e-4;  // base.py:37
+constexpr double BT_SHRINK = 0.5;     // base.py:38
+constexpr int MAX_BT = 60;            // base.py:39
+constexpr double MEAS_EPS = 64.0 * 2.220446049250313e-16;  // base.py:41
+
+constexpr int LOCAL_THREADS = 128;
+#ifndef LOCAL_MIN_BLOCKS
+#define LOCAL_MIN_BLOCKS 4
+#endif
+
+inline int local_blocks(int64_t M) {
+    int64_t b = (M + LOCAL_THREADS - 1) / LOCAL_THREADS;
+    return (int)std::min<int64_t>(b, 148 * 16);
+}
+
+// ---------------------------------------------------------------------------
+// 2D compiled kernel (mooney_rivlin.py:169-255)
+// slots: 0 sum res^2, 1 n_conv, 2 max nsw, 3..6 sum F
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(LOCAL_THREADS)
+k_mr2d(double *__restrict__ F, const double *__restrict__ G, const double *__restrict__ Lam,
+       const double *__restrict__ mu, const double *__restrict__ kap, int64_t M, double rho,
+       double tol, int64_t max_sweeps, double phi_scale, double *__restrict__ res_out,
+       int32_t *__restrict__ nsw_out, double *partials, double *red_out, unsigned int *count) {
+    __shared__ double smem[32 * 7];
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        double a = F[p], b = F[M + p], c = F[2 * M + p], d = F[3 * M + p];
+        const double g00 = G[p], g01 = G[M + p], g10 = G[2 * M + p], g11 = G[3 * M + p];
+        const double l00 = Lam[p], l01 = Lam[M + p], l10 = Lam[2 * M + p], l11 = Lam[3 * M + p];
+        const double m = mu[p], k = kap[p];
+        double t = 1.0 / (rho + m + 4.0 * k);
+        const double tmax = 16.0 * t;
+        bool freemode = false;
+        double res_prev = 1e300, res = 0.0;
+        int64_t nsw = 0;
+        for (int64_t it = 0; it < max_sweeps + 1; ++it) {
+            const double J = a * d - b * c;
+            const double iJ = 1.0 / J;
+            const double jm1 = J - 1.0;
+            const double s00 = m * (a - d * iJ) + k * jm1 * d;
+            const double s01 = m * (b + c * iJ) - k * jm1 * c;
+            const double s10 = m * (c + b * iJ) - k * jm1 * b;
+            const double s11 = m * (d - a * iJ) + k * jm1 * a;
+            const double r00 = s00 - l00 - rho * (g00 - a);
+            const double r01 = s01 - l01 - rho * (g01 - b);
+            const double r10 = s10 - l10 - rho * (g10 - c);
+            const double r11 = s11 - l11 - rho * (g11 - d);
+            const double gsq = r00 * r00 + r01 * r01 + r10 * r10 + r11 * r11;
+            res = sqrt(gsq);
+            if (freemode) {
+                if (res > res_prev) t *= BT_SHRINK;
+                else t = fmin(t * 1.3, tmax);
+                res_prev = res;
+            }
+            if (res < tol || nsw >= max_sweeps) break;
+            nsw += 1;
+            bool did = false;
+            if (!freemode) {
+                const double W = 0.5 * m * (a * a + b * b + c * c + d * d - 2.0 * log(J) - 2.0) +
+                                 0.5 * k * jm1 * jm1;
+                const double phi0 =
+                    W - (l00 * a + l01 * b + l10 * c + l11 * d) +
+                    0.5 * rho * ((g00 - a) * (g00 - a) + (g01 - b) * (g01 - b) +
+                                 (g10 - c) * (g10 - c) + (g11 - d) * (g11 - d));
+                if (BT_DECREASE * t * gsq <= MEAS_EPS * (fabs(phi0) + phi_scale)) {
+                    freemode = true;
+                    res_prev = res;
+                } else {
+                    const double t_in = t;
+                    for (int bt = 0; bt < MAX_BT; ++bt) {
+                        const double a2 = a - t * r00, b2 = b - t * r01;
+                        const double c2 = c - t * r10, d2 = d - t * r11;
+                        const double J2 = a2 * d2 - b2 * c2;
+                        if (J2 > 1e-12) {
+                            const double jm2 = J2 - 1.0;
+                            const double W2 =
+                                0.5 * m * (a2 * a2 + b2 * b2 + c2 * c2 + d2 * d2 - 2.0 * log(J2) - 2.0) +
+                                0.5 * k * jm2 * jm2;
+                            const double phi2 =
+                                W2 - (l00 * a2 + l01 * b2 + l10 * c2 + l11 * d2) +
+                                0.5 * rho * ((g00 - a2) * (g00 - a2) + (g01 - b2) * (g01 - b2) +
+                                             (g10 - c2) * (g10 - c2) + (g11 - d2) * (g11 - d2));
+                            if (phi2 <= phi0 - BT_DECREASE * t * gsq) {
+                                a = a2; b = b2; c = c2; d = d2;
+                                did = true;
+                                break;
+                            }
+                        }
+                        t *= BT_SHRINK;
+                    }
+                    if (did) {
+                        t = fmin(t * 1.6, tmax);
+                    } else {
+                        freemode = true;
+                        t = t_in;
+                        res_prev = res;
+                    }
+                }
+            }
+            if (freemode && !did) {
+                for (int bt = 0; bt < 12; ++bt) {
+                    const double a2 = a - t * r00, b2 = b - t * r01;
+                    const double c2 = c - t * r10, d2 = d - t * r11;
+                    if (a2 * d2 - b2 * c2 > 1e-12) {
+                        a = a2; b = b2; c = c2; d = d2;
+                        break;
+                    }
+                    t *= BT_SHRINK;
+                }
+            }
+        }
+        F[p] = a; F[M + p] = b; F[2 * M + p] = c; F[3 * M + p] = d;
+        if (res_out) res_out[p] = res;
+        if (nsw_out) nsw_out[p] = (int32_t)nsw;
+        acc[0] += res * res;
+        acc[1] += (res < tol) ? 1.0 : 0.0;
+        acc[2] = fmax(acc[2], (double)nsw);
+        acc[3] += a; acc[4] += b; acc[5] += c; acc[6] += d;
+    }
+    const int ops[7] = {RED_SUM, RED_SUM, RED_MAX, RED_SUM, RED_SUM, RED_SUM, RED_SUM};
+    block_reduce<7>(acc, ops, smem);
+    grid_finalize<7>(acc, ops, partials, red_out, count, smem);
+}
+
+// ---------------------------------------------------------------------------
+// vectorised descent restated per point (base.py:124-230)
+// ---------------------------------------------------------------------------
+enum { MAT_MR = 0, MAT_QUAD = 1 };
+
+template <int D>
+__device__ __forceinline__ double det_t(const double (&X)[D]) {
+    if constexpr (D == 4) return X[0] * X[3] - X[1] * X[2];
+    else
+    return X[0] * (X[4] * X[8] - X[5] * X[7]) - X[1] * (X[3] * X[8] - X[5] * X[6]) +
+           X[2] * (X[3] * X[7] - X[4] * X[6]);
+}
+
+template <int D>
+__device__ __forceinline__ void cof_t(const double (&X)[D], double (&C)[D]) {
+    if constexpr (D == 4) {
+        C[0] = X[3]; C[1] = -X[2]; C[2] = -X[1]; C[3] = X[0];
+    } else {
+        C[0] = X[4] * X[8] - X[5] * X[7];
+        C[1] = X[5] * X[6] - X[3] * X[8];
+        C[2] = X[3] * X[7] - X[4] * X[6];
+        C[3] = X[2] * X[7] - X[1] * X[8];
+        C[4] = X[0] * X[8] - X[2] * X[6];
+        C[5] = X[1] * X[6] - X[0] * X[7];
+        C[6] = X[1] * X[5] - X[2] * X[4];
+        C[7] = X[2] * X[3] - X[0] * X[5];
+        C[8] = X[0] * X[4] - X[1] * X[3];
+    }
+}
+
+// The per-point coupling  -lam:X + rho/2 |G - X|^2  is carried as
+//   rho/2 |X|^2 - B:X + cG,   B = lam + rho G,  cG = rho/2 |G|^2,
+// (identical up to roundoff) so only 9 + 1 doubles of (G, lam) stay live in
+// registers across the sweep loop instead of 18.
+
+// objective (mooney_rivlin.py:132-141 / quadratic.py:52-55); +inf if det <= 0
+template <int MAT, int D>
+__device__ __forceinline__ double objective(const double (&X)[D], const double (&B)[D],
+                                            double cG, double m, double k, double rho) {
+    double bx = 0.0, I1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        bx += B[i] * X[i];
+        I1 += X[i] * X[i];
+    }
+    const double coupling = 0.5 * rho * I1 - bx + cG;
+    if constexpr (MAT == MAT_QUAD) return 0.5 * m * I1 + coupling;
+    const double J = det_t<D>(X);
+    if (J <= 0.0) return INFINITY;
+    const double dd = (D == 4) ? 2.0 : 3.0;
+    return 0.5 * m * (I1 - 2.0 * log(J) - dd) + 0.5 * k * (J - 1.0) * (J - 1.0) + coupling;
+}
+
+// gradient S(X) - lam - rho (G - X) = S(X) + rho X - B
+// (mooney_rivlin.py:143-151 / quadratic.py:57-58)
+template <int MAT, int D>
+__device__ __forceinline__ void gradient(const double (&X)[D], const double (&B)[D], double m,
+                                         double k, double rho, double (&g)[D]) {
+    if constexpr (MAT == MAT_QUAD) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) g[i] = (m + rho) * X[i] - B[i];
+    } else {
+        const double J = det_t<D>(X);
+        double C[D];
+        cof_t<D>(X, C);
+        const double iJ = 1.0 / J;
+        const double c2 = k * (J * J - J) - m;  // coefficient of F^{-T}
+#pragma unroll
+        for (int i = 0; i < D; ++i) g[i] = (m + rho) * X[i] + c2 * (C[i] * iJ) - B[i];
+    }
+}
+
+template <int MAT, int D>
+__device__ __forceinline__ bool admissible(const double (&X)[D]) {
+    if (MAT == MAT_QUAD) return true;
+    return det_t<D>(X) > 0.0;
+}
+
+// slots: 0 sum res^2, 1 n_conv (res < tol), 2 max nsw (cumulative),
+//        3 guard sum (sum res where res > tol), 4..4+D sum F
+template <int MAT, int D>
+__global__ void __launch_bounds__(LOCAL_THREADS, LOCAL_MIN_BLOCKS)
+k_descent(double *__restrict__ F, const double *__restrict__ G, const double *__restrict__ Lam,
+          const double *__restrict__ modA, const double *__restrict__ modB, int64_t M,
+          double rho, double tol, double phi_scale, int s0, int s1, double *__restrict__ tstate,
+          uint8_t *__restrict__ freestate, double *__restrict__ res_out,
+          int32_t *__restrict__ nsw_io, double *partials, double *red_out, unsigned int *count) {
+    constexpr int K = 4 + D;
+    __shared__ double smem[32 * K];
+    double acc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = 0.0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        double X[D], B[D], g[D], Xt[D];
+        double cG = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            X[i] = F[i * M + p];
+            const double gi = G[i * M + p];
+            B[i] = Lam[i * M + p] + rho * gi;
+            cG += gi * gi;
+        }
+        cG *= 0.5 * rho;
+        const double m = modA[p];
+        const double k = (MAT == MAT_MR) ? modB[p] : 0.0;
+        // t0 ~ inverse local curvature (mooney_rivlin.py:388-390, quadratic.py:63)
+        const double t0 = (MAT == MAT_MR) ? 1.0 / (rho + m + 4.0 * k) : 1.0 / (rho + m);
+        const double tmax = t0 * 16.0;
+        double t = t0;
+        bool freem = false;
+        int nsw = 0;
+        if (s0 > 0) {
+            t = tstate[p];
+            freem = freestate[p] != 0;
+            nsw = nsw_io[p];
+        }
+        gradient<MAT, D>(X, B, m, k, rho, g);
+        double gs = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) gs += g[i] * g[i];
+        double res = sqrt(gs);
+        bool moved = false;
+        // a point is active at global sweep s iff it was active at every
+        // earlier sweep (nsw == s) and res > tol; once inactive it stays so
+        for (int s = s0; s < s1; ++s) {
+            if (nsw != s || !(res > tol)) break;
+            nsw += 1;
+            moved = true;
+            bool in_free = freem, in_arm = false;
+            double phi0 = 0.0, gsq = 0.0;
+            if (!freem) {
+                phi0 = objective<MAT, D>(X, B, cG, m, k, rho);
+#pragma unroll
+                for (int i = 0; i < D; ++i) gsq += g[i] * g[i];
+                // base.py:168-171: unmeasurable decrease -> free mode, and the
+                // point takes this sweep's free step
+                const bool meas = BT_DECREASE * t * gsq > MEAS_EPS * (fabs(phi0) + phi_scale);
+                if (!meas) {
+                    freem = true;
+                    in_free = true;
+                } else {
+                    in_arm = true;
+                }
+            }
+            const double res_before = res;
+            if (in_arm) {
+                const double t_in = t;
+                bool accepted = false;
+                for (int bt = 0; bt < MAX_BT; ++bt) {
+#pragma unroll
+                    for (int i = 0; i < D; ++i) Xt[i] = X[i] - t * g[i];
+                    double phi_try = INFINITY;
+                    if (admissible<MAT, D>(Xt)) phi_try = objective<MAT, D>(Xt, B, cG, m, k, rho);
+                    if (phi_try <= phi0 - BT_DECREASE * t * gsq) {
+#pragma unroll
+                        for (int i = 0; i < D; ++i) X[i] = Xt[i];
+                        accepted = true;
+                        break;
+                    }
+                    t *= BT_SHRINK;
+                }
+                if (accepted) {
+                    t = fmin(t * 1.6, tmax);
+                } else {
+                    freem = true;
+                    t = t_in;
+                }
+            }
+            if (in_free) {
+#pragma unroll
+                for (int i = 0; i < D; ++i) Xt[i] = X[i] - t * g[i];
+                bool took = admissible<MAT, D>(Xt);
+                for (int bt = 0; bt < 12 && !took; ++bt) {
+                    t *= BT_SHRINK;
+#pragma unroll
+                    for (int i = 0; i < D; ++i) Xt[i] = X[i] - t * g[i];
+                    took = admissible<MAT, D>(Xt);
+                }
+                if (took) {
+#pragma unroll
+                    for (int i = 0; i < D; ++i) X[i] = Xt[i];
+                }
+            }
+            gradient<MAT, D>(X, B, m, k, rho, g);
+            gs = 0.0;
+#pragma unroll
+            for (int i = 0; i < D; ++i) gs += g[i] * g[i];
+            res = sqrt(gs);
+            if (in_free) {
+                if (res > res_before) t *= BT_SHRINK;
+                else t = fmin(t * 1.3, tmax);
+            }
+        }
+        if (moved) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) F[i * M + p] = X[i];
+        }
+        if (tstate) {
+            tstate[p] = t;
+            freestate[p] = freem ? 1 : 0;
+        }
+        if (nsw_io) nsw_io[p] = nsw;
+        if (res_out) res_out[p] = res;
+        acc[0] += res * res;
+        acc[1] += (res < tol) ? 1.0 : 0.0;
+        acc[2] = fmax(acc[2], (double)nsw);
+        acc[3] += (res > tol) ? res : 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) acc[4 + i] += X[i];
+    }
+    int ops[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) ops[k] = RED_SUM;
+    ops[2] = RED_MAX;
+    block_reduce<K>(acc, ops, smem);
+    grid_finalize<K>(acc, ops, partials, red_out, count, smem);
+}
+
+
+// ---------------------------------------------------------------------------
+// det F > 0 pre-check (base.py:116-121), run once after F is uploaded
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256)
+k_count_bad_det(const double *__restrict__ F, int64_t M, double *partials, double *red_out,
+                unsigned int *count) {
+    __shared__ double smem[32];
+    double acc[1] = {0.0};
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        double X[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) X[i] = F[i * M + p];
+        acc[0] += (det_t<D>(X) <= 0.0) ? 1.0 : 0.0;
+    }
+    const int ops[1] = {RED_SUM};
+    block_reduce<1>(acc, ops, smem);
+    grid_finalize<1>(acc, ops, partials, red_out, count, smem);
+}
+
+// per-component sums over points
+template <int NC>
+__global__ void __launch_bounds__(256)
+k_field_sums(const double *__restrict__ f, int64_t M, double *partials, double *red_out,
+             unsigned int *count) {
+    __shared__ double smem[32 * NC];
+    double acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
+         p += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c] += f[c * M + p];
+    }
+    int ops[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) ops[c] = RED_SUM;
+    block_reduce<NC>(acc, ops, smem);
+    grid_finalize<NC>(acc, ops, partials, red_out, count, smem);
+}
+
+}  // namespace
+
+static int reduce_blocks(mm_ctx *ctx, int threads) {
+    int64_t b = (ctx->M + threads - 1) / threads;
+    return (int)std::min<int64_t>(b, 148 * 8);
+}
+
+int mm_run_field_sums(mm_ctx *ctx, const double *field, int ncomp, double *out) {
+    const int blocks = reduce_blocks(ctx, 256);
+    int rc = mm_ensure_partials(ctx, blocks);
+    if (rc) return rc;
+    {
+        StageScope ss(ctx, MM_STAGE_OTHER);
+        switch (ncomp) {
+#define CASE(N)                                                                               \
+    case N:                                                                                   \
+        k_field_sums<N><<<blocks, 256, 0, ctx->stream>>>(field, ctx->M, ctx->partials,        \
+                                                         ctx->red_out, ctx->red_count);       \
+        break;
+            CASE(1) CASE(2) CASE(3) CASE(4) CASE(9)
+#undef CASE
+            default: return mm_fail(ctx, MM_ERR_CONFIG, "field_sums: unsupported ncomp %d", ncomp);
+        }
+    }
+    MM_LAUNCH_CHECK(ctx);
+    return mm_fetch_reduction(ctx, ncomp, out);
+}
+
+int mm_check_det(mm_ctx *ctx, int *bad) {
+    const int blocks = reduce_blocks(ctx, 256);
+    int rc = mm_ensure_partials(ctx, blocks);
+    if (rc) return rc;
+    {
+        StageScope ss(ctx, MM_STAGE_OTHER);
+        if (ctx->dim == 2)
+            k_count_bad_det<4><<<blocks, 256, 0, ctx->stream>>>(ctx->F, ctx->M, ctx->partials,
+                                                                ctx->red_out, ctx->red_count);
+        else
+            k_count_bad_det<9><<<blocks, 256, 0, ctx->stream>>>(ctx->F, ctx->M, ctx->partials,
+                                                                ctx->red_out, ctx->red_count);
+    }
+    MM_LAUNCH_CHECK(ctx);
+    double v;
+    rc = mm_fetch_reduction(ctx, 1, &v);
+    if (rc) return rc;
+    *bad = (int)v;
+    return MM_OK;
+}
+
+static int ensure_points(mm_ctx *ctx) {
+    int rc;
+    if (!ctx->res && (rc = mm_alloc(ctx, (void **)&ctx->res, sizeof(double) * ctx->M))) return rc;
+    if (!ctx->nsw && (rc = mm_alloc(ctx, (void **)&ctx->nsw, sizeof(int32_t) * ctx->M))) return rc;
+    if (!ctx->ok && (rc = mm_alloc(ctx, (void **)&ctx->ok, ctx->M))) return rc;
+    return MM_OK;
+}
+
+template <int MAT, int D>
+static int launch_descent(mm_ctx *ctx, double rho, double tol, double phi_scale, int s0, int s1,
+                          bool persist, bool want_points) {
+    const int blocks = local_blocks(ctx->M);
+    int rc = mm_ensure_partials(ctx, blocks);
+    if (rc) return rc;
+    StageScope ss(ctx, MM_STAGE_LOCAL);
+    k_descent<MAT, D><<<blocks, LOCAL_THREADS, 0, ctx->stream>>>(
+        ctx->F, ctx->G, ctx->Lam, ctx->modA, MAT == MAT_MR ? ctx->modB : ctx->modA, ctx->M, rho,
+        tol, phi_scale, s0, s1, persist ? ctx->tstate : nullptr,
+        persist ? ctx->freestate : nullptr, want_points ? ctx->res : nullptr,
+        (persist || want_points) ? ctx->nsw : nullptr, ctx->partials, ctx->red_out,
+        ctx->red_count);
+    MM_LAUNCH_CHECK(ctx);
+    return MM_OK;
+}
+
+static int launch_descent_any(mm_ctx *ctx, int material, double rho, double tol,
+                              double phi_scale, int s0, int s1, bool persist, bool want_points) {
+    const bool mr = material == MM_MAT_MR || material == MM_MAT_MR_DESCENT;
+    if (ctx->dim == 2)
+        return mr ? launch_descent<MAT_MR, 4>(ctx, rho, tol, phi_scale, s0, s1, persist, want_points)
+                  : launch_descent<MAT_QUAD, 4>(ctx, rho, tol, phi_scale, s0, s1, persist,
+                                                want_points);
+    return mr ? launch_descent<MAT_MR, 9>(ctx, rho, tol, phi_scale, s0, s1, persist, want_points)
+              : launch_descent<MAT_QUAD, 9>(ctx, rho, tol, phi_scale, s0, s1, persist,
+                                            want_points);
+}
+
+int mm_run_lce(mm_ctx *ctx, double rho, double tol, int64_t max_sweeps, int want_points,
+               mm_local_stats *out);
+
+int mm_run_local(mm_ctx *ctx, int material, double rho, double tol, int64_t max_sweeps,
+                 double phi_scale, int want_points, mm_local_stats *out) {
+    int rc;
+    const int D = ctx->D;
+    memset(out, 0, sizeof *out);
+    if (want_points && (rc = ensure_points(ctx))) return rc;
+    if (material == MM_MAT_LCE) return mm_run_lce(ctx, rho, tol, max_sweeps, want_points, out);
+    if (material == MM_MAT_MR && ctx->dim == 2) {
+        // compiled 2D kernel (mooney_rivlin.py:169-255)
+        const int blocks = local_blocks(ctx->M);
+        if ((rc = mm_ensure_partials(ctx, blocks))) return rc;
+        {
+            StageScope ss(ctx, MM_STAGE_LOCAL);
+            k_mr2d<<<blocks, LOCAL_THREADS, 0, ctx->stream>>>(
+                ctx->F, ctx->G, ctx->Lam, ctx->modA, ctx->modB, ctx->M, rho, tol, max_sweeps,
+                phi_scale, want_points ? ctx->res : nullptr, want_points ? ctx->nsw : nullptr,
+                ctx->partials, ctx->red_out, ctx->red_count);
+        }
+        MM_LAUNCH_CHECK(ctx);
+        double r[7];
+        if ((rc = mm_fetch_reduction(ctx, 7, r))) return rc;
+        out->sum_res2 = r[0];
+        out->n_conv = (int64_t)r[1];
+        out->sweeps = ctx->M ? (int64_t)r[2] : 0;
+        for (int i = 0; i < 4; ++i) out->sum_F[i] = r[3 + i];
+        if (want_points) MM_CUDA(ctx, cudaMemsetAsync(ctx->ok, 0, ctx->M, ctx->stream));
+        return MM_OK;
+    }
+    // vectorised-descent semantics (base.py:124-230)
+    if (material == MM_MAT_MR_DESCENT) material = MM_MAT_MR;
+    if (material == MM_MAT_MR && !ctx->F_checked) {
+        int bad = 0;
+        if ((rc = mm_check_det(ctx, &bad))) return rc;
+        if (bad) return mm_fail(ctx, MM_ERR_INADMISSIBLE, "det F <= 0 at %d point(s)", bad);
+        ctx->F_checked = true;
+    }
+    const int K = 4 + D;
+    double r[MM_MAX_PARTIALS];
+    const bool segmented = max_sweeps > 64;
+    if (segmented) {
+        if (!ctx->tstate && (rc = mm_alloc(ctx, (void **)&ctx->tstate, sizeof(double) * ctx->M)))
+            return rc;
+        if (!ctx->freestate && (rc = mm_alloc(ctx, (void **)&ctx->freestate, ctx->M))) return rc;
+        if (!ctx->nsw && (rc = mm_alloc(ctx, (void **)&ctx->nsw, sizeof(int32_t) * ctx->M)))
+            return rc;
+    }
+    int64_t sweeps = 0;
+    if (!segmented) {
+        rc = launch_descent_any(ctx, material, rho, tol, phi_scale, 0, (int)max_sweeps, false,
+                                want_points);
+        if (rc) return rc;
+        if ((rc = mm_fetch_reduction(ctx, K, r))) return rc;
+        sweeps = (int64_t)r[2];
+    } else {
+        double ref = INFINITY;
+        while (sweeps < max_sweeps) {
+            const int64_t s1 = std::min<int64_t>((sweeps / 32 + 1) * 32, max_sweeps);
+            rc = launch_descent_any(ctx, material, rho, tol, phi_scale, (int)sweeps, (int)s1, true,
+                                    want_points);
+            if (rc) return rc;
+            if ((rc = mm_fetch_reduction(ctx, K, r))) return rc;
+            const int64_t mx = (int64_t)r[2];
+            if (mx < s1) {  // every point stopped before s1
+                sweeps = mx;
+                break;
+            }
+            sweeps = s1;
+            if (sweeps % 32 == 0) {  // stall guard, base.py:224-229
+                const double cur = r[3];
+                if (cur > 0.995 * ref) break;
+                ref = cur;
+            }
+        }
+    }
+    out->sum_res2 = r[0];
+    out->n_conv = (int64_t)r[1];
+    out->sweeps = ctx->M ? sweeps : 0;
+    for (int i = 0; i < D; ++i) out->sum_F[i] = r[4 + i];
+    if (want_points) MM_CUDA(ctx, cudaMemsetAsync(ctx->ok, 0, ctx->M, ctx->stream));
+    return MM_OK;
+}

@@ -1,0 +1,799 @@
+// Global step of the ADMM iteration: Helmholtz projection (projection.py:132-168)
+// fused with the multiplier ascent and residuals (solver.py:268-279).
+//
+// The reference transforms 9 tensor components forward and 3 + 9 inverse.
+// Here the same result (exact in exact arithmetic) is obtained with d
+// components each way:
+//   A  k_row_fwd   stencil divergence d_i = sum_j T_ij(x+e_j) - T_ij(x-e_j),
+//                  T = F - lam/rho, fused with the real-to-complex FFT along
+//                  the contiguous axis (two reals packed per complex, one
+//                  N/2-point complex FFT per row + split)
+//   B  k_col       complex FFT along axis 1 (3D only)
+//   C  k_col<SOLVE> complex FFT along axis 0, the per-wavevector solve
+//                  u_hat = -d_hat / |g|^2 (masked modes -> 0, projection.py:
+//                  155-157), and the inverse FFT along axis 0, in one pass
+//   D  k_col       inverse FFT along axis 1 (3D only)
+//   E  k_row_inv   complex-to-real inverse along the contiguous axis -> u_tilde
+//   F  k_grad      grad_u = u_mean + central difference of u_tilde, and (solver
+//                  path) |dG|^2, lam += rho (grad_u - F), |misfit|^2, sum lam
+// Every FFT keeps a tile of lines in shared memory; power-of-two lengths use a
+// register four-step (N = N1 x N2, one N1-point FFT per thread, twiddle, one
+// shared-memory exchange, one N2-point FFT per thread); other lengths use an
+// exact O(N^2) DFT over the same tile (small grids only).
+#include <math.h>
+
+#include <algorithm>
+
+#include "mm_internal.cuh"
+
+namespace {
+
+__constant__ double2 c_w32[32];  // exp(-2 pi i k / 32)
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+
+template <int R>
+__host__ __device__ constexpr int brev(int i) {
+    int r = 0;
+    for (int b = 1; b < R; b <<= 1) {
+        r = (r << 1) | (i & 1);
+        i >>= 1;
+    }
+    return r;
+}
+
+// In-register radix-2 DIT FFT of R <= 32 points, natural-order output.
+template <int R, bool INV>
+__device__ __forceinline__ void fft_reg(double2 (&v)[R]) {
+    if constexpr (R > 1) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int j = brev<R>(i);
+            if (j > i) {
+                double2 t = v[i];
+                v[i] = v[j];
+                v[j] = t;
+            }
+        }
+#pragma unroll
+        for (int half = 1; half < R; half <<= 1) {
+#pragma unroll
+            for (int i = 0; i < R; i += 2 * half) {
+#pragma unroll
+                for (int k = 0; k < half; ++k) {
+                    const double2 a = v[i + k];
+                    double2 b = v[i + k + half];
+                    if (k != 0) {
+                        if (2 * k == half) {  // W_{2 half}^{half/2} = -i (fwd) / +i (inv)
+                            b = INV ? make_double2(-b.y, b.x) : make_double2(b.y, -b.x);
+                        } else {
+                            double2 w = c_w32[k * (16 / half)];
+                            if (INV) w.y = -w.y;
+                            b = cmul(b, w);
+                        }
+                    }
+                    v[i + k] = cadd(a, b);
+                    v[i + k + half] = csub(a, b);
+                }
+            }
+        }
+    }
+}
+
+// FFT of TK lines of length N = N1*N2 held in shared memory, element n of
+// line c at buf[n*LD + c], LD = TK + 1.  Requires blockDim >= TK*max(N1,N2).
+// tw: exp(-2 pi i k / N), k < N.
+template <int N1, int N2, int TK, bool INV>
+__device__ __forceinline__ void tile_fft(double2 *buf, const double2 *__restrict__ tw) {
+    constexpr int LD = TK + 1;
+    const int tid = threadIdx.x;
+    const int c = tid % TK;
+    if constexpr (N2 == 1) {
+        if (tid < TK) {
+            double2 v[N1];
+#pragma unroll
+            for (int i = 0; i < N1; ++i) v[i] = buf[i * LD + c];
+            fft_reg<N1, INV>(v);
+#pragma unroll
+            for (int i = 0; i < N1; ++i) buf[i * LD + c] = v[i];
+        }
+        __syncthreads();
+    } else {
+        double2 v[N1];
+        const int n2 = tid / TK;
+        const bool act1 = tid < TK * N2;
+        if (act1) {
+#pragma unroll
+            for (int n1 = 0; n1 < N1; ++n1) v[n1] = buf[(N2 * n1 + n2) * LD + c];
+            fft_reg<N1, INV>(v);
+#pragma unroll
+            for (int k1 = 1; k1 < N1; ++k1) {
+                if (n2 != 0) {
+                    double2 w = __ldg(&tw[n2 * k1]);
+                    if (INV) w.y = -w.y;
+                    v[k1] = cmul(v[k1], w);
+                }
+            }
+        }
+        __syncthreads();
+        if (act1) {
+#pragma unroll
+            for (int k1 = 0; k1 < N1; ++k1) buf[(k1 * N2 + n2) * LD + c] = v[k1];
+        }
+        __syncthreads();
+        double2 u[N2];
+        const int k1 = tid / TK;
+        const bool act2 = tid < TK * N1;
+        if (act2) {
+#pragma unroll
+            for (int j = 0; j < N2; ++j) u[j] = buf[(k1 * N2 + j) * LD + c];
+            fft_reg<N2, INV>(u);
+        }
+        __syncthreads();
+        if (act2) {
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) buf[(k1 + N1 * k2) * LD + c] = u[k2];
+        }
+        __syncthreads();
+    }
+}
+
+// Exact DFT of TK lines of runtime length N (any N), via a scratch tile.
+template <int TK, bool INV>
+__device__ __forceinline__ void tile_dft(double2 *buf, double2 *scr, int N,
+                                         const double2 *__restrict__ tw) {
+    constexpr int LD = TK + 1;
+    for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
+        const int k = w / TK, c = w % TK;
+        double2 s = make_double2(0.0, 0.0);
+        int idx = 0;
+        for (int n = 0; n < N; ++n) {
+            double2 t = tw[idx];
+            if (INV) t.y = -t.y;
+            s = cadd(s, cmul(buf[n * LD + c], t));
+            idx += k;
+            if (idx >= N) idx -= N;
+        }
+        scr[k * LD + c] = s;
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
+        const int k = w / TK, c = w % TK;
+        buf[k * LD + c] = scr[k * LD + c];
+    }
+    __syncthreads();
+}
+
+template <int N1, int N2, int TK, bool INV>
+__device__ __forceinline__ void line_transform(double2 *buf, double2 *scr, int N,
+                                               const double2 *__restrict__ tw) {
+    if constexpr (N1 == 0)
+        tile_dft<TK, INV>(buf, scr, N, tw);
+    else
+        tile_fft<N1, N2, TK, INV>(buf, tw);
+}
+
+struct RowGeom {
+    int n;          // points per axis
+    int dim;
+    int64_t M;      // points
+    int64_t nrows;  // M / n
+    int P;          // spectral pitch
+    int N;          // complex line length (n/2 packed, or n when odd)
+    int packed;     // 1: two reals per complex (even n)
+};
+
+// ---------------------------------------------------------------------------
+// A: divergence of T = F - lam/rho fused with the R2C transform of each row
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double tval(const double *__restrict__ F, const double *__restrict__ L,
+                                       int64_t off, double rho) {
+    return __ldg(&F[off]) - __ldg(&L[off]) / rho;  // projection.py:154 (F - lam / rho)
+}
+
+// start offsets (row * n) of a row and of its neighbour rows along axes 0, 1
+struct RowNbr {
+    int64_t self, zp, zm, yp, ym;
+};
+
+__device__ __forceinline__ RowNbr row_nbrs(const RowGeom &g, int row) {
+    const int n = g.n;
+    RowNbr r;
+    if (g.dim == 3) {
+        const int i0 = row / n, i1 = row - i0 * n;
+        const int i0p = (i0 + 1 == n) ? 0 : i0 + 1, i0m = (i0 == 0) ? n - 1 : i0 - 1;
+        const int i1p = (i1 + 1 == n) ? 0 : i1 + 1, i1m = (i1 == 0) ? n - 1 : i1 - 1;
+        r.zp = (int64_t)(i0p * n + i1) * n;
+        r.zm = (int64_t)(i0m * n + i1) * n;
+        r.yp = (int64_t)(i0 * n + i1p) * n;
+        r.ym = (int64_t)(i0 * n + i1m) * n;
+    } else {
+        const int rp = (row + 1 == n) ? 0 : row + 1, rm = (row == 0) ? n - 1 : row - 1;
+        r.zp = (int64_t)rp * n;
+        r.zm = (int64_t)rm * n;
+        r.yp = r.ym = 0;
+    }
+    r.self = (int64_t)row * n;
+    return r;
+}
+
+// unscaled divergence sum_j [T_cj(x+e_j) - T_cj(x-e_j)] at point x of a row
+__device__ __forceinline__ double div_at(const double *__restrict__ F, const double *__restrict__ L,
+                                         double rho, const RowGeom &g, int c, const RowNbr &nb,
+                                         int x) {
+    const int n = g.n;
+    const int64_t M = g.M;
+    const int d = g.dim;
+    double s;
+    {  // axis 0 (slowest)
+        const int64_t comp = (int64_t)(c * d + 0) * M + x;
+        s = tval(F, L, comp + nb.zp, rho) - tval(F, L, comp + nb.zm, rho);
+    }
+    if (d == 3) {  // axis 1
+        const int64_t comp = (int64_t)(c * d + 1) * M + x;
+        s += tval(F, L, comp + nb.yp, rho) - tval(F, L, comp + nb.ym, rho);
+    }
+    {  // contiguous axis
+        const int64_t comp = (int64_t)(c * d + d - 1) * M + nb.self;
+        const int xp = (x + 1 == n) ? 0 : x + 1, xm = (x == 0) ? n - 1 : x - 1;
+        s += tval(F, L, comp + xp, rho) - tval(F, L, comp + xm, rho);
+    }
+    return s;
+}
+
+template <int N1, int N2, int TK>
+__global__ void k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho,
+                          double2 *__restrict__ spec, RowGeom g,
+                          const double2 *__restrict__ tw_line,
+                          const double2 *__restrict__ tw_r2c) {
+    extern __shared__ double2 smem_c[];
+    constexpr int LD = TK + 1;
+    const int rows = TK / g.dim;
+    double2 *buf = smem_c;
+    double2 *scr = smem_c + (size_t)(g.N + 1) * LD;
+    const int64_t row0 = (int64_t)blockIdx.x * rows;
+    const int N = g.N;
+    // pack: line = c * rows + r
+    for (int w = threadIdx.x; w < TK * N; w += blockDim.x) {
+        const int line = w / N, m = w - line * N;
+        const int c = line / rows, r = line - c * rows;
+        const int64_t row = row0 + r;
+        double2 z = make_double2(0.0, 0.0);
+        if (row < g.nrows) {
+            const RowNbr nb = row_nbrs(g, (int)row);
+            if (g.packed) {
+                z.x = div_at(F, L, rho, g, c, nb, 2 * m);
+                z.y = div_at(F, L, rho, g, c, nb, 2 * m + 1);
+            } else {
+                z.x = div_at(F, L, rho, g, c, nb, m);
+            }
+        }
+        buf[m * LD + line] = z;
+    }
+    __syncthreads();
+    line_transform<N1, N2, TK, false>(buf, scr, N, tw_line);
+    // split (packed) and store k = 0 .. n/2
+    const int nh = g.n / 2 + 1;
+    for (int w = threadIdx.x; w < TK * nh; w += blockDim.x) {
+        const int line = w / nh, k = w - line * nh;
+        const int c = line / rows, r = line - c * rows;
+        const int64_t row = row0 + r;
+        if (row >= g.nrows) continue;
+        double2 X;
+        if (g.packed) {
+            const double2 Zk = buf[(k == N ? 0 : k) * LD + line];
+            const double2 Zc = cconj(buf[(k == 0 ? 0 : N - k) * LD + line]);
+            const double2 E = cscale(cadd(Zk, Zc), 0.5);
+            const double2 Od = csub(Zk, Zc);  // 2i * O
+            // X = E + W^k * Od / (2i) = E - 0.5 i W^k Od
+            const double2 WO = cmul(__ldg(&tw_r2c[k]), Od);
+            X = make_double2(E.x + 0.5 * WO.y, E.y - 0.5 * WO.x);
+        } else {
+            X = buf[k * LD + line];
+        }
+        spec[((int64_t)c * g.nrows + row) * g.P + k] = X;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// E: inverse C2R along rows -> u_tilde (unnormalised; 1/n^d folded into C)
+// ---------------------------------------------------------------------------
+template <int N1, int N2, int TK>
+__global__ void k_row_inv(const double2 *__restrict__ spec, double *__restrict__ Ut, RowGeom g,
+                          const double2 *__restrict__ tw_line,
+                          const double2 *__restrict__ tw_r2c) {
+    extern __shared__ double2 smem_c[];
+    constexpr int LD = TK + 1;
+    const int rows = TK / g.dim;
+    double2 *buf = smem_c;
+    double2 *scr = smem_c + (size_t)(g.N + 1) * LD;
+    const int64_t row0 = (int64_t)blockIdx.x * rows;
+    const int N = g.N;
+    const int nh = g.n / 2 + 1;
+    for (int w = threadIdx.x; w < TK * nh; w += blockDim.x) {
+        const int line = w / nh, k = w - line * nh;
+        const int c = line / rows, r = line - c * rows;
+        const int64_t row = row0 + r;
+        double2 X = make_double2(0.0, 0.0);
+        if (row < g.nrows) X = spec[((int64_t)c * g.nrows + row) * g.P + k];
+        buf[k * LD + line] = X;
+    }
+    __syncthreads();
+    if (g.packed) {
+        // Z[k] = A[k] + i B[k], A = X[k] + conj X[N-k], B = (X[k] - conj X[N-k]) conj(W^k)
+        const int npair = N / 2 + 1;
+        for (int w = threadIdx.x; w < TK * npair; w += blockDim.x) {
+            const int line = w / npair, k = w - line * npair;
+            const int kc = N - k;
+            const double2 Xk = buf[k * LD + line];
+            const double2 Xc = buf[kc * LD + line];
+            const double2 A1 = cadd(Xk, cconj(Xc));
+            const double2 B1 = cmul(csub(Xk, cconj(Xc)), cconj(__ldg(&tw_r2c[k])));
+            const double2 Z1 = make_double2(A1.x - B1.y, A1.y + B1.x);
+            if (kc != k && kc != N) {
+                const double2 A2 = cadd(Xc, cconj(Xk));
+                const double2 B2 = cmul(csub(Xc, cconj(Xk)), cconj(__ldg(&tw_r2c[kc])));
+                buf[kc * LD + line] = make_double2(A2.x - B2.y, A2.y + B2.x);
+            }
+            buf[k * LD + line] = Z1;  // k == 0 also overwrites slot 0; slot N unused
+        }
+    } else {
+        // odd n: full Hermitian spectrum
+        for (int w = threadIdx.x; w < TK * (N - nh); w += blockDim.x) {
+            const int line = w / (N - nh), k = nh + (w - line * (N - nh));
+            buf[k * LD + line] = cconj(buf[(N - k) * LD + line]);
+        }
+    }
+    __syncthreads();
+    line_transform<N1, N2, TK, true>(buf, scr, N, tw_line);
+    for (int w = threadIdx.x; w < TK * N; w += blockDim.x) {
+        const int line = w / N, m = w - line * N;
+        const int c = line / rows, r = line - c * rows;
+        const int64_t row = row0 + r;
+        if (row >= g.nrows) continue;
+        const double2 z = buf[m * LD + line];
+        double *dst = Ut + (int64_t)c * g.M + row * g.n;
+        if (g.packed) {
+            dst[2 * m] = z.x;
+            dst[2 * m + 1] = z.y;
+        } else {
+            dst[m] = z.x;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// B/C/D: column transforms on the half spectrum (TK contiguous columns / tile)
+// ---------------------------------------------------------------------------
+struct ColGeom {
+    int N;             // line length (= n)
+    int ncol;          // valid columns (n/2 + 1)
+    int64_t es;        // element stride along the line (complex units)
+    int64_t os;        // outer stride
+    int64_t cs;        // component stride
+    // solve (MODE 2)
+    int n, dim;
+    const double *sym;
+    double thresh, scale;
+};
+
+enum { COL_FWD = 0, COL_INV = 1, COL_SOLVE = 2 };
+
+template <int N1, int N2, int MODE>
+__global__ void k_col(double2 *__restrict__ spec, ColGeom g, const double2 *__restrict__ tw) {
+    constexpr int TK = 8, LD = TK + 1;
+    extern __shared__ double2 smem_c[];
+    double2 *buf = smem_c;
+    double2 *scr = smem_c + (size_t)(g.N + 1) * LD;
+    const int k0 = blockIdx.x * TK;
+    const int outer = blockIdx.y;
+    const int comp = blockIdx.z;
+    double2 *base = spec + comp * g.cs + outer * g.os + k0;
+    const int N = g.N;
+    for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
+        const int n = w / TK, c = w - n * TK;
+        double2 v = make_double2(0.0, 0.0);
+        if (k0 + c < g.ncol) v = base[n * g.es + c];
+        buf[n * LD + c] = v;
+    }
+    __syncthreads();
+    if constexpr (MODE == COL_FWD || MODE == COL_SOLVE)
+        line_transform<N1, N2, TK, false>(buf, scr, N, tw);
+    else
+        line_transform<N1, N2, TK, true>(buf, scr, N, tw);
+    if constexpr (MODE == COL_SOLVE) {
+        // u_hat = -d_hat / |g|^2 on live modes (projection.py:150-158); the
+        // column is the last-axis frequency, `outer` the axis-1 one in 3D
+        const double *s0 = g.sym;
+        const double *slast = g.sym + (int64_t)(g.dim - 1) * g.n;
+        for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
+            const int kl = w / TK, c = w - kl * TK;
+            double gsq = s0[kl];
+            if (g.dim == 3) gsq = gsq + g.sym[g.n + outer];
+            gsq = gsq + slast[min(k0 + c, g.n - 1)];
+            const double inv = (gsq > g.thresh) ? 1.0 / gsq : 0.0;
+            buf[kl * LD + c] = cscale(buf[kl * LD + c], -inv * g.scale);
+        }
+        __syncthreads();
+        line_transform<N1, N2, TK, true>(buf, scr, N, tw);
+    }
+    for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
+        const int n = w / TK, c = w - n * TK;
+        if (k0 + c < g.ncol) base[n * g.es + c] = buf[n * LD + c];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// F: gradient of u_tilde, multiplier ascent and residual sums
+// slots: 0 sum dG^2, 1 sum misfit^2, 2.. sum lam (D)
+// ---------------------------------------------------------------------------
+struct Mean9 {
+    double v[9];
+};
+
+// periodic neighbour offsets of point p (< 2^31) along each axis; lgn = log2 n
+// when n is a power of two (shift/mask), else -1 (32-bit division)
+template <int DIM>
+__device__ __forceinline__ void nbr_offsets(int64_t p64, int n, int lgn, int (&off_p)[DIM],
+                                            int (&off_m)[DIM]) {
+    const unsigned p = (unsigned)p64;
+    unsigned c[DIM];
+    if (lgn >= 0) {
+        const unsigned mask = (unsigned)n - 1u;
+#pragma unroll
+        for (int j = DIM - 1; j >= 0; --j) c[j] = (p >> (lgn * (DIM - 1 - j))) & mask;
+    } else {
+        unsigned q = p;
+#pragma unroll
+        for (int j = DIM - 1; j >= 0; --j) {
+            const unsigned nq = q / (unsigned)n;
+            c[j] = q - nq * (unsigned)n;
+            q = nq;
+        }
+    }
+    int stride = 1;
+#pragma unroll
+    for (int j = DIM - 1; j >= 0; --j) {
+        off_p[j] = (c[j] + 1 == (unsigned)n) ? -(n - 1) * stride : stride;
+        off_m[j] = (c[j] == 0) ? (n - 1) * stride : -stride;
+        stride *= n;
+    }
+}
+
+template <int DIM, bool UPDATE>
+__global__ void __launch_bounds__(256)
+k_grad(const double *__restrict__ Ut, double *__restrict__ G, const double *__restrict__ F,
+       double *__restrict__ Lam, int n, int lgn, int64_t M, double inv2h, double rho, Mean9 um,
+       double *partials, double *red_out, unsigned int *count) {
+    constexpr int D = DIM * DIM;
+    constexpr int K = 2 + D;
+    __shared__ double smem[32 * K];
+    double acc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = 0.0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        // neighbour offsets along each axis (periodic)
+        int off_p[DIM], off_m[DIM];
+        nbr_offsets<DIM>(p, n, lgn, off_p, off_m);
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) {
+            const double *u = Ut + (int64_t)i * M + p;
+#pragma unroll
+            for (int j = 0; j < DIM; ++j) {
+                const double gfl = (__ldg(u + off_p[j]) - __ldg(u + off_m[j])) * inv2h;
+                const int c = i * DIM + j;
+                const double gnew = gfl + um.v[c];  // projection.py:168
+                const int64_t o = (int64_t)c * M + p;
+                if (UPDATE) {
+                    const double dg = gnew - G[o];
+                    const double mis = gnew - F[o];  // solver.py:277
+                    const double lnew = Lam[o] + rho * mis;  // solver.py:279
+                    G[o] = gnew;
+                    Lam[o] = lnew;
+                    acc[0] += dg * dg;
+                    acc[1] += mis * mis;
+                    acc[2 + c] += lnew;
+                } else {
+                    G[o] = gnew;
+                }
+            }
+        }
+    }
+    if (UPDATE) {
+        int ops[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) ops[k] = RED_SUM;
+        block_reduce<K>(acc, ops, smem);
+        grid_finalize<K>(acc, ops, partials, red_out, count, smem);
+    }
+}
+
+// stencil divergence of F into Ut: (div F)_i = sum_j (F_ij(x+e_j) - F_ij(x-e_j)) / (2h)
+template <int DIM>
+__global__ void __launch_bounds__(256)
+k_div(const double *__restrict__ F, double *__restrict__ Ut, int n, int lgn, int64_t M,
+      double inv2h) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int off_p[DIM], off_m[DIM];
+        nbr_offsets<DIM>(p, n, lgn, off_p, off_m);
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < DIM; ++j) {
+                const double *f = F + (int64_t)(i * DIM + j) * M + p;
+                s += (__ldg(f + off_p[j]) - __ldg(f + off_m[j])) * inv2h;
+            }
+            Ut[(int64_t)i * M + p] = s;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host-side dispatch
+// ---------------------------------------------------------------------------
+bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+
+int ilog2(int n) {
+    if (!is_pow2(n)) return -1;
+    int l = 0;
+    while ((1 << l) < n) ++l;
+    return l;
+}
+
+// (N1, N2) factorisation for the register four-step; (0,0) = exact DFT path
+void factor(int N, int &N1, int &N2) {
+    N1 = N2 = 0;
+    if (!is_pow2(N) || N > 1024) return;
+    switch (N) {
+        case 1: N1 = 1; N2 = 1; break;
+        case 2: N1 = 2; N2 = 1; break;
+        case 4: N1 = 4; N2 = 1; break;
+        case 8: N1 = 8; N2 = 1; break;
+        case 16: N1 = 4; N2 = 4; break;
+        case 32: N1 = 8; N2 = 4; break;
+        case 64: N1 = 8; N2 = 8; break;
+        case 128: N1 = 16; N2 = 8; break;
+        case 256: N1 = 16; N2 = 16; break;
+        case 512: N1 = 32; N2 = 16; break;
+        case 1024: N1 = 32; N2 = 32; break;
+    }
+}
+
+template <typename Kern>
+int launch_smem(mm_ctx *ctx, Kern kern, dim3 grid, int threads, size_t smem) {
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess)
+            return mm_fail(ctx, MM_ERR_CUDA, "smem attribute (%zu B): %s", smem,
+                           cudaGetErrorString(e));
+    }
+    return MM_OK;
+}
+
+template <int N1, int N2, int TK>
+int run_rows_t(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double2 *tw_line) {
+    const int rows = TK / g.dim;
+    const int threads = N1 ? std::max(64, TK * std::max(N1, N2)) : 256;
+    const size_t smem = sizeof(double2) * (size_t)(g.N + 1) * (TK + 1) * (N1 ? 1 : 2);
+    dim3 grid((unsigned)((g.nrows + rows - 1) / rows));
+    if (fwd) {
+        auto kern = k_row_fwd<N1, N2, TK>;
+        int rc = launch_smem(ctx, kern, grid, threads, smem);
+        if (rc) return rc;
+        kern<<<grid, threads, smem, ctx->stream>>>(ctx->F, ctx->Lam, rho, ctx->spec, g, tw_line,
+                                                   ctx->tw_r2c);
+    } else {
+        auto kern = k_row_inv<N1, N2, TK>;
+        int rc = launch_smem(ctx, kern, grid, threads, smem);
+        if (rc) return rc;
+        kern<<<grid, threads, smem, ctx->stream>>>(ctx->spec, ctx->Ut, g, tw_line, ctx->tw_r2c);
+    }
+    MM_LAUNCH_CHECK(ctx);
+    return MM_OK;
+}
+
+template <int N1, int N2>
+int run_rows_n(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double2 *tw) {
+    // lines per tile: TK = dim * rows, bounded so TK*max(N1,N2) <= 512 threads
+    const bool big = N1 >= 32;
+    if (g.dim == 2)
+        return big ? run_rows_t<N1, N2, 8>(ctx, fwd, rho, g, tw)
+                   : run_rows_t<N1, N2, 16>(ctx, fwd, rho, g, tw);
+    return big ? run_rows_t<N1, N2, 12>(ctx, fwd, rho, g, tw)
+               : run_rows_t<N1, N2, 24>(ctx, fwd, rho, g, tw);
+}
+
+int run_rows(mm_ctx *ctx, bool fwd, double rho) {
+    RowGeom g;
+    g.n = ctx->n;
+    g.dim = ctx->dim;
+    g.M = ctx->M;
+    g.nrows = ctx->nrows;
+    g.P = ctx->P;
+    g.packed = (ctx->n % 2 == 0) ? 1 : 0;
+    g.N = g.packed ? ctx->n / 2 : ctx->n;
+    const double2 *tw = g.packed ? ctx->tw_half : ctx->tw_full;
+    int N1, N2;
+    factor(g.N, N1, N2);
+    switch (N1 * 100 + N2) {
+#define CASE(a, b) \
+    case a * 100 + b: return run_rows_n<a, b>(ctx, fwd, rho, g, tw);
+        CASE(1, 1) CASE(2, 1) CASE(4, 1) CASE(8, 1) CASE(4, 4) CASE(8, 4) CASE(8, 8)
+        CASE(16, 8) CASE(16, 16) CASE(32, 16) CASE(32, 32)
+#undef CASE
+        default: return run_rows_n<0, 0>(ctx, fwd, rho, g, tw);
+    }
+}
+
+template <int N1, int N2, int MODE>
+int run_col_t(mm_ctx *ctx, const ColGeom &g, int n_outer) {
+    constexpr int TK = 8;
+    const int threads = N1 ? std::max(64, TK * std::max(N1, N2)) : 256;
+    const size_t smem = sizeof(double2) * (size_t)(g.N + 1) * (TK + 1) * (N1 ? 1 : 2);
+    dim3 grid((unsigned)((g.ncol + TK - 1) / TK), (unsigned)n_outer, (unsigned)ctx->dim);
+    auto kern = k_col<N1, N2, MODE>;
+    int rc = launch_smem(ctx, kern, grid, threads, smem);
+    if (rc) return rc;
+    kern<<<grid, threads, smem, ctx->stream>>>(ctx->spec, g, ctx->tw_full);
+    MM_LAUNCH_CHECK(ctx);
+    return MM_OK;
+}
+
+template <int MODE>
+int run_col(mm_ctx *ctx, const ColGeom &g, int n_outer) {
+    int N1, N2;
+    factor(g.N, N1, N2);
+    switch (N1 * 100 + N2) {
+#define CASE(a, b) \
+    case a * 100 + b: return run_col_t<a, b, MODE>(ctx, g, n_outer);
+        CASE(1, 1) CASE(2, 1) CASE(4, 1) CASE(8, 1) CASE(4, 4) CASE(8, 4) CASE(8, 8)
+        CASE(16, 8) CASE(16, 16) CASE(32, 16) CASE(32, 32)
+#undef CASE
+        default: return run_col_t<0, 0, MODE>(ctx, g, n_outer);
+    }
+}
+
+bool g_const_ready[64] = {false};
+
+int ensure_constants(mm_ctx *ctx) {
+    if (ctx->device >= 0 && ctx->device < 64 && g_const_ready[ctx->device]) return MM_OK;
+    double2 w[32];
+    for (int k = 0; k < 32; ++k) {
+        long double a = -2.0L * 3.141592653589793238462643383279502884L * k / 32.0L;
+        w[k].x = (double)cosl(a);
+        w[k].y = (double)sinl(a);
+    }
+    MM_CUDA(ctx, cudaMemcpyToSymbol(c_w32, w, sizeof w));
+    if (ctx->device >= 0 && ctx->device < 64) g_const_ready[ctx->device] = true;
+    return MM_OK;
+}
+
+}  // namespace
+
+int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
+                   mm_update_stats *out) {
+    int rc = ensure_constants(ctx);
+    if (rc) return rc;
+    const int n = ctx->n, d = ctx->dim;
+    // A: divergence + R2C rows
+    {
+        StageScope ss(ctx, MM_STAGE_ROW_FWD);
+        if ((rc = run_rows(ctx, true, rho))) return rc;
+    }
+    ColGeom g;
+    g.N = n;
+    g.ncol = ctx->nh;
+    g.n = n;
+    g.dim = d;
+    g.sym = ctx->sym;
+    g.thresh = ctx->sym_thresh;
+    double nd = 1.0;
+    for (int i = 0; i < d; ++i) nd *= (double)n;
+    g.scale = 1.0 / (2.0 * ctx->h) / nd;
+    if (d == 3) {
+        // spectral index ((c*n + i0)*n + i1)*P + k2
+        ColGeom gy = g;
+        gy.es = ctx->P;
+        gy.os = (int64_t)n * ctx->P;
+        gy.cs = (int64_t)n * n * ctx->P;
+        ColGeom gz = g;
+        gz.es = (int64_t)n * ctx->P;
+        gz.os = ctx->P;
+        gz.cs = gy.cs;
+        {
+            StageScope ss(ctx, MM_STAGE_COL_FWD);
+            if ((rc = run_col<COL_FWD>(ctx, gy, n))) return rc;
+        }
+        {
+            StageScope ss(ctx, MM_STAGE_COL_SOLVE);
+            if ((rc = run_col<COL_SOLVE>(ctx, gz, n))) return rc;
+        }
+        {
+            StageScope ss(ctx, MM_STAGE_COL_INV);
+            if ((rc = run_col<COL_INV>(ctx, gy, n))) return rc;
+        }
+    } else {
+        ColGeom gz = g;
+        gz.es = ctx->P;
+        gz.os = 0;
+        gz.cs = (int64_t)n * ctx->P;
+        StageScope ss(ctx, MM_STAGE_COL_SOLVE);
+        if ((rc = run_col<COL_SOLVE>(ctx, gz, 1))) return rc;
+    }
+    // E: C2R rows -> u_tilde
+    {
+        StageScope ss(ctx, MM_STAGE_ROW_INV);
+        if ((rc = run_rows(ctx, false, rho))) return rc;
+    }
+    // F: gradient (+ ascent and residual sums)
+    Mean9 um;
+    for (int i = 0; i < 9; ++i) um.v[i] = i < ctx->D ? u_mean[i] : 0.0;
+    const int threads = 256;
+    const int blocks = (int)std::min<int64_t>((ctx->M + threads - 1) / threads, 148 * 8);
+    if ((rc = mm_ensure_partials(ctx, blocks))) return rc;
+    const double inv2h = 1.0 / (2.0 * ctx->h);
+    const int lgn = ilog2(n);
+#define LAUNCH(DIM, UPD)                                                                      \
+    k_grad<DIM, UPD><<<blocks, threads, 0, ctx->stream>>>(ctx->Ut, ctx->G, ctx->F, ctx->Lam, n, lgn, \
+                                                          ctx->M, inv2h, rho, um,               \
+                                                          ctx->partials, ctx->red_out,          \
+                                                          ctx->red_count)
+    {
+        StageScope ss(ctx, MM_STAGE_GRAD);
+        if (d == 2) {
+            if (update) LAUNCH(2, true);
+            else LAUNCH(2, false);
+        } else {
+            if (update) LAUNCH(3, true);
+            else LAUNCH(3, false);
+        }
+    }
+#undef LAUNCH
+    MM_LAUNCH_CHECK(ctx);
+    if (!update) return MM_OK;
+    double r[MM_MAX_PARTIALS];
+    const int K = 2 + ctx->D;
+    if ((rc = mm_fetch_reduction(ctx, K, r))) return rc;
+    out->sum_dG2 = r[0];
+    out->sum_mis2 = r[1];
+    for (int i = 0; i < 9; ++i) out->sum_lam[i] = i < ctx->D ? r[2 + i] : 0.0;
+    return MM_OK;
+}
+
+int mm_run_stencil(mm_ctx *ctx, int op) {
+    StageScope ss(ctx, MM_STAGE_OTHER);
+    const int threads = 256;
+    const int blocks = (int)std::min<int64_t>((ctx->M + threads - 1) / threads, 148 * 8);
+    const double inv2h = 1.0 / (2.0 * ctx->h);
+    if (op == 0) {
+        Mean9 um;
+        for (int i = 0; i < 9; ++i) um.v[i] = 0.0;
+        if (ctx->dim == 2)
+            k_grad<2, false><<<blocks, threads, 0, ctx->stream>>>(
+                ctx->Ut, ctx->G, ctx->F, ctx->Lam, ctx->n, ilog2(ctx->n), ctx->M, inv2h, 0.0, um, nullptr,
+                nullptr, nullptr);
+        else
+            k_grad<3, false><<<blocks, threads, 0, ctx->stream>>>(
+                ctx->Ut, ctx->G, ctx->F, ctx->Lam, ctx->n, ilog2(ctx->n), ctx->M, inv2h, 0.0, um, nullptr,
+                nullptr, nullptr);
+    } else {
+        if (ctx->dim == 2)
+            k_div<2><<<blocks, threads, 0, ctx->stream>>>(ctx->F, ctx->Ut, ctx->n, ilog2(ctx->n),
+                                                          ctx->M, inv2h);
+        else
+            k_div<3><<<blocks, threads, 0, ctx->stream>>>(ctx->F, ctx->Ut, ctx->n, ilog2(ctx->n),
+                                                          ctx->M, inv2h);
+    }
+    MM_LAUNCH_CHECK(ctx);
+    return MM_OK;
+}

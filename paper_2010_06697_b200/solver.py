@@ -1,0 +1,466 @@
+"""ADMM outer iteration on the device — drop-in for micromech/solver.py.
+
+Same public surface as the reference module (solver.py:45-59): parameters,
+residual record, state, local policies, ``init_state``, ``begin_time_step``,
+``outer_iteration``, ``solve``, ``equilibrium_residual``, ``macro_stress``.
+
+One outer iteration (solver.py:236-302) is, on the B200:
+  1. [LCE] frozen Frank force: one stencil kernel;
+  2. local step: one kernel launch per metered chunk (the policy decides on
+     the host from a 13-double reduction read back per chunk);
+  3. projection + multiplier ascent + residuals: six kernels (d-component
+     FFT pipeline and one fused gradient/update/reduction pass), one
+     11-double readback for r_p, r_d, the divergence guard and rho adaptation.
+Fields stay resident in HBM between iterations and across solve() calls on
+the same state; the host only ever sees reductions.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+from typing import NamedTuple
+
+import numpy as np
+
+from . import _lib
+from ._engine import STATE_FIELDS, Engine, field_shape
+from .errors import ConvergenceError, DivergenceError, ParameterError
+from .grid import Grid, forward_transform, mean_field, modified_symbols
+from .projection import MacroBC, macro_gradient
+
+__all__ = [
+    "SolverParams",
+    "Residuals",
+    "ADMMState",
+    "LocalPolicy",
+    "ExactAll",
+    "FractionConverged",
+    "RatioToDual",
+    "init_state",
+    "outer_iteration",
+    "solve",
+    "begin_time_step",
+    "equilibrium_residual",
+    "macro_stress",
+]
+
+
+@dataclass
+class SolverParams:
+    """Outer-loop tolerances and penalty schedule (solver.py:66-93)."""
+
+    r_p_tol: float = 1e-6
+    r_d_tol: float = 1e-6
+    r_l_tol: float | None = None
+    point_tol: float = 1e-11
+    max_outer: int = 20000
+    max_local: int = 2000
+    rho_init: float | None = None
+    rho_min_factor: float = 1e-3
+    kappa_adapt: float = 1.3
+    tau_adapt: float = 10.0
+    adapt: bool = True
+    divergence_limit: float = 1e8
+
+    def __post_init__(self):
+        if self.r_p_tol <= 0 or self.r_d_tol <= 0:
+            raise ParameterError("residual tolerances must be positive")
+        if self.kappa_adapt <= 1.0:
+            raise ParameterError("kappa_adapt must exceed 1")
+        if self.tau_adapt < 1.0:
+            raise ParameterError("tau_adapt must be at least 1")
+
+
+class Residuals(NamedTuple):
+    outer_iter: int
+    r_p: float
+    r_d: float
+    r_l: float
+    rho: float
+    wall_ms: float
+
+
+# ---------------------------------------------------------------------------
+# state: host views over device-resident fields
+# ---------------------------------------------------------------------------
+
+class ADMMState:
+    """Complete solver state (solver.py:105-121).
+
+    Field attributes (F, grad_u, lam, u_tilde, prev_F, internal, prev_internal)
+    are device-resident while the state is attached to an engine.  Reading one
+    downloads a numpy view; reading or assigning marks it to be uploaded again
+    before the next device operation, so in-place edits of a freshly read
+    array are honoured.  A view read before a solve is not updated by it —
+    read the attribute again afterwards.
+    """
+
+    _FIELD_NAMES = tuple(STATE_FIELDS)
+
+    def __init__(self, u_mean, u_tilde, grad_u, F, lam, internal, rho, outer_iter=0,
+                 r_d_prev=np.inf, total_sweeps=0, history=None, prev_F=None,
+                 prev_internal=None):
+        object.__setattr__(self, "_host", {})
+        object.__setattr__(self, "_dev", set())     # names valid on the device
+        object.__setattr__(self, "_stale", set())   # host copy out of date
+        object.__setattr__(self, "_dirty", set())   # host copy must be uploaded
+        object.__setattr__(self, "_engine", None)
+        self.u_mean = np.asarray(u_mean, dtype=float)
+        self.F = F
+        self.grad_u = grad_u
+        self.lam = lam
+        self.u_tilde = u_tilde
+        self.prev_F = prev_F
+        self.internal = internal if internal is not None else {}
+        self.prev_internal = prev_internal
+        self.rho = float(rho)
+        self.outer_iter = int(outer_iter)
+        self.r_d_prev = r_d_prev
+        self.total_sweeps = int(total_sweeps)
+        self.history = list(history) if history is not None else []
+
+    # -- field access ----------------------------------------------------------
+    def _get(self, name):
+        eng = self._engine
+        if name in self._stale and eng is not None:
+            grid = eng.grid
+            if name in STATE_FIELDS:
+                fid, rank = STATE_FIELDS[name]
+                self._host[name] = eng.ctx.download(fid, field_shape(grid, rank))
+            else:
+                self._host[name] = eng.model._download_internal(eng.ctx, name)
+            self._stale.discard(name)
+        val = self._host.get(name)
+        if val is not None:
+            self._dirty.add(name)
+        return val
+
+    def _set(self, name, value):
+        if value is not None and name in STATE_FIELDS:
+            value = np.asarray(value, dtype=float)
+        self._host[name] = value
+        self._stale.discard(name)
+        self._dev.discard(name)
+        if value is not None:
+            self._dirty.add(name)
+        else:
+            self._dirty.discard(name)
+
+    def _mark_device(self, *names):
+        """Fields just rewritten on the device: host copies are stale."""
+        for nm in names:
+            self._dev.add(nm)
+            self._stale.add(nm)
+            self._dirty.discard(nm)
+            self._host[nm] = None
+
+    def __getstate__(self):
+        for nm in list(self._stale):
+            self._get(nm)
+        d = {k: self._host.get(k) for k in self._FIELD_NAMES + ("internal", "prev_internal")}
+        d.update(u_mean=self.u_mean, rho=self.rho, outer_iter=self.outer_iter,
+                 r_d_prev=self.r_d_prev, total_sweeps=self.total_sweeps,
+                 history=list(self.history))
+        return d
+
+    def __setstate__(self, d):
+        self.__init__(d["u_mean"], d["u_tilde"], d["grad_u"], d["F"], d["lam"],
+                      d["internal"], d["rho"], d["outer_iter"], d["r_d_prev"],
+                      d["total_sweeps"], d["history"], d["prev_F"], d["prev_internal"])
+
+    # -- device attachment -------------------------------------------------------
+    def _attach(self, grid: Grid, model) -> Engine:
+        eng = self._engine
+        if eng is None or not eng.matches(grid):
+            if eng is not None:
+                # leaving an old engine: bring everything home first
+                for nm in list(self._stale):
+                    self._get(nm)
+            eng = Engine(grid)
+            object.__setattr__(self, "_engine", eng)
+            self._dev.clear()
+            self._stale.clear()
+            self._dirty.update(k for k, v in self._host.items() if v is not None)
+        eng.bind_model(model)
+        ctx = eng.ctx
+        d = grid.dim
+        for nm, (fid, rank) in STATE_FIELDS.items():
+            val = self._host.get(nm)
+            if nm in self._stale:
+                continue
+            if val is None:
+                continue
+            if nm in self._dirty or nm not in self._dev:
+                grid.check_field(val, rank, nm)
+                ctx.upload(fid, val)
+                self._dev.add(nm)
+                if nm == "lam":
+                    eng.lam_sum = None
+        for nm in ("internal", "prev_internal"):
+            if nm in self._stale:
+                continue
+            val = self._host.get(nm)
+            if val and (nm in self._dirty or nm not in self._dev):
+                model._upload_internal(ctx, nm, val)
+                self._dev.add(nm)
+        self._dirty.clear()
+        return eng
+
+
+def _field_property(name):
+    def fget(self):
+        return self._get(name)
+
+    def fset(self, value):
+        self._set(name, value)
+
+    return property(fget, fset)
+
+
+for _nm in ADMMState._FIELD_NAMES + ("internal", "prev_internal"):
+    setattr(ADMMState, _nm, _field_property(_nm))
+
+
+# ---------------------------------------------------------------------------
+# local inexactness policies (solver.py:128-199)
+# ---------------------------------------------------------------------------
+
+class LocalPolicy:
+    """Meters the local sweeps spent per outer iteration; ``target_tol`` is
+    the pointwise tolerance (relative to mu_rep), ``is_done`` judges a batch."""
+
+    name = "base"
+    chunk = 50
+
+    def target_tol(self, params: SolverParams, r_d_prev: float) -> float:
+        return params.point_tol
+
+    def is_done(self, stats, sweeps_total: int) -> bool:
+        raise NotImplementedError
+
+
+class ExactAll(LocalPolicy):
+    """Every point to the pointwise tolerance."""
+
+    name = "exact"
+    chunk = 50
+
+    def is_done(self, stats, sweeps_total):
+        return stats.converged_frac >= 1.0
+
+
+class FractionConverged(LocalPolicy):
+    """Stop once ``fraction`` of the points meet the tolerance, checking
+    every ``check_every`` sweeps."""
+
+    name = "fraction"
+
+    def __init__(self, fraction: float = 0.9, check_every: int = 2):
+        if not 0.0 < fraction <= 1.0:
+            raise ParameterError("fraction must lie in (0, 1]")
+        self.fraction = float(fraction)
+        self.chunk = int(check_every)
+
+    def is_done(self, stats, sweeps_total):
+        return stats.converged_frac >= self.fraction
+
+
+class RatioToDual(LocalPolicy):
+    """Pointwise tolerance tied to the previous dual residual: tol =
+    max(point_tol, ratio * r_d_prev), unbounded (1.0) before any r_d exists."""
+
+    name = "ratio"
+    chunk = 25
+
+    def __init__(self, ratio: float = 0.3):
+        if ratio <= 0:
+            raise ParameterError("ratio must be positive")
+        self.ratio = float(ratio)
+
+    def target_tol(self, params, r_d_prev):
+        if not np.isfinite(r_d_prev):
+            return 1.0
+        return max(params.point_tol, self.ratio * r_d_prev)
+
+    def is_done(self, stats, sweeps_total):
+        return stats.converged_frac >= 1.0
+
+
+_BUILTIN_POLICIES = (ExactAll, FractionConverged, RatioToDual)
+
+
+def _needs_points(policy) -> bool:
+    """Custom policies may inspect res_pts: keep per-point residuals then."""
+    return type(policy) not in _BUILTIN_POLICIES
+
+
+# ---------------------------------------------------------------------------
+# state setup and the outer iteration
+# ---------------------------------------------------------------------------
+
+def init_state(grid: Grid, model, bc: MacroBC, params: SolverParams, rng=None) -> ADMMState:
+    """Uniform state at the pinned macroscopic strain (solver.py:206-227)."""
+    d = grid.dim
+    if bc.strain_mask.shape != (d, d):
+        raise ParameterError("boundary control dimension mismatch")
+    Fbar0 = np.where(bc.strain_mask, bc.value, np.eye(d))
+    F = np.empty(grid.shape + (d, d))
+    F[...] = Fbar0
+    state = ADMMState(
+        u_mean=Fbar0.copy(), u_tilde=np.zeros(grid.shape + (d,)), grad_u=F.copy(), F=F,
+        lam=np.zeros(grid.shape + (d, d)), internal=model.init_internal(grid.npoints, rng),
+        rho=float(params.rho_init if params.rho_init is not None else model.mu_rep))
+    if state.rho <= 0:
+        raise ParameterError("initial penalty must be positive")
+    return state
+
+
+def begin_time_step(state: ADMMState):
+    """Freeze the current fields as the previous-step reference
+    (solver.py:230-233); device-to-device copies when the state is resident."""
+    eng = state._engine
+    resident = eng is not None and "F" in state._dev and "F" not in state._dirty
+    if resident:
+        eng.ctx.copy_field(_lib.FIELD_PREV_F, _lib.FIELD_F)
+        state._mark_device("prev_F")
+    else:
+        state.prev_F = state.F.copy()
+    model = eng.model if eng is not None else None
+    if (resident and model is not None and hasattr(model, "_copy_internal_to_prev")
+            and "internal" in state._dev and "internal" not in state._dirty):
+        model._copy_internal_to_prev(eng.ctx)
+        state._mark_device("prev_internal")
+    else:
+        state.prev_internal = {k: v.copy() for k, v in state.internal.items()}
+
+
+def outer_iteration(grid: Grid, model, state: ADMMState, params: SolverParams, bc: MacroBC,
+                    policy: LocalPolicy, dt: float = 0.0, freqs=None) -> Residuals:
+    """One splitting round on the device; updates state in place
+    (solver.py:236-302)."""
+    t_start = time.perf_counter()
+    if bc.dim != grid.dim:
+        from .errors import ConfigurationError
+        raise ConfigurationError(f"MacroBC dim {bc.dim} does not match grid dim {grid.dim}")
+    eng = state._attach(grid, model)
+    ctx = eng.ctx
+    d = grid.dim
+    npts = grid.npoints
+    mu_rep = model.mu_rep
+
+    if hasattr(model, "_device_prepare_frozen"):
+        model._device_prepare_frozen(ctx)
+
+    # ---- step 1: metered local solves (solver.py:252-266)
+    tol_pt = policy.target_tol(params, state.r_d_prev)
+    want_points = _needs_points(policy)
+    local_kw = {}
+    if getattr(model, "_material_id", None) == _lib.MAT_LCE:
+        local_kw["viscous_ready"] = "prev_F" in state._dev and "prev_internal" in state._dev
+    sweeps_total = 0
+    while True:
+        chunk = min(policy.chunk, params.max_local - sweeps_total)
+        stats = model._device_local(ctx, npts, state.rho, dt, chunk, tol_pt, want_points,
+                                    **local_kw)
+        sweeps_total += stats.sweeps
+        if (policy.is_done(stats, sweeps_total) or stats.sweeps < chunk
+                or sweeps_total >= params.max_local):
+            break
+    state.total_sweeps += sweeps_total
+    state._mark_device("F")
+    if getattr(model, "_material_id", None) == _lib.MAT_LCE:
+        state._mark_device("internal")
+    r_l = float(np.sqrt(stats.sum_res2 / npts)) / mu_rep
+
+    # ---- step 2 + 3: projection, dual residual, multiplier ascent (:268-279)
+    F_mean = (stats.sum_F[: d * d] / npts).reshape(d, d)
+    u_mean = macro_gradient(bc, F_mean, eng.lam_mean(), state.rho)
+    up = ctx.project_update(state.rho, u_mean)
+    state._mark_device("grad_u", "lam", "u_tilde")
+    eng.lam_sum = np.array(up.sum_lam[: d * d])
+    r_d = state.rho * float(np.sqrt(up.sum_dG2 / npts)) / mu_rep
+    r_p = float(np.sqrt(up.sum_mis2 / npts))
+    state.u_mean = u_mean
+
+    state.outer_iter += 1
+    state.r_d_prev = r_d
+
+    if not np.isfinite(r_p) or r_p > params.divergence_limit:
+        raise DivergenceError(f"primal residual {r_p:.3e} at outer iteration {state.outer_iter}")
+
+    # ---- penalty rebalancing (:288-296)
+    if params.adapt and state.outer_iter > 1:
+        rho_ref = params.rho_init if params.rho_init is not None else model.mu_rep
+        if r_p > params.tau_adapt * r_d:
+            state.rho *= params.kappa_adapt
+        elif r_d > params.tau_adapt * r_p:
+            state.rho = max(state.rho / params.kappa_adapt, params.rho_min_factor * rho_ref)
+
+    wall_ms = (time.perf_counter() - t_start) * 1e3
+    resid = Residuals(state.outer_iter, float(r_p), float(r_d), float(r_l), float(state.rho),
+                      wall_ms)
+    state.history.append(resid)
+    return resid
+
+
+def solve(grid: Grid, model, bc: MacroBC, params: SolverParams,
+          policy: LocalPolicy | None = None, state: ADMMState | None = None, dt: float = 0.0,
+          rng=None, callback=None, raise_on_max: bool = True):
+    """Iterate to joint primal/dual/local tolerance; returns (state, converged)
+    (solver.py:305-339)."""
+    if policy is None:
+        policy = ExactAll()
+    if state is None:
+        state = init_state(grid, model, bc, params, rng)
+    r_l_tol = params.r_l_tol if params.r_l_tol is not None else max(params.r_p_tol,
+                                                                   params.r_d_tol)
+    converged = False
+    resid = None
+    for _ in range(params.max_outer):
+        resid = outer_iteration(grid, model, state, params, bc, policy, dt=dt)
+        if callback is not None:
+            callback(state, resid)
+        if resid.r_p <= params.r_p_tol and resid.r_d <= params.r_d_tol and resid.r_l <= r_l_tol:
+            converged = True
+            break
+    if not converged and raise_on_max:
+        raise ConvergenceError(
+            f"no convergence in {params.max_outer} outer iterations "
+            f"(r_p={resid.r_p:.3e}, r_d={resid.r_d:.3e})" if resid is not None else
+            "no outer iterations allowed", history=state.history)
+    return state, converged
+
+
+# ---------------------------------------------------------------------------
+# diagnostics
+# ---------------------------------------------------------------------------
+
+def equilibrium_residual(grid: Grid, model, state: ADMMState, dt: float = 0.0) -> float:
+    """H^-1-type norm of div P (solver.py:346-371); post-convergence
+    diagnostic evaluated on host views of the state."""
+    d = grid.dim
+    npts = grid.npoints
+    prev = state.prev_F
+    Pf = model.stress_total(state.F.reshape(npts, d, d), state.internal,
+                            prev.reshape(npts, d, d) if prev is not None else None,
+                            state.prev_internal, dt)
+    P = Pf.reshape(grid.shape + (d, d))
+    freqs = modified_symbols(grid)
+    Phat = forward_transform(grid, P)
+    divhat = np.einsum("...ij,...j->...i", Phat, freqs.grad_sym)
+    gsq = freqs.grad_sq
+    live = gsq > 1e-14 * gsq.max()
+    w = np.where(live, 1.0 / np.where(live, gsq, 1.0), 0.0)
+    total = np.sum(np.abs(divhat) ** 2 * w[..., None])
+    return float(np.sqrt(total) / npts)
+
+
+def macro_stress(grid: Grid, state: ADMMState) -> np.ndarray:
+    """Volume average of the multiplier (solver.py:374-377); from the device
+    reduction when the state is resident."""
+    eng = state._engine
+    if eng is not None and eng.matches(grid) and "lam" in state._dev \
+            and "lam" not in state._dirty:
+        return eng.lam_mean().copy()
+    return mean_field(grid, state.lam)
