@@ -259,22 +259,64 @@ __global__ void k_row_fwd(const double *__restrict__ F, const double *__restrict
     double2 *scr = smem_c + (size_t)(g.N + 1) * LD;
     const int64_t row0 = (int64_t)blockIdx.x * rows;
     const int N = g.N;
-    // pack: line = c * rows + r
-    for (int w = threadIdx.x; w < TK * N; w += blockDim.x) {
-        const int line = w / N, m = w - line * N;
-        const int c = line / rows, r = line - c * rows;
-        const int64_t row = row0 + r;
-        double2 z = make_double2(0.0, 0.0);
-        if (row < g.nrows) {
+    // pack: line = c * rows + r.  A work item is (row r, complex slot m) and
+    // produces the slot for every component, so the neighbour-row offsets
+    // are computed once and all loads are issued before any arithmetic.
+    const double irho = 1.0 / rho;
+    if (g.packed) {
+        for (int w = threadIdx.x; w < rows * N; w += blockDim.x) {
+            const int r = w / N, m = w - r * N;
+            const int64_t row = row0 + r;
+            if (row >= g.nrows) {
+                for (int c = 0; c < g.dim; ++c) buf[m * LD + c * rows + r] = make_double2(0.0, 0.0);
+                continue;
+            }
             const RowNbr nb = row_nbrs(g, (int)row);
-            if (g.packed) {
-                z.x = div_at(F, L, rho, g, c, nb, 2 * m);
-                z.y = div_at(F, L, rho, g, c, nb, 2 * m + 1);
-            } else {
-                z.x = div_at(F, L, rho, g, c, nb, m);
+            const int n = g.n;
+            const int x0 = 2 * m, x1 = 2 * m + 1;
+            const int xm = (x0 == 0) ? n - 1 : x0 - 1;
+            const int xp = (x1 + 1 == n) ? 0 : x1 + 1;
+            for (int c = 0; c < g.dim; ++c) {
+                const int d = g.dim;
+                const int64_t cz = (int64_t)(c * d) * g.M;          // T_c0 (axis 0)
+                const int64_t cy = (int64_t)(c * d + 1) * g.M;      // T_c1 (axis 1, 3D)
+                const int64_t cx = (int64_t)(c * d + d - 1) * g.M + nb.self;  // contiguous
+                // all loads first
+                const double fxm = __ldg(&F[cx + xm]), lxm = __ldg(&L[cx + xm]);
+                const double fx0 = __ldg(&F[cx + x0]), lx0 = __ldg(&L[cx + x0]);
+                const double fx1 = __ldg(&F[cx + x1]), lx1 = __ldg(&L[cx + x1]);
+                const double fxp = __ldg(&F[cx + xp]), lxp = __ldg(&L[cx + xp]);
+                const double fzp0 = __ldg(&F[cz + nb.zp + x0]), lzp0 = __ldg(&L[cz + nb.zp + x0]);
+                const double fzp1 = __ldg(&F[cz + nb.zp + x1]), lzp1 = __ldg(&L[cz + nb.zp + x1]);
+                const double fzm0 = __ldg(&F[cz + nb.zm + x0]), lzm0 = __ldg(&L[cz + nb.zm + x0]);
+                const double fzm1 = __ldg(&F[cz + nb.zm + x1]), lzm1 = __ldg(&L[cz + nb.zm + x1]);
+                double y0 = 0.0, y1 = 0.0;
+                if (d == 3) {
+                    const double fyp0 = __ldg(&F[cy + nb.yp + x0]), lyp0 = __ldg(&L[cy + nb.yp + x0]);
+                    const double fyp1 = __ldg(&F[cy + nb.yp + x1]), lyp1 = __ldg(&L[cy + nb.yp + x1]);
+                    const double fym0 = __ldg(&F[cy + nb.ym + x0]), lym0 = __ldg(&L[cy + nb.ym + x0]);
+                    const double fym1 = __ldg(&F[cy + nb.ym + x1]), lym1 = __ldg(&L[cy + nb.ym + x1]);
+                    y0 = (fyp0 - lyp0 * irho) - (fym0 - lym0 * irho);
+                    y1 = (fyp1 - lyp1 * irho) - (fym1 - lym1 * irho);
+                }
+                // T = F - lam/rho (projection.py:154), as F - lam * (1/rho)
+                double2 z;
+                z.x = ((fzp0 - lzp0 * irho) - (fzm0 - lzm0 * irho)) + y0 +
+                      ((fx1 - lx1 * irho) - (fxm - lxm * irho));
+                z.y = ((fzp1 - lzp1 * irho) - (fzm1 - lzm1 * irho)) + y1 +
+                      ((fxp - lxp * irho) - (fx0 - lx0 * irho));
+                buf[m * LD + c * rows + r] = z;
             }
         }
-        buf[m * LD + line] = z;
+    } else {
+        for (int w = threadIdx.x; w < TK * N; w += blockDim.x) {
+            const int line = w / N, m = w - line * N;
+            const int c = line / rows, r = line - c * rows;
+            const int64_t row = row0 + r;
+            double2 z = make_double2(0.0, 0.0);
+            if (row < g.nrows) z.x = div_at(F, L, rho, g, c, row_nbrs(g, (int)row), m);
+            buf[m * LD + line] = z;
+        }
     }
     __syncthreads();
     line_transform<N1, N2, TK, false>(buf, scr, N, tw_line);
@@ -482,27 +524,42 @@ k_grad(const double *__restrict__ Ut, double *__restrict__ G, const double *__re
         // neighbour offsets along each axis (periodic)
         int off_p[DIM], off_m[DIM];
         nbr_offsets<DIM>(p, n, lgn, off_p, off_m);
+        // issue every load before any store (G and Lam are read and written)
+        double up[D], um_[D];
 #pragma unroll
         for (int i = 0; i < DIM; ++i) {
             const double *u = Ut + (int64_t)i * M + p;
 #pragma unroll
             for (int j = 0; j < DIM; ++j) {
-                const double gfl = (__ldg(u + off_p[j]) - __ldg(u + off_m[j])) * inv2h;
-                const int c = i * DIM + j;
-                const double gnew = gfl + um.v[c];  // projection.py:168
+                up[i * DIM + j] = __ldg(u + off_p[j]);
+                um_[i * DIM + j] = __ldg(u + off_m[j]);
+            }
+        }
+        double gold[D], fv[D], lv[D];
+        if (UPDATE) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
                 const int64_t o = (int64_t)c * M + p;
-                if (UPDATE) {
-                    const double dg = gnew - G[o];
-                    const double mis = gnew - F[o];  // solver.py:277
-                    const double lnew = Lam[o] + rho * mis;  // solver.py:279
-                    G[o] = gnew;
-                    Lam[o] = lnew;
-                    acc[0] += dg * dg;
-                    acc[1] += mis * mis;
-                    acc[2 + c] += lnew;
-                } else {
-                    G[o] = gnew;
-                }
+                gold[c] = G[o];
+                fv[c] = __ldg(&F[o]);
+                lv[c] = Lam[o];
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            const double gnew = (up[c] - um_[c]) * inv2h + um.v[c];  // projection.py:168
+            const int64_t o = (int64_t)c * M + p;
+            if (UPDATE) {
+                const double dg = gnew - gold[c];
+                const double mis = gnew - fv[c];          // solver.py:277
+                const double lnew = lv[c] + rho * mis;    // solver.py:279
+                G[o] = gnew;
+                Lam[o] = lnew;
+                acc[0] += dg * dg;
+                acc[1] += mis * mis;
+                acc[2 + c] += lnew;
+            } else {
+                G[o] = gnew;
             }
         }
     }
