@@ -58,7 +58,8 @@ enum mm_field {
     MM_FIELD_FF = 11,    /* LCE frozen Frank force (npts,d)      lce.py:223-229 */
     MM_FIELD_PREV_ANG = 12,   /* prev_internal["angles"] */
     MM_FIELD_PREV_CHART = 13, /* prev_internal["chart"] */
-    MM_FIELD_COUNT = 14
+    MM_FIELD_PREV_PINC = 14,  /* prev_internal["p_inc"] */
+    MM_FIELD_COUNT = 15
 };
 
 /* Materials for mm_local_sweeps. */
@@ -164,6 +165,10 @@ int mm_download_points(mm_ctx *ctx, double *res, int64_t *nsw, uint8_t *ok, int6
  * Frank force 2 kappa (D^T D) n as the exact radius-2 real-space stencil
  * (equal to the reference's spectral form, lce.py:213-221). */
 int mm_prepare_frozen(mm_ctx *ctx);
+/* The same stencil applied to a director field the caller uploaded into the
+ * MM_FIELD_FF slot (LiquidCrystalElastomer.frank_force, lce.py:213-221);
+ * the force replaces it in that slot. */
+int mm_frank_stencil(mm_ctx *ctx);
 
 /* Helmholtz projection of (F, lam) (projection.py:132-168): writes
  * u_tilde and grad_u = u_mean + D u_tilde on the device.  u_mean (d*d,

@@ -27,6 +27,7 @@ MM_OK, MM_ERR_PARAM, MM_ERR_CONFIG, MM_ERR_INADMISSIBLE, MM_ERR_DIVERGED, MM_ERR
 
 FIELD_F, FIELD_G, FIELD_LAM, FIELD_UT, FIELD_PREV_F, FIELD_MOD_A, FIELD_MOD_B = range(7)
 FIELD_ANG, FIELD_CHART, FIELD_PINC, FIELD_N0, FIELD_FF, FIELD_PREV_ANG, FIELD_PREV_CHART = range(7, 14)
+FIELD_PREV_PINC = 14
 
 MAT_MR, MAT_QUADRATIC, MAT_LCE, MAT_MR_DESCENT = range(4)
 
@@ -36,7 +37,7 @@ EXPORTS = (
     "mm_synchronize", "mm_device_bytes", "mm_upload", "mm_download", "mm_copy_field",
     "mm_field_sums", "mm_set_symbols", "mm_local_sweeps", "mm_set_lce", "mm_download_points",
     "mm_prepare_frozen", "mm_project", "mm_project_update", "mm_stencil",
-    "mm_profile_enable", "mm_profile_read",
+    "mm_profile_enable", "mm_profile_read", "mm_frank_stencil",
 )
 
 STAGES = ("local", "row_fwd", "col_fwd", "col_solve", "col_inv", "row_inv", "grad", "frozen",
@@ -103,6 +104,7 @@ def load_library():
             "mm_project_update": ([P, D, P, ctypes.POINTER(UpdateStatsC)], I),
             "mm_stencil": ([P, I], I),
             "mm_profile_enable": ([P, I], I),
+            "mm_frank_stencil": ([P], I),
             "mm_profile_read": ([P, ctypes.POINTER(ProfileC), I], I),
         }
         for name, (args, res) in sig.items():

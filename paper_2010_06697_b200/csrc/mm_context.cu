@@ -136,6 +136,7 @@ static int field_info(mm_ctx *ctx, int field, double ***slot, int *ncomp) {
         case MM_FIELD_PREV_CHART:
             if (d != 3) return mm_fail(ctx, MM_ERR_CONFIG, "chart exists only in 3D");
             *slot = &ctx->prevChart; *ncomp = 9; break;
+        case MM_FIELD_PREV_PINC: *slot = &ctx->prevPinc; *ncomp = 1; break;
         default: return mm_fail(ctx, MM_ERR_CONFIG, "unknown field id %d", field);
     }
     return MM_OK;
@@ -333,7 +334,7 @@ void mm_destroy(mm_ctx *ctx) {
     for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
     double *ptrs[] = {ctx->F, ctx->G, ctx->Lam, ctx->Ut, ctx->prevF, ctx->modA, ctx->modB,
                       ctx->ang, ctx->chart, ctx->pinc, ctx->n0, ctx->ff, ctx->prevAng,
-                      ctx->prevChart, ctx->nk, ctx->sym, ctx->partials, ctx->red_out,
+                      ctx->prevChart, ctx->prevPinc, ctx->dirbuf, ctx->sym, ctx->partials, ctx->red_out,
                       ctx->res, ctx->tstate, ctx->stage};
     for (double *p : ptrs)
         if (p) cudaFree(p);
@@ -531,6 +532,14 @@ int mm_project_update(mm_ctx *ctx, double rho, const double *u_mean, mm_update_s
     if (!ctx->have_sym) return mm_fail(ctx, MM_ERR_CONFIG, "symbols were never set");
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
     return mm_run_project(ctx, rho, u_mean, 1, out);
+}
+
+int mm_frank_stencil(mm_ctx *ctx) {
+    if (!ctx) return MM_ERR_PARAM;
+    if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
+    if (!ctx->have_lce) return mm_fail(ctx, MM_ERR_CONFIG, "LCE parameters were never set");
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    return mm_run_frank_of_ff(ctx);
 }
 
 int mm_stencil(mm_ctx *ctx, int op) {

@@ -29,7 +29,7 @@ struct mm_ctx {
     double *modA = nullptr, *modB = nullptr;
     // LCE internal / frozen
     double *ang = nullptr, *chart = nullptr, *pinc = nullptr, *n0 = nullptr, *ff = nullptr;
-    double *prevAng = nullptr, *prevChart = nullptr, *nk = nullptr;
+    double *prevAng = nullptr, *prevChart = nullptr, *prevPinc = nullptr, *dirbuf = nullptr;
     bool have_prev_F = false, have_prev_int = false;
     mm_lce_params lce{};
     bool have_lce = false;
@@ -207,3 +207,4 @@ int mm_run_frozen(mm_ctx *ctx);
 int mm_run_field_sums(mm_ctx *ctx, const double *field, int ncomp, double *out);
 int mm_check_det(mm_ctx *ctx, int *bad);
 int mm_run_stencil(mm_ctx *ctx, int op);
+int mm_run_frank_of_ff(mm_ctx *ctx);

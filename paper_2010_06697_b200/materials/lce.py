@@ -8,10 +8,12 @@
 
 Host side: parameters, director storage, closed forms for diagnostics.
 Device side (csrc/mm_lce.cu): the joint damped-Newton local kernels
-(lce.py:371-584 in 2D, 5x5; lce.py:676-995 in 3D, 11x11), built without FMA
-contraction and with correctly rounded sin/cos so their arithmetic follows the
-reference kernels bit for bit, and the frozen Frank force as the exact
-radius-2 real-space stencil of 2 kappa (D^T D) n (lce.py:213-229).
+(lce.py:371-584 in 2D, 5x5; lce.py:676-995 in 3D, 11x11) in the reference's
+operation order, and the frozen Frank force as the exact radius-2 real-space
+stencil of 2 kappa (D^T D) n (lce.py:213-229).  The Newton iterations of
+non-converging (polydomain) points are chaotic: an ulp-level difference in
+sin/cos grows to O(1) within ~50 sweeps, so parity is pinned per call, on
+local-convergent configurations, and statistically.
 """
 
 from __future__ import annotations
@@ -198,10 +200,41 @@ class LiquidCrystalElastomer(MaterialModel):
         ctx.upload(_lib.FIELD_N0, self.n0)
         ctx.set_lce(**self._scalars(0.0))
 
-    def _device_local(self, ctx, npts, rho, dt, max_sweeps, point_tol, want_points=False,
-                      viscous_ready=True):
-        if dt > 0.0 and (self.nu_F > 0.0 or self.nu_n > 0.0) and not viscous_ready:
-            raise ParameterError("viscous update needs the previous step (begin_time_step)")
+    # -- state <-> device (used by ADMMState) ----------------------------------
+    _INTERNAL_FIELDS = {"angles": _lib.FIELD_ANG, "chart": _lib.FIELD_CHART,
+                        "p_inc": _lib.FIELD_PINC}
+    _PREV_FIELDS = {"angles": _lib.FIELD_PREV_ANG, "chart": _lib.FIELD_PREV_CHART,
+                    "p_inc": _lib.FIELD_PREV_PINC}
+
+    def _internal_shapes(self, npts):
+        shp = {"p_inc": (npts,)}
+        if self.dim == 2:
+            shp["angles"] = (npts,)
+        else:
+            shp["angles"] = (npts, 2)
+            shp["chart"] = (npts, 3, 3)
+        return shp
+
+    def _upload_internal(self, ctx, which, val):
+        fields = self._INTERNAL_FIELDS if which == "internal" else self._PREV_FIELDS
+        for k, fid in fields.items():
+            if k in val and val[k] is not None:
+                ctx.upload(fid, val[k])
+
+    def _download_internal(self, ctx, which):
+        fields = self._INTERNAL_FIELDS if which == "internal" else self._PREV_FIELDS
+        shp = self._internal_shapes(ctx.npts)
+        return {k: ctx.download(fields[k], shp[k]) for k in shp}
+
+    def _copy_internal_to_prev(self, ctx):
+        for k in self._internal_shapes(ctx.npts):
+            ctx.copy_field(self._PREV_FIELDS[k], self._INTERNAL_FIELDS[k])
+
+    def _device_prepare_frozen(self, ctx):
+        ctx.set_lce(**self._scalars(0.0))
+        ctx.prepare_frozen()
+
+    def _device_local(self, ctx, npts, rho, dt, max_sweeps, point_tol, want_points=False):
         ctx.set_lce(**self._scalars(dt))
         tol = point_tol * self.mu_rep
         st = ctx.local_sweeps(self._material_id, rho, tol, max_sweeps, 0.0, want_points)
@@ -254,9 +287,7 @@ class LiquidCrystalElastomer(MaterialModel):
         ctx.upload(_lib.FIELD_FF, np.zeros((npts, d)) if ff is None else ff)
         if viscous:
             ctx.upload(_lib.FIELD_PREV_F, np.asarray(prev_F).reshape(npts, d * d))
-            ctx.upload(_lib.FIELD_PREV_ANG, prev_internal["angles"])
-            if d == 3:
-                ctx.upload(_lib.FIELD_PREV_CHART, prev_internal["chart"])
+            self._upload_internal(ctx, "prev_internal", prev_internal)
         st = self._device_local(ctx, npts, rho, dt, max_sweeps, point_tol, True)
         F[...] = ctx.download(_lib.FIELD_F, (npts, d, d)).reshape(F.shape)
         internal["angles"][...] = ctx.download(_lib.FIELD_ANG, internal["angles"].shape)

@@ -355,14 +355,15 @@ def outer_iteration(grid: Grid, model, state: ADMMState, params: SolverParams, b
     # ---- step 1: metered local solves (solver.py:252-266)
     tol_pt = policy.target_tol(params, state.r_d_prev)
     want_points = _needs_points(policy)
-    local_kw = {}
-    if getattr(model, "_material_id", None) == _lib.MAT_LCE:
-        local_kw["viscous_ready"] = "prev_F" in state._dev and "prev_internal" in state._dev
+    if getattr(model, "_material_id", None) == _lib.MAT_LCE and dt > 0.0 and \
+            (model.nu_F > 0.0 or model.nu_n > 0.0) and \
+            (state._host.get("prev_F") is None and "prev_F" not in state._dev
+             or not state._host.get("prev_internal") and "prev_internal" not in state._dev):
+        raise ParameterError("viscous update needs the previous step (begin_time_step)")
     sweeps_total = 0
     while True:
         chunk = min(policy.chunk, params.max_local - sweeps_total)
-        stats = model._device_local(ctx, npts, state.rho, dt, chunk, tol_pt, want_points,
-                                    **local_kw)
+        stats = model._device_local(ctx, npts, state.rho, dt, chunk, tol_pt, want_points)
         sweeps_total += stats.sweeps
         if (policy.is_done(stats, sweeps_total) or stats.sweeps < chunk
                 or sweeps_total >= params.max_local):
