@@ -1,0 +1,51 @@
+"""LCE local-step timing on a polydomain director field.
+
+python tools/lce_perf.py [n] [max_local] [dim]
+"""
+
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402  (only to generate the seeded polydomain n0, as the reference does)
+import paper_2010_06697_b200 as mm  # noqa: E402
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+    max_local = int(sys.argv[2]) if len(sys.argv) > 2 else 2000
+    dim = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    grid = mm.Grid(dim, n, 0.5)
+    t0 = time.perf_counter()
+    n0 = oracle.polydomain_n0(dim, n, 0.5, 0.25, seed=1)
+    m = mm.LiquidCrystalElastomer(mu=1.0, r=2.0, alpha=0.1, frank_kappa=1e-4, n0=n0, dim=dim)
+    bc = mm.MacroBC.stress(np.zeros((dim, dim)))
+    params = mm.SolverParams(max_outer=2, max_local=max_local)
+    st = mm.solver.init_state(grid, m, bc, params)
+    st.F = st.F + 1e-3 * np.random.default_rng(1).standard_normal(st.F.shape)
+    print(f"setup {time.perf_counter() - t0:.1f} s", flush=True)
+    pol = mm.RatioToDual(0.3)
+    r = mm.solver.outer_iteration(grid, m, st, params, bc, pol)
+    ctx = st._engine.ctx
+    ctx.synchronize()
+    ctx.profile_read(reset=True)
+    ctx.profile_enable(True)
+    t0 = time.perf_counter()
+    r = mm.solver.outer_iteration(grid, m, st, params, bc, pol)
+    ctx.synchronize()
+    wall = time.perf_counter() - t0
+    ms, nl = ctx.profile_read(reset=True)
+    sw = st.total_sweeps
+    print(f"{dim}D LCE n={n}: outer iteration {wall * 1e3:.1f} ms, residuals {r}, "
+          f"total sweeps {sw}", flush=True)
+    print({k: round(v, 3) for k, v in ms.items() if v}, nl)
+    print(f"voxel-iter/s {grid.npoints / wall:.3e}")
+
+
+if __name__ == "__main__":
+    main()
