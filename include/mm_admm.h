@@ -186,6 +186,13 @@ int mm_project_update(mm_ctx *ctx, double rho, const double *u_mean, mm_update_s
 int mm_profile_enable(mm_ctx *ctx, int on);
 int mm_profile_read(mm_ctx *ctx, mm_profile *out, int reset);
 
+/* Options.  MM_OPT_IMPLICIT_GRAD (default 0): after a fused projection keep
+ * grad_u implicitly as u_mean + D u_tilde instead of storing the 9-component
+ * field (the local step and the next update rebuild it with the same
+ * stencil expression; a download materialises it). */
+enum mm_option { MM_OPT_IMPLICIT_GRAD = 0 };
+int mm_set_option(mm_ctx *ctx, int option, int64_t value);
+
 /* Central-difference stencils on the grid fields (grid.py:227-249):
  * op 0: grad_u = D u_tilde (discrete_grad);  op 1: u_tilde = div F
  * (discrete_div).  Both equal the reference's spectral forms to roundoff. */

@@ -2,12 +2,14 @@
 an ADMMState's host views and its device-resident fields consistent.
 
 Ownership model: during solve() the fields live in HBM in SoA
-layout; ADMMState attributes materialise host numpy views on demand (D2H),
-and assigning (or reading, since the caller may mutate the returned array in
-place) marks the field for re-upload before the next device operation.
+layout; ADMMState attributes materialise read-only host numpy snapshots on
+demand (D2H), and assigning a new array marks the field for upload before the
+next device operation.
 """
 
 from __future__ import annotations
+
+import os
 
 import numpy as np
 
@@ -32,6 +34,8 @@ class Engine:
         self.ctx = _lib.Context(grid.dim, n=grid.n, length=grid.length, device=device)
         tab, thresh = axis_symbol_tables(grid)
         self.ctx.set_symbols(tab, thresh)
+        # grad_u storage policy (include/mm_admm.h, MM_OPT_IMPLICIT_GRAD)
+        self.ctx.set_option(0, int(os.environ.get("MM_IMPLICIT_GRAD", "0")))
         self.model = None          # model whose parameters are on the device
         self.model_version = None
         self.lam_sum = None        # device-side sum of lam (None: recompute)

@@ -37,7 +37,7 @@ EXPORTS = (
     "mm_synchronize", "mm_device_bytes", "mm_upload", "mm_download", "mm_copy_field",
     "mm_field_sums", "mm_set_symbols", "mm_local_sweeps", "mm_set_lce", "mm_download_points",
     "mm_prepare_frozen", "mm_project", "mm_project_update", "mm_stencil",
-    "mm_profile_enable", "mm_profile_read", "mm_frank_stencil",
+    "mm_profile_enable", "mm_profile_read", "mm_frank_stencil", "mm_set_option",
 )
 
 STAGES = ("local", "row_fwd", "col_fwd", "col_solve", "col_inv", "row_inv", "grad", "frozen",
@@ -105,6 +105,7 @@ def load_library():
             "mm_stencil": ([P, I], I),
             "mm_profile_enable": ([P, I], I),
             "mm_frank_stencil": ([P], I),
+            "mm_set_option": ([P, I, I64], I),
             "mm_profile_read": ([P, ctypes.POINTER(ProfileC), I], I),
         }
         for name, (args, res) in sig.items():
@@ -258,3 +259,6 @@ class Context:
         self.check(self.lib.mm_profile_read(self.h, ctypes.byref(p), 1 if reset else 0))
         return ({s: p.ms[i] for i, s in enumerate(STAGES)},
                 {s: int(p.launches[i]) for i, s in enumerate(STAGES)})
+
+    def set_option(self, option, value):
+        self.check(self.lib.mm_set_option(self.h, int(option), int(value)))

@@ -334,7 +334,7 @@ void mm_destroy(mm_ctx *ctx) {
     for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
     double *ptrs[] = {ctx->F, ctx->G, ctx->Lam, ctx->Ut, ctx->prevF, ctx->modA, ctx->modB,
                       ctx->ang, ctx->chart, ctx->pinc, ctx->n0, ctx->ff, ctx->prevAng,
-                      ctx->prevChart, ctx->prevPinc, ctx->dirbuf, ctx->sym, ctx->partials, ctx->red_out,
+                      ctx->prevChart, ctx->prevPinc, ctx->dirbuf, ctx->Ut2, ctx->sym, ctx->partials, ctx->red_out,
                       ctx->res, ctx->tstate, ctx->stage};
     for (double *p : ptrs)
         if (p) cudaFree(p);
@@ -398,6 +398,15 @@ int mm_upload(mm_ctx *ctx, int field, const double *host, int64_t count) {
     if (field == MM_FIELD_F) ctx->F_checked = false;
     if (field == MM_FIELD_PREV_F) ctx->have_prev_F = true;
     if (field == MM_FIELD_PREV_ANG) ctx->have_prev_int = true;
+    if (field == MM_FIELD_UT && ctx->g_implicit) {
+        // grad_u was held as ubar + D u_tilde: pin it before u_tilde changes
+        if ((rc = mm_materialize_G(ctx))) return rc;
+        ctx->g_implicit = false;
+    }
+    if (field == MM_FIELD_G) {
+        ctx->g_implicit = false;
+        ctx->g_buf_valid = true;
+    }
     return transfer(ctx, *slot, ncomp, host, nullptr);
 }
 
@@ -412,6 +421,7 @@ int mm_download(mm_ctx *ctx, int field, double *host, int64_t count) {
                        (long long)count, (long long)(ctx->M * ncomp));
     if (!*slot) return mm_fail(ctx, MM_ERR_CONFIG, "field %d was never set", field);
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    if (field == MM_FIELD_G && (rc = mm_materialize_G(ctx))) return rc;
     return transfer(ctx, *slot, ncomp, nullptr, host);
 }
 
@@ -426,6 +436,13 @@ int mm_copy_field(mm_ctx *ctx, int dst_field, int src_field) {
     if (nd != ns) return mm_fail(ctx, MM_ERR_CONFIG, "field shapes differ");
     if (!*ss) return mm_fail(ctx, MM_ERR_CONFIG, "source field %d was never set", src_field);
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    if ((src_field == MM_FIELD_G || dst_field == MM_FIELD_UT) && (rc = mm_materialize_G(ctx)))
+        return rc;
+    if (dst_field == MM_FIELD_UT) ctx->g_implicit = false;
+    if (dst_field == MM_FIELD_G) {
+        ctx->g_implicit = false;
+        ctx->g_buf_valid = true;
+    }
     rc = ensure_field(ctx, ds, nd);
     if (rc) return rc;
     MM_CUDA(ctx, cudaMemcpyAsync(*ds, *ss, sizeof(double) * nd * ctx->M,
@@ -532,6 +549,23 @@ int mm_project_update(mm_ctx *ctx, double rho, const double *u_mean, mm_update_s
     if (!ctx->have_sym) return mm_fail(ctx, MM_ERR_CONFIG, "symbols were never set");
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
     return mm_run_project(ctx, rho, u_mean, 1, out);
+}
+
+int mm_set_option(mm_ctx *ctx, int option, int64_t value) {
+    if (!ctx) return MM_ERR_PARAM;
+    switch (option) {
+        case MM_OPT_IMPLICIT_GRAD: {
+            const bool on = value != 0;
+            if (!on && ctx->g_implicit) {
+                int rc = mm_materialize_G(ctx);
+                if (rc) return rc;
+                ctx->g_implicit = false;
+            }
+            ctx->opt_implicit_g = on;
+            return MM_OK;
+        }
+        default: return mm_fail(ctx, MM_ERR_PARAM, "unknown option %d", option);
+    }
 }
 
 int mm_frank_stencil(mm_ctx *ctx) {

@@ -70,6 +70,14 @@ struct mm_ctx {
     };
     std::vector<PendingTiming> pending;
     std::vector<cudaEvent_t> event_pool;
+    // grad_u bookkeeping: after a fused projection grad_u is held implicitly
+    // as ubar + D u_tilde (the gradient field is not stored); G is then a
+    // cache filled on demand (downloads, LCE local step).
+    bool opt_implicit_g = false;  // MM_OPT_IMPLICIT_GRAD
+    bool g_implicit = false;
+    bool g_buf_valid = true;
+    double ubar[9] = {0};
+    double *Ut2 = nullptr;  // second u_tilde buffer (new u during a projection)
     bool F_checked = false;
     bool points_only = false;    // F verified admissible since the last upload
     int64_t bytes = 0;
@@ -182,6 +190,66 @@ __device__ void grid_finalize(const double (&vals)[K], const int (&ops)[K], doub
     }
 }
 
+// periodic neighbour offsets of point p (< 2^31) along each axis; lgn = log2 n
+// when n is a power of two (shift/mask), else -1 (32-bit division)
+template <int DIM>
+__device__ __forceinline__ void nbr_offsets(int64_t p64, int n, int lgn, int (&off_p)[DIM],
+                                            int (&off_m)[DIM]) {
+    const unsigned p = (unsigned)p64;
+    unsigned c[DIM];
+    if (lgn >= 0) {
+        const unsigned mask = (unsigned)n - 1u;
+#pragma unroll
+        for (int j = DIM - 1; j >= 0; --j) c[j] = (p >> (lgn * (DIM - 1 - j))) & mask;
+    } else {
+        unsigned q = p;
+#pragma unroll
+        for (int j = DIM - 1; j >= 0; --j) {
+            const unsigned nq = q / (unsigned)n;
+            c[j] = q - nq * (unsigned)n;
+            q = nq;
+        }
+    }
+    int stride = 1;
+#pragma unroll
+    for (int j = DIM - 1; j >= 0; --j) {
+        off_p[j] = (c[j] + 1 == (unsigned)n) ? -(n - 1) * stride : stride;
+        off_m[j] = (c[j] == 0) ? (n - 1) * stride : -stride;
+        stride *= n;
+    }
+}
+
+// Source of grad_u for the local step: the explicit field, or (implicit
+// mode, after a fused projection) u_mean + central difference of u_tilde,
+// evaluated with exactly the expression the projection's gradient pass uses.
+struct GSrc {
+    const double *G;  // explicit field (nullptr: implicit)
+    const double *U;  // u_tilde for the implicit form
+    double ubar[9];
+    int n, lgn;
+    double inv2h;
+    int64_t M;
+};
+
+template <int DIM>
+__device__ __forceinline__ void gsrc_load(const GSrc &s, int64_t p, double (&g)[DIM * DIM]) {
+    constexpr int D = DIM * DIM;
+    if (s.G) {
+#pragma unroll
+        for (int c = 0; c < D; ++c) g[c] = s.G[c * s.M + p];
+        return;
+    }
+    int op[DIM], om[DIM];
+    nbr_offsets<DIM>(p, s.n, s.lgn, op, om);
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) {
+        const double *u = s.U + (int64_t)i * s.M + p;
+#pragma unroll
+        for (int j = 0; j < DIM; ++j)
+            g[i * DIM + j] = (__ldg(u + op[j]) - __ldg(u + om[j])) * s.inv2h + s.ubar[i * DIM + j];
+    }
+}
+
 // stage timing: brackets the kernel launches of one pipeline stage with CUDA
 // events on the context stream when profiling is on, and counts launches.
 void mm_stage_begin(mm_ctx *ctx, int stage, cudaEvent_t *ev);
@@ -208,3 +276,6 @@ int mm_run_field_sums(mm_ctx *ctx, const double *field, int ncomp, double *out);
 int mm_check_det(mm_ctx *ctx, int *bad);
 int mm_run_stencil(mm_ctx *ctx, int op);
 int mm_run_frank_of_ff(mm_ctx *ctx);
+int mm_ilog2(int n);
+GSrc mm_gsrc(mm_ctx *ctx);
+int mm_materialize_G(mm_ctx *ctx);

@@ -875,6 +875,8 @@ int mm_run_lce(mm_ctx *ctx, double rho, double tol, int64_t max_sweeps, int want
     if (viscous && (!ctx->prevF || !ctx->prevAng || (d == 3 && !ctx->prevChart)))
         return mm_fail(ctx, MM_ERR_PARAM,
                        "viscous update needs the previous step (begin_time_step)");
+    // the Newton kernels read grad_u many times per sweep: use the explicit field
+    if ((rc = mm_materialize_G(ctx))) return rc;
     LcePar P = make_par(ctx->lce, rho, tol, max_sweeps);
     const double *Fk = viscous ? ctx->prevF : nullptr;
     const double *angk = viscous ? ctx->prevAng : nullptr;

@@ -43,7 +43,7 @@ inline int local_blocks(int64_t M) {
 // slots: 0 sum res^2, 1 n_conv, 2 max nsw, 3..6 sum F
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(LOCAL_THREADS)
-k_mr2d(double *__restrict__ F, const double *__restrict__ G, const double *__restrict__ Lam,
+k_mr2d(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
        const double *__restrict__ mu, const double *__restrict__ kap, int64_t M, double rho,
        double tol, int64_t max_sweeps, double phi_scale, double *__restrict__ res_out,
        int32_t *__restrict__ nsw_out, double *partials, double *red_out, unsigned int *count) {
@@ -52,7 +52,9 @@ k_mr2d(double *__restrict__ F, const double *__restrict__ G, const double *__res
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
          p += (int64_t)gridDim.x * blockDim.x) {
         double a = F[p], b = F[M + p], c = F[2 * M + p], d = F[3 * M + p];
-        const double g00 = G[p], g01 = G[M + p], g10 = G[2 * M + p], g11 = G[3 * M + p];
+        double gv[4];
+        gsrc_load<2>(gs, p, gv);
+        const double g00 = gv[0], g01 = gv[1], g10 = gv[2], g11 = gv[3];
         const double l00 = Lam[p], l01 = Lam[M + p], l10 = Lam[2 * M + p], l11 = Lam[3 * M + p];
         const double m = mu[p], k = kap[p];
         double t = 1.0 / (rho + m + 4.0 * k);
@@ -202,6 +204,22 @@ __device__ __forceinline__ double objective(const double (&X)[D], const double (
     return 0.5 * m * (I1 - 2.0 * log(J) - dd) + 0.5 * k * (J - 1.0) * (J - 1.0) + coupling;
 }
 
+// objective given det X (>0) already computed by the admissibility test
+template <int MAT, int D>
+__device__ __forceinline__ double objective_J(const double (&X)[D], double J, const double (&B)[D],
+                                              double cG, double m, double k, double rho) {
+    double bx = 0.0, I1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        bx += B[i] * X[i];
+        I1 += X[i] * X[i];
+    }
+    const double coupling = 0.5 * rho * I1 - bx + cG;
+    if constexpr (MAT == MAT_QUAD) return 0.5 * m * I1 + coupling;
+    const double dd = (D == 4) ? 2.0 : 3.0;
+    return 0.5 * m * (I1 - 2.0 * log(J) - dd) + 0.5 * k * (J - 1.0) * (J - 1.0) + coupling;
+}
+
 // gradient S(X) - lam - rho (G - X) = S(X) + rho X - B
 // (mooney_rivlin.py:143-151 / quadratic.py:57-58)
 template <int MAT, int D>
@@ -231,7 +249,7 @@ __device__ __forceinline__ bool admissible(const double (&X)[D]) {
 //        3 guard sum (sum res where res > tol), 4..4+D sum F
 template <int MAT, int D>
 __global__ void __launch_bounds__(LOCAL_THREADS, LOCAL_MIN_BLOCKS)
-k_descent(double *__restrict__ F, const double *__restrict__ G, const double *__restrict__ Lam,
+k_descent(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
           const double *__restrict__ modA, const double *__restrict__ modB, int64_t M,
           double rho, double tol, double phi_scale, int s0, int s1, double *__restrict__ tstate,
           uint8_t *__restrict__ freestate, double *__restrict__ res_out,
@@ -245,10 +263,11 @@ k_descent(double *__restrict__ F, const double *__restrict__ G, const double *__
          p += (int64_t)gridDim.x * blockDim.x) {
         double X[D], B[D], g[D], Xt[D];
         double cG = 0.0;
+        gsrc_load<(D == 4 ? 2 : 3)>(gs, p, B);  // B holds grad_u until the next line
 #pragma unroll
         for (int i = 0; i < D; ++i) {
             X[i] = F[i * M + p];
-            const double gi = G[i * M + p];
+            const double gi = B[i];
             B[i] = Lam[i * M + p] + rho * gi;
             cG += gi * gi;
         }
@@ -272,6 +291,8 @@ k_descent(double *__restrict__ F, const double *__restrict__ G, const double *__
         for (int i = 0; i < D; ++i) gs += g[i] * g[i];
         double res = sqrt(gs);
         bool moved = false;
+        bool have_phi = false;
+        double phi_cur = 0.0;
         // a point is active at global sweep s iff it was active at every
         // earlier sweep (nsw == s) and res > tol; once inactive it stays so
         for (int s = s0; s < s1; ++s) {
@@ -281,7 +302,11 @@ k_descent(double *__restrict__ F, const double *__restrict__ G, const double *__
             bool in_free = freem, in_arm = false;
             double phi0 = 0.0, gsq = 0.0;
             if (!freem) {
-                phi0 = objective<MAT, D>(X, B, cG, m, k, rho);
+                // phi at the current X is known when the previous sweep ended on
+                // an accepted Armijo step or took no step (same X, same bits)
+                phi0 = have_phi ? phi_cur : objective<MAT, D>(X, B, cG, m, k, rho);
+                phi_cur = phi0;
+                have_phi = true;
 #pragma unroll
                 for (int i = 0; i < D; ++i) gsq += g[i] * g[i];
                 // base.py:168-171: unmeasurable decrease -> free mode, and the
@@ -302,10 +327,16 @@ k_descent(double *__restrict__ F, const double *__restrict__ G, const double *__
 #pragma unroll
                     for (int i = 0; i < D; ++i) Xt[i] = X[i] - t * g[i];
                     double phi_try = INFINITY;
-                    if (admissible<MAT, D>(Xt)) phi_try = objective<MAT, D>(Xt, B, cG, m, k, rho);
+                    if constexpr (MAT == MAT_QUAD) {
+                        phi_try = objective<MAT, D>(Xt, B, cG, m, k, rho);
+                    } else {
+                        const double Jt = det_t<D>(Xt);  // admissibility and objective share J
+                        if (Jt > 0.0) phi_try = objective_J<MAT, D>(Xt, Jt, B, cG, m, k, rho);
+                    }
                     if (phi_try <= phi0 - BT_DECREASE * t * gsq) {
 #pragma unroll
                         for (int i = 0; i < D; ++i) X[i] = Xt[i];
+                        phi_cur = phi_try;
                         accepted = true;
                         break;
                     }
@@ -331,6 +362,7 @@ k_descent(double *__restrict__ F, const double *__restrict__ G, const double *__
                 if (took) {
 #pragma unroll
                     for (int i = 0; i < D; ++i) X[i] = Xt[i];
+                    have_phi = false;
                 }
             }
             gradient<MAT, D>(X, B, m, k, rho, g);
@@ -476,7 +508,7 @@ static int launch_descent(mm_ctx *ctx, double rho, double tol, double phi_scale,
     if (rc) return rc;
     StageScope ss(ctx, MM_STAGE_LOCAL);
     k_descent<MAT, D><<<blocks, LOCAL_THREADS, 0, ctx->stream>>>(
-        ctx->F, ctx->G, ctx->Lam, ctx->modA, MAT == MAT_MR ? ctx->modB : ctx->modA, ctx->M, rho,
+        ctx->F, mm_gsrc(ctx), ctx->Lam, ctx->modA, MAT == MAT_MR ? ctx->modB : ctx->modA, ctx->M, rho,
         tol, phi_scale, s0, s1, persist ? ctx->tstate : nullptr,
         persist ? ctx->freestate : nullptr, want_points ? ctx->res : nullptr,
         (persist || want_points) ? ctx->nsw : nullptr, ctx->partials, ctx->red_out,
@@ -514,7 +546,7 @@ int mm_run_local(mm_ctx *ctx, int material, double rho, double tol, int64_t max_
         {
             StageScope ss(ctx, MM_STAGE_LOCAL);
             k_mr2d<<<blocks, LOCAL_THREADS, 0, ctx->stream>>>(
-                ctx->F, ctx->G, ctx->Lam, ctx->modA, ctx->modB, ctx->M, rho, tol, max_sweeps,
+                ctx->F, mm_gsrc(ctx), ctx->Lam, ctx->modA, ctx->modB, ctx->M, rho, tol, max_sweeps,
                 phi_scale, want_points ? ctx->res : nullptr, want_points ? ctx->nsw : nullptr,
                 ctx->partials, ctx->red_out, ctx->red_count);
         }

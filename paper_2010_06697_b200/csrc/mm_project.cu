@@ -248,7 +248,16 @@ __device__ __forceinline__ double div_at(const double *__restrict__ F, const dou
 }
 
 template <int N1, int N2, int TK>
-__global__ void k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho,
+struct RowCfg {
+    static constexpr int NT0 = N1 ? TK * (N1 > N2 ? N1 : N2) : 256;
+    static constexpr int NT = NT0 < 64 ? 64 : NT0;
+    static constexpr int MINB0 = 65536 / (NT * 96);
+    static constexpr int MINB = MINB0 < 1 ? 1 : MINB0;  // aim at <= 96 registers
+};
+
+template <int N1, int N2, int TK>
+__global__ void __launch_bounds__(RowCfg<N1, N2, TK>::NT, RowCfg<N1, N2, TK>::MINB)
+k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho,
                           double2 *__restrict__ spec, RowGeom g,
                           const double2 *__restrict__ tw_line,
                           const double2 *__restrict__ tw_r2c) {
@@ -347,7 +356,8 @@ __global__ void k_row_fwd(const double *__restrict__ F, const double *__restrict
 // E: inverse C2R along rows -> u_tilde (unnormalised; 1/n^d folded into C)
 // ---------------------------------------------------------------------------
 template <int N1, int N2, int TK>
-__global__ void k_row_inv(const double2 *__restrict__ spec, double *__restrict__ Ut, RowGeom g,
+__global__ void __launch_bounds__(RowCfg<N1, N2, TK>::NT, RowCfg<N1, N2, TK>::MINB)
+k_row_inv(const double2 *__restrict__ spec, double *__restrict__ Ut, RowGeom g,
                           const double2 *__restrict__ tw_line,
                           const double2 *__restrict__ tw_r2c) {
     extern __shared__ double2 smem_c[];
@@ -427,22 +437,52 @@ struct ColGeom {
 
 enum { COL_FWD = 0, COL_INV = 1, COL_SOLVE = 2 };
 
+template <int N1, int N2>
+struct ColCfg {
+    static constexpr int TK = 8;
+    static constexpr int NT = N1 ? (TK * (N1 > N2 ? N1 : N2) < 64 ? 64 : TK * (N1 > N2 ? N1 : N2))
+                                 : 256;
+    // resident blocks per SM requested from the register allocator
+    static constexpr int MINB = N1 ? (NT <= 128 ? 5 : 2) : 1;
+};
+
 template <int N1, int N2, int MODE>
-__global__ void k_col(double2 *__restrict__ spec, ColGeom g, const double2 *__restrict__ tw) {
-    constexpr int TK = 8, LD = TK + 1;
+__global__ void __launch_bounds__(ColCfg<N1, N2>::NT, ColCfg<N1, N2>::MINB)
+k_col(double2 *__restrict__ spec, ColGeom g, const double2 *__restrict__ tw) {
+    constexpr int TK = ColCfg<N1, N2>::TK, LD = TK + 1, NT = ColCfg<N1, N2>::NT;
     extern __shared__ double2 smem_c[];
     double2 *buf = smem_c;
-    double2 *scr = smem_c + (size_t)(g.N + 1) * LD;
+    double2 *scr = smem_c + (size_t)g.N * LD;
     const int k0 = blockIdx.x * TK;
     const int outer = blockIdx.y;
     const int comp = blockIdx.z;
     double2 *base = spec + comp * g.cs + outer * g.os + k0;
     const int N = g.N;
-    for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
-        const int n = w / TK, c = w - n * TK;
-        double2 v = make_double2(0.0, 0.0);
-        if (k0 + c < g.ncol) v = base[n * g.es + c];
-        buf[n * LD + c] = v;
+    const bool full = k0 + TK <= g.ncol;
+    if constexpr (N1 != 0) {
+        // compile-time trip count: all loads of the tile are in flight at once
+        constexpr int NN = N1 * N2;
+        constexpr int IT = (NN * TK + NT - 1) / NT;
+        double2 v[IT];
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int w = it * NT + threadIdx.x;
+            const int n = w / TK, c = w % TK;
+            v[it] = (w < NN * TK && (full || k0 + c < g.ncol)) ? base[n * g.es + c]
+                                                               : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int w = it * NT + threadIdx.x;
+            if (w < NN * TK) buf[(w / TK) * LD + (w % TK)] = v[it];
+        }
+    } else {
+        for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
+            const int n = w / TK, c = w - n * TK;
+            double2 v = make_double2(0.0, 0.0);
+            if (k0 + c < g.ncol) v = base[n * g.es + c];
+            buf[n * LD + c] = v;
+        }
     }
     __syncthreads();
     if constexpr (MODE == COL_FWD || MODE == COL_SOLVE)
@@ -454,10 +494,11 @@ __global__ void k_col(double2 *__restrict__ spec, ColGeom g, const double2 *__re
         // column is the last-axis frequency, `outer` the axis-1 one in 3D
         const double *s0 = g.sym;
         const double *slast = g.sym + (int64_t)(g.dim - 1) * g.n;
+        const double s1 = (g.dim == 3) ? g.sym[g.n + outer] : 0.0;
         for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
             const int kl = w / TK, c = w - kl * TK;
             double gsq = s0[kl];
-            if (g.dim == 3) gsq = gsq + g.sym[g.n + outer];
+            if (g.dim == 3) gsq = gsq + s1;
             gsq = gsq + slast[min(k0 + c, g.n - 1)];
             const double inv = (gsq > g.thresh) ? 1.0 / gsq : 0.0;
             buf[kl * LD + c] = cscale(buf[kl * LD + c], -inv * g.scale);
@@ -465,9 +506,20 @@ __global__ void k_col(double2 *__restrict__ spec, ColGeom g, const double2 *__re
         __syncthreads();
         line_transform<N1, N2, TK, true>(buf, scr, N, tw);
     }
-    for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
-        const int n = w / TK, c = w - n * TK;
-        if (k0 + c < g.ncol) base[n * g.es + c] = buf[n * LD + c];
+    if constexpr (N1 != 0) {
+        constexpr int NN = N1 * N2;
+        constexpr int IT = (NN * TK + NT - 1) / NT;
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int w = it * NT + threadIdx.x;
+            const int n = w / TK, c = w % TK;
+            if (w < NN * TK && (full || k0 + c < g.ncol)) base[n * g.es + c] = buf[n * LD + c];
+        }
+    } else {
+        for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
+            const int n = w / TK, c = w - n * TK;
+            if (k0 + c < g.ncol) base[n * g.es + c] = buf[n * LD + c];
+        }
     }
 }
 
@@ -479,40 +531,19 @@ struct Mean9 {
     double v[9];
 };
 
-// periodic neighbour offsets of point p (< 2^31) along each axis; lgn = log2 n
-// when n is a power of two (shift/mask), else -1 (32-bit division)
-template <int DIM>
-__device__ __forceinline__ void nbr_offsets(int64_t p64, int n, int lgn, int (&off_p)[DIM],
-                                            int (&off_m)[DIM]) {
-    const unsigned p = (unsigned)p64;
-    unsigned c[DIM];
-    if (lgn >= 0) {
-        const unsigned mask = (unsigned)n - 1u;
-#pragma unroll
-        for (int j = DIM - 1; j >= 0; --j) c[j] = (p >> (lgn * (DIM - 1 - j))) & mask;
-    } else {
-        unsigned q = p;
-#pragma unroll
-        for (int j = DIM - 1; j >= 0; --j) {
-            const unsigned nq = q / (unsigned)n;
-            c[j] = q - nq * (unsigned)n;
-            q = nq;
-        }
-    }
-    int stride = 1;
-#pragma unroll
-    for (int j = DIM - 1; j >= 0; --j) {
-        off_p[j] = (c[j] + 1 == (unsigned)n) ? -(n - 1) * stride : stride;
-        off_m[j] = (c[j] == 0) ? (n - 1) * stride : -stride;
-        stride *= n;
-    }
-}
+// MODE: GRAD_WRITE  grad_u = u_mean + D u (projection API; writes G)
+//       GRAD_EXPL   solver tail with an explicit previous grad_u (reads G)
+//       GRAD_IMPL   solver tail with grad_u_old = ubar_old + D u_old implicit
+// The solver modes do not write G: afterwards grad_u is implicit.
+//       GRAD_EXPLW  solver tail, explicit grad_u in and out (reads and writes G)
+enum { GRAD_WRITE = 0, GRAD_EXPL = 1, GRAD_IMPL = 2, GRAD_EXPLW = 3 };
 
-template <int DIM, bool UPDATE>
+template <int DIM, int MODE>
 __global__ void __launch_bounds__(256)
-k_grad(const double *__restrict__ Ut, double *__restrict__ G, const double *__restrict__ F,
-       double *__restrict__ Lam, int n, int lgn, int64_t M, double inv2h, double rho, Mean9 um,
-       double *partials, double *red_out, unsigned int *count) {
+k_grad(const double *__restrict__ Ut, const double *__restrict__ Uold, double *__restrict__ G,
+       const double *__restrict__ F, double *__restrict__ Lam, int n, int lgn, int64_t M,
+       double inv2h, double rho, Mean9 um, Mean9 um_old, double *partials, double *red_out,
+       unsigned int *count) {
     constexpr int D = DIM * DIM;
     constexpr int K = 2 + D;
     __shared__ double smem[32 * K];
@@ -521,40 +552,49 @@ k_grad(const double *__restrict__ Ut, double *__restrict__ G, const double *__re
     for (int k = 0; k < K; ++k) acc[k] = 0.0;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
          p += (int64_t)gridDim.x * blockDim.x) {
-        // neighbour offsets along each axis (periodic)
         int off_p[DIM], off_m[DIM];
         nbr_offsets<DIM>(p, n, lgn, off_p, off_m);
-        // issue every load before any store (G and Lam are read and written)
-        double up[D], um_[D];
+        // issue every load before any store
+        double up[D], dn[D];
 #pragma unroll
         for (int i = 0; i < DIM; ++i) {
             const double *u = Ut + (int64_t)i * M + p;
 #pragma unroll
             for (int j = 0; j < DIM; ++j) {
                 up[i * DIM + j] = __ldg(u + off_p[j]);
-                um_[i * DIM + j] = __ldg(u + off_m[j]);
+                dn[i * DIM + j] = __ldg(u + off_m[j]);
             }
         }
         double gold[D], fv[D], lv[D];
-        if (UPDATE) {
+        if (MODE == GRAD_IMPL) {
+#pragma unroll
+            for (int i = 0; i < DIM; ++i) {
+                const double *u = Uold + (int64_t)i * M + p;
+#pragma unroll
+                for (int j = 0; j < DIM; ++j)
+                    gold[i * DIM + j] = (__ldg(u + off_p[j]) - __ldg(u + off_m[j])) * inv2h +
+                                        um_old.v[i * DIM + j];
+            }
+        }
+        if (MODE != GRAD_WRITE) {
 #pragma unroll
             for (int c = 0; c < D; ++c) {
                 const int64_t o = (int64_t)c * M + p;
-                gold[c] = G[o];
+                if (MODE == GRAD_EXPL || MODE == GRAD_EXPLW) gold[c] = G[o];
                 fv[c] = __ldg(&F[o]);
                 lv[c] = Lam[o];
             }
         }
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-            const double gnew = (up[c] - um_[c]) * inv2h + um.v[c];  // projection.py:168
+            const double gnew = (up[c] - dn[c]) * inv2h + um.v[c];  // projection.py:168
             const int64_t o = (int64_t)c * M + p;
-            if (UPDATE) {
-                const double dg = gnew - gold[c];
-                const double mis = gnew - fv[c];          // solver.py:277
-                const double lnew = lv[c] + rho * mis;    // solver.py:279
-                G[o] = gnew;
+            if (MODE != GRAD_WRITE) {
+                const double dg = gnew - gold[c];          // solver.py:271
+                const double mis = gnew - fv[c];           // solver.py:277
+                const double lnew = lv[c] + rho * mis;     // solver.py:279
                 Lam[o] = lnew;
+                if (MODE == GRAD_EXPLW) G[o] = gnew;
                 acc[0] += dg * dg;
                 acc[1] += mis * mis;
                 acc[2 + c] += lnew;
@@ -563,7 +603,7 @@ k_grad(const double *__restrict__ Ut, double *__restrict__ G, const double *__re
             }
         }
     }
-    if (UPDATE) {
+    if (MODE != GRAD_WRITE) {
         int ops[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) ops[k] = RED_SUM;
@@ -599,7 +639,7 @@ k_div(const double *__restrict__ F, double *__restrict__ Ut, int n, int lgn, int
 // ---------------------------------------------------------------------------
 bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
 
-int ilog2(int n) {
+int ilog2_(int n) {
     if (!is_pow2(n)) return -1;
     int l = 0;
     while ((1 << l) < n) ++l;
@@ -638,9 +678,10 @@ int launch_smem(mm_ctx *ctx, Kern kern, dim3 grid, int threads, size_t smem) {
 }
 
 template <int N1, int N2, int TK>
-int run_rows_t(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double2 *tw_line) {
+int run_rows_t(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double2 *tw_line,
+               double *u_out) {
     const int rows = TK / g.dim;
-    const int threads = N1 ? std::max(64, TK * std::max(N1, N2)) : 256;
+    const int threads = RowCfg<N1, N2, TK>::NT;
     const size_t smem = sizeof(double2) * (size_t)(g.N + 1) * (TK + 1) * (N1 ? 1 : 2);
     dim3 grid((unsigned)((g.nrows + rows - 1) / rows));
     if (fwd) {
@@ -653,24 +694,26 @@ int run_rows_t(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double
         auto kern = k_row_inv<N1, N2, TK>;
         int rc = launch_smem(ctx, kern, grid, threads, smem);
         if (rc) return rc;
-        kern<<<grid, threads, smem, ctx->stream>>>(ctx->spec, ctx->Ut, g, tw_line, ctx->tw_r2c);
+        kern<<<grid, threads, smem, ctx->stream>>>(ctx->spec, u_out, g, tw_line, ctx->tw_r2c);
     }
     MM_LAUNCH_CHECK(ctx);
     return MM_OK;
 }
 
 template <int N1, int N2>
-int run_rows_n(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double2 *tw) {
+int run_rows_n(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double2 *tw,
+               double *u_out) {
     // lines per tile: TK = dim * rows, bounded so TK*max(N1,N2) <= 512 threads
+    // lines per tile TK = dim * rows: 4 rows (2 for 32-point register FFTs)
     const bool big = N1 >= 32;
     if (g.dim == 2)
-        return big ? run_rows_t<N1, N2, 8>(ctx, fwd, rho, g, tw)
-                   : run_rows_t<N1, N2, 16>(ctx, fwd, rho, g, tw);
-    return big ? run_rows_t<N1, N2, 12>(ctx, fwd, rho, g, tw)
-               : run_rows_t<N1, N2, 24>(ctx, fwd, rho, g, tw);
+        return big ? run_rows_t<N1, N2, 4>(ctx, fwd, rho, g, tw, u_out)
+                   : run_rows_t<N1, N2, 8>(ctx, fwd, rho, g, tw, u_out);
+    return big ? run_rows_t<N1, N2, 6>(ctx, fwd, rho, g, tw, u_out)
+               : run_rows_t<N1, N2, 12>(ctx, fwd, rho, g, tw, u_out);
 }
 
-int run_rows(mm_ctx *ctx, bool fwd, double rho) {
+int run_rows(mm_ctx *ctx, bool fwd, double rho, double *u_out = nullptr) {
     RowGeom g;
     g.n = ctx->n;
     g.dim = ctx->dim;
@@ -684,19 +727,19 @@ int run_rows(mm_ctx *ctx, bool fwd, double rho) {
     factor(g.N, N1, N2);
     switch (N1 * 100 + N2) {
 #define CASE(a, b) \
-    case a * 100 + b: return run_rows_n<a, b>(ctx, fwd, rho, g, tw);
+    case a * 100 + b: return run_rows_n<a, b>(ctx, fwd, rho, g, tw, u_out);
         CASE(1, 1) CASE(2, 1) CASE(4, 1) CASE(8, 1) CASE(4, 4) CASE(8, 4) CASE(8, 8)
         CASE(16, 8) CASE(16, 16) CASE(32, 16) CASE(32, 32)
 #undef CASE
-        default: return run_rows_n<0, 0>(ctx, fwd, rho, g, tw);
+        default: return run_rows_n<0, 0>(ctx, fwd, rho, g, tw, u_out);
     }
 }
 
 template <int N1, int N2, int MODE>
 int run_col_t(mm_ctx *ctx, const ColGeom &g, int n_outer) {
-    constexpr int TK = 8;
-    const int threads = N1 ? std::max(64, TK * std::max(N1, N2)) : 256;
-    const size_t smem = sizeof(double2) * (size_t)(g.N + 1) * (TK + 1) * (N1 ? 1 : 2);
+    constexpr int TK = ColCfg<N1, N2>::TK;
+    const int threads = ColCfg<N1, N2>::NT;
+    const size_t smem = sizeof(double2) * (size_t)g.N * (TK + 1) * (N1 ? 1 : 2);
     dim3 grid((unsigned)((g.ncol + TK - 1) / TK), (unsigned)n_outer, (unsigned)ctx->dim);
     auto kern = k_col<N1, N2, MODE>;
     int rc = launch_smem(ctx, kern, grid, threads, smem);
@@ -787,43 +830,114 @@ int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
         StageScope ss(ctx, MM_STAGE_COL_SOLVE);
         if ((rc = run_col<COL_SOLVE>(ctx, gz, 1))) return rc;
     }
-    // E: C2R rows -> u_tilde
+    // E: C2R rows -> u (new buffer on the solver path)
+    double *u_new = ctx->Ut;
+    if (update && ctx->opt_implicit_g) {
+        if (!ctx->Ut2 && (rc = mm_alloc(ctx, (void **)&ctx->Ut2, sizeof(double) * d * ctx->M)))
+            return rc;
+        u_new = ctx->Ut2;
+    }
     {
         StageScope ss(ctx, MM_STAGE_ROW_INV);
-        if ((rc = run_rows(ctx, false, rho))) return rc;
+        if ((rc = run_rows(ctx, false, rho, u_new))) return rc;
     }
     // F: gradient (+ ascent and residual sums)
-    Mean9 um;
-    for (int i = 0; i < 9; ++i) um.v[i] = i < ctx->D ? u_mean[i] : 0.0;
+    Mean9 um, umo;
+    for (int i = 0; i < 9; ++i) {
+        um.v[i] = i < ctx->D ? u_mean[i] : 0.0;
+        umo.v[i] = ctx->ubar[i];
+    }
     const int threads = 256;
     const int blocks = (int)std::min<int64_t>((ctx->M + threads - 1) / threads, 148 * 8);
     if ((rc = mm_ensure_partials(ctx, blocks))) return rc;
     const double inv2h = 1.0 / (2.0 * ctx->h);
-    const int lgn = ilog2(n);
-#define LAUNCH(DIM, UPD)                                                                      \
-    k_grad<DIM, UPD><<<blocks, threads, 0, ctx->stream>>>(ctx->Ut, ctx->G, ctx->F, ctx->Lam, n, lgn, \
-                                                          ctx->M, inv2h, rho, um,               \
-                                                          ctx->partials, ctx->red_out,          \
-                                                          ctx->red_count)
+    const int lgn = ilog2_(n);
+    const int mode = !update ? GRAD_WRITE
+                     : !ctx->opt_implicit_g ? GRAD_EXPLW
+                     : (ctx->g_implicit ? GRAD_IMPL : GRAD_EXPL);
+#define LAUNCH(DIM, MODE)                                                                       \
+    k_grad<DIM, MODE><<<blocks, threads, 0, ctx->stream>>>(u_new, ctx->Ut, ctx->G, ctx->F,       \
+                                                           ctx->Lam, n, lgn, ctx->M, inv2h, rho, \
+                                                           um, umo, ctx->partials, ctx->red_out, \
+                                                           ctx->red_count)
     {
         StageScope ss(ctx, MM_STAGE_GRAD);
         if (d == 2) {
-            if (update) LAUNCH(2, true);
-            else LAUNCH(2, false);
+            if (mode == GRAD_WRITE) LAUNCH(2, GRAD_WRITE);
+            else if (mode == GRAD_EXPL) LAUNCH(2, GRAD_EXPL);
+            else if (mode == GRAD_EXPLW) LAUNCH(2, GRAD_EXPLW);
+            else LAUNCH(2, GRAD_IMPL);
         } else {
-            if (update) LAUNCH(3, true);
-            else LAUNCH(3, false);
+            if (mode == GRAD_WRITE) LAUNCH(3, GRAD_WRITE);
+            else if (mode == GRAD_EXPL) LAUNCH(3, GRAD_EXPL);
+            else if (mode == GRAD_EXPLW) LAUNCH(3, GRAD_EXPLW);
+            else LAUNCH(3, GRAD_IMPL);
         }
     }
 #undef LAUNCH
     MM_LAUNCH_CHECK(ctx);
-    if (!update) return MM_OK;
+    for (int i = 0; i < 9; ++i) ctx->ubar[i] = um.v[i];
+    if (!update) {
+        // grad_u written explicitly
+        ctx->g_implicit = false;
+        ctx->g_buf_valid = true;
+        return MM_OK;
+    }
+    if (ctx->opt_implicit_g) {
+        // new u becomes current; grad_u is now ubar + D u (implicit)
+        std::swap(ctx->Ut, ctx->Ut2);
+        ctx->g_implicit = true;
+        ctx->g_buf_valid = false;
+    } else {
+        ctx->g_implicit = false;
+        ctx->g_buf_valid = true;
+    }
     double r[MM_MAX_PARTIALS];
     const int K = 2 + ctx->D;
     if ((rc = mm_fetch_reduction(ctx, K, r))) return rc;
     out->sum_dG2 = r[0];
     out->sum_mis2 = r[1];
     for (int i = 0; i < 9; ++i) out->sum_lam[i] = i < ctx->D ? r[2 + i] : 0.0;
+    return MM_OK;
+}
+
+int mm_ilog2(int n) { return ilog2_(n); }
+
+GSrc mm_gsrc(mm_ctx *ctx) {
+    GSrc s;
+    const bool impl = ctx->g_implicit && !ctx->g_buf_valid;
+    s.G = impl ? nullptr : ctx->G;
+    s.U = ctx->Ut;
+    for (int i = 0; i < 9; ++i) s.ubar[i] = ctx->ubar[i];
+    s.n = ctx->n;
+    s.lgn = ctx->points_only ? -1 : ilog2_(ctx->n);
+    s.inv2h = ctx->points_only ? 0.0 : 1.0 / (2.0 * ctx->h);
+    s.M = ctx->M;
+    return s;
+}
+
+// fill the G buffer from the implicit form (ubar + D u_tilde)
+int mm_materialize_G(mm_ctx *ctx) {
+    if (!ctx->g_implicit || ctx->g_buf_valid) return MM_OK;
+    Mean9 um, umo;
+    for (int i = 0; i < 9; ++i) um.v[i] = umo.v[i] = ctx->ubar[i];
+    const int threads = 256;
+    const int blocks = (int)std::min<int64_t>((ctx->M + threads - 1) / threads, 148 * 8);
+    const double inv2h = 1.0 / (2.0 * ctx->h);
+    const int lgn = ilog2_(ctx->n);
+    {
+        StageScope ss(ctx, MM_STAGE_OTHER);
+        if (ctx->dim == 2)
+            k_grad<2, GRAD_WRITE><<<blocks, threads, 0, ctx->stream>>>(
+                ctx->Ut, ctx->Ut, ctx->G, ctx->F, ctx->Lam, ctx->n, lgn, ctx->M, inv2h, 0.0, um,
+                umo, nullptr, nullptr, nullptr);
+        else
+            k_grad<3, GRAD_WRITE><<<blocks, threads, 0, ctx->stream>>>(
+                ctx->Ut, ctx->Ut, ctx->G, ctx->F, ctx->Lam, ctx->n, lgn, ctx->M, inv2h, 0.0, um,
+                umo, nullptr, nullptr, nullptr);
+    }
+    MM_LAUNCH_CHECK(ctx);
+    ctx->g_buf_valid = true;
     return MM_OK;
 }
 
@@ -836,19 +950,21 @@ int mm_run_stencil(mm_ctx *ctx, int op) {
         Mean9 um;
         for (int i = 0; i < 9; ++i) um.v[i] = 0.0;
         if (ctx->dim == 2)
-            k_grad<2, false><<<blocks, threads, 0, ctx->stream>>>(
-                ctx->Ut, ctx->G, ctx->F, ctx->Lam, ctx->n, ilog2(ctx->n), ctx->M, inv2h, 0.0, um, nullptr,
-                nullptr, nullptr);
+            k_grad<2, GRAD_WRITE><<<blocks, threads, 0, ctx->stream>>>(
+                ctx->Ut, ctx->Ut, ctx->G, ctx->F, ctx->Lam, ctx->n, ilog2_(ctx->n), ctx->M, inv2h,
+                0.0, um, um, nullptr, nullptr, nullptr);
         else
-            k_grad<3, false><<<blocks, threads, 0, ctx->stream>>>(
-                ctx->Ut, ctx->G, ctx->F, ctx->Lam, ctx->n, ilog2(ctx->n), ctx->M, inv2h, 0.0, um, nullptr,
-                nullptr, nullptr);
+            k_grad<3, GRAD_WRITE><<<blocks, threads, 0, ctx->stream>>>(
+                ctx->Ut, ctx->Ut, ctx->G, ctx->F, ctx->Lam, ctx->n, ilog2_(ctx->n), ctx->M, inv2h,
+                0.0, um, um, nullptr, nullptr, nullptr);
+        ctx->g_implicit = false;
+        ctx->g_buf_valid = true;
     } else {
         if (ctx->dim == 2)
-            k_div<2><<<blocks, threads, 0, ctx->stream>>>(ctx->F, ctx->Ut, ctx->n, ilog2(ctx->n),
+            k_div<2><<<blocks, threads, 0, ctx->stream>>>(ctx->F, ctx->Ut, ctx->n, ilog2_(ctx->n),
                                                           ctx->M, inv2h);
         else
-            k_div<3><<<blocks, threads, 0, ctx->stream>>>(ctx->F, ctx->Ut, ctx->n, ilog2(ctx->n),
+            k_div<3><<<blocks, threads, 0, ctx->stream>>>(ctx->F, ctx->Ut, ctx->n, ilog2_(ctx->n),
                                                           ctx->M, inv2h);
     }
     MM_LAUNCH_CHECK(ctx);

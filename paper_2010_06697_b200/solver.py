@@ -90,10 +90,11 @@ class ADMMState:
 
     Field attributes (F, grad_u, lam, u_tilde, prev_F, internal, prev_internal)
     are device-resident while the state is attached to an engine.  Reading one
-    downloads a numpy view; reading or assigning marks it to be uploaded again
-    before the next device operation, so in-place edits of a freshly read
-    array are honoured.  A view read before a solve is not updated by it —
-    read the attribute again afterwards.
+    returns a read-only numpy snapshot (downloaded on first access after the
+    device changed it); assigning a new array (``state.F = state.F + dF``)
+    uploads it before the next device operation.  In-place edits of a snapshot
+    raise instead of being silently lost.  A snapshot read before a solve is
+    not updated by it — read the attribute again afterwards.
     """
 
     _FIELD_NAMES = tuple(STATE_FIELDS)
@@ -127,14 +128,15 @@ class ADMMState:
             grid = eng.grid
             if name in STATE_FIELDS:
                 fid, rank = STATE_FIELDS[name]
-                self._host[name] = eng.ctx.download(fid, field_shape(grid, rank))
+                val = eng.ctx.download(fid, field_shape(grid, rank))
+                val.flags.writeable = False
             else:
-                self._host[name] = eng.model._download_internal(eng.ctx, name)
+                val = eng.model._download_internal(eng.ctx, name)
+                for a in val.values():
+                    a.flags.writeable = False
+            self._host[name] = val
             self._stale.discard(name)
-        val = self._host.get(name)
-        if val is not None:
-            self._dirty.add(name)
-        return val
+        return self._host.get(name)
 
     def _set(self, name, value):
         if value is not None and name in STATE_FIELDS:
@@ -194,16 +196,17 @@ class ADMMState:
             if nm in self._dirty or nm not in self._dev:
                 grid.check_field(val, rank, nm)
                 ctx.upload(fid, val)
-                self._dev.add(nm)
                 if nm == "lam":
                     eng.lam_sum = None
+            # the caller keeps its array; ours is re-read from the device
+            self._mark_device(nm)
         for nm in ("internal", "prev_internal"):
             if nm in self._stale:
                 continue
             val = self._host.get(nm)
             if val and (nm in self._dirty or nm not in self._dev):
                 model._upload_internal(ctx, nm, val)
-                self._dev.add(nm)
+                self._mark_device(nm)
         self._dirty.clear()
         return eng
 
