@@ -102,7 +102,8 @@ enum mm_stage {
     MM_STAGE_GRAD = 6,      /* gradient + multiplier ascent + residual sums */
     MM_STAGE_FROZEN = 7,    /* LCE director + Frank stencil */
     MM_STAGE_OTHER = 8,     /* transfers, sums, checks */
-    MM_NSTAGE = 9
+    MM_STAGE_FUSED = 9,     /* multiplier ascent fused with the next first local chunk */
+    MM_NSTAGE = 10
 };
 
 typedef struct {
@@ -185,6 +186,21 @@ int mm_project_update(mm_ctx *ctx, double rho, const double *u_mean, mm_update_s
  * kernel-launch counts (launch counts are kept even when off). */
 int mm_profile_enable(mm_ctx *ctx, int on);
 int mm_profile_read(mm_ctx *ctx, mm_profile *out, int reset);
+
+/* Split form of the solver tail used by solve() to fuse the multiplier
+ * ascent of iteration k with the first local chunk of iteration k+1:
+ *  mm_project_residuals: projection + sums for r_d and r_p only
+ *    (solver.py:268-278); the ascent lam += rho (grad_u - F) is left pending
+ *    and grad_u becomes implicit (u_mean + D u_tilde);
+ *  mm_update_multiplier: apply the pending ascent (sum_lam filled);
+ *  mm_update_and_sweep: apply it and, in the same pass, run the first local
+ *    chunk of the next iteration with rho_next / tol (at most 64 sweeps;
+ *    MR and quadratic).  Any other call first applies a pending ascent. */
+int mm_project_residuals(mm_ctx *ctx, double rho, const double *u_mean, mm_update_stats *out);
+int mm_update_multiplier(mm_ctx *ctx, mm_update_stats *out);
+int mm_update_and_sweep(mm_ctx *ctx, int material, double rho_next, double tol,
+                        int64_t max_sweeps, double phi_scale, int want_points,
+                        mm_local_stats *ls, mm_update_stats *us);
 
 /* Options.  MM_OPT_IMPLICIT_GRAD (default 0): after a fused projection keep
  * grad_u implicitly as u_mean + D u_tilde instead of storing the 9-component

@@ -38,10 +38,11 @@ EXPORTS = (
     "mm_field_sums", "mm_set_symbols", "mm_local_sweeps", "mm_set_lce", "mm_download_points",
     "mm_prepare_frozen", "mm_project", "mm_project_update", "mm_stencil",
     "mm_profile_enable", "mm_profile_read", "mm_frank_stencil", "mm_set_option",
+    "mm_project_residuals", "mm_update_multiplier", "mm_update_and_sweep",
 )
 
 STAGES = ("local", "row_fwd", "col_fwd", "col_solve", "col_inv", "row_inv", "grad", "frozen",
-          "other")
+          "other", "fused")
 
 
 class LocalStatsC(ctypes.Structure):
@@ -55,7 +56,7 @@ class UpdateStatsC(ctypes.Structure):
 
 
 class ProfileC(ctypes.Structure):
-    _fields_ = [("ms", ctypes.c_double * 9), ("launches", ctypes.c_int64 * 9)]
+    _fields_ = [("ms", ctypes.c_double * 10), ("launches", ctypes.c_int64 * 10)]
 
 
 class LCEParamsC(ctypes.Structure):
@@ -106,6 +107,10 @@ def load_library():
             "mm_profile_enable": ([P, I], I),
             "mm_frank_stencil": ([P], I),
             "mm_set_option": ([P, I, I64], I),
+            "mm_project_residuals": ([P, D, P, ctypes.POINTER(UpdateStatsC)], I),
+            "mm_update_multiplier": ([P, ctypes.POINTER(UpdateStatsC)], I),
+            "mm_update_and_sweep": ([P, I, D, D, I64, D, I, ctypes.POINTER(LocalStatsC),
+                                     ctypes.POINTER(UpdateStatsC)], I),
             "mm_profile_read": ([P, ctypes.POINTER(ProfileC), I], I),
         }
         for name, (args, res) in sig.items():
@@ -262,3 +267,23 @@ class Context:
 
     def set_option(self, option, value):
         self.check(self.lib.mm_set_option(self.h, int(option), int(value)))
+
+    def project_residuals(self, rho, u_mean):
+        um = np.ascontiguousarray(u_mean, dtype=np.float64).reshape(-1)
+        st = UpdateStatsC()
+        self.check(self.lib.mm_project_residuals(self.h, float(rho), _ptr(um), ctypes.byref(st)))
+        return st
+
+    def update_multiplier(self):
+        st = UpdateStatsC()
+        self.check(self.lib.mm_update_multiplier(self.h, ctypes.byref(st)))
+        return st
+
+    def update_and_sweep(self, material, rho_next, tol, max_sweeps, phi_scale, want_points=False):
+        ls = LocalStatsC()
+        us = UpdateStatsC()
+        self.check(self.lib.mm_update_and_sweep(self.h, int(material), float(rho_next), float(tol),
+                                                int(max_sweeps), float(phi_scale),
+                                                1 if want_points else 0, ctypes.byref(ls),
+                                                ctypes.byref(us)))
+        return ls, us

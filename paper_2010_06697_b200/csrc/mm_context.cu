@@ -272,6 +272,7 @@ int mm_create(int dim, int n, double length, int device, mm_ctx **out) {
     } while (0)
     MM_CUDA(ctx, cudaSetDevice(device));
     MM_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    MM_CUDA(ctx, cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
     const int64_t M = ctx->M;
     TRY(mm_alloc(ctx, (void **)&ctx->F, sizeof(double) * ctx->D * M));
     TRY(mm_alloc(ctx, (void **)&ctx->G, sizeof(double) * ctx->D * M));
@@ -385,6 +386,10 @@ int mm_profile_read(mm_ctx *ctx, mm_profile *out, int reset) {
 
 int mm_upload(mm_ctx *ctx, int field, const double *host, int64_t count) {
     if (!ctx || !host) return MM_ERR_PARAM;
+    {
+        int prc = mm_flush_pending(ctx);
+        if (prc) return prc;
+    }
     double **slot;
     int ncomp;
     int rc = field_info(ctx, field, &slot, &ncomp);
@@ -412,6 +417,10 @@ int mm_upload(mm_ctx *ctx, int field, const double *host, int64_t count) {
 
 int mm_download(mm_ctx *ctx, int field, double *host, int64_t count) {
     if (!ctx || !host) return MM_ERR_PARAM;
+    {
+        int prc = mm_flush_pending(ctx);
+        if (prc) return prc;
+    }
     double **slot;
     int ncomp;
     int rc = field_info(ctx, field, &slot, &ncomp);
@@ -427,6 +436,10 @@ int mm_download(mm_ctx *ctx, int field, double *host, int64_t count) {
 
 int mm_copy_field(mm_ctx *ctx, int dst_field, int src_field) {
     if (!ctx) return MM_ERR_PARAM;
+    {
+        int prc = mm_flush_pending(ctx);
+        if (prc) return prc;
+    }
     double **ds, **ss;
     int nd, ns;
     int rc = field_info(ctx, dst_field, &ds, &nd);
@@ -455,6 +468,10 @@ int mm_copy_field(mm_ctx *ctx, int dst_field, int src_field) {
 
 int mm_field_sums(mm_ctx *ctx, int field, double *out) {
     if (!ctx || !out) return MM_ERR_PARAM;
+    {
+        int prc = mm_flush_pending(ctx);
+        if (prc) return prc;
+    }
     double **slot;
     int ncomp;
     int rc = field_info(ctx, field, &slot, &ncomp);
@@ -498,6 +515,8 @@ int mm_local_sweeps(mm_ctx *ctx, int material, double rho, double tol, int64_t m
     if (material == MM_MAT_MR_DESCENT && (!ctx->modA || !ctx->modB))
         return mm_fail(ctx, MM_ERR_CONFIG, "material moduli were never uploaded");
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    int rc = mm_flush_pending(ctx);
+    if (rc) return rc;
     return mm_run_local(ctx, material, rho, tol, max_sweeps, phi_scale, want_points, out);
 }
 
@@ -528,6 +547,8 @@ int mm_prepare_frozen(mm_ctx *ctx) {
     if (!ctx->have_lce) return mm_fail(ctx, MM_ERR_CONFIG, "LCE parameters were never set");
     if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    int rc = mm_flush_pending(ctx);
+    if (rc) return rc;
     return mm_run_frozen(ctx);
 }
 
@@ -538,7 +559,42 @@ int mm_project(mm_ctx *ctx, double rho, const double *u_mean) {
     if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
     if (!ctx->have_sym) return mm_fail(ctx, MM_ERR_CONFIG, "symbols were never set");
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    int rc = mm_flush_pending(ctx);
+    if (rc) return rc;
     return mm_run_project(ctx, rho, u_mean, 0, nullptr);
+}
+
+int mm_project_residuals(mm_ctx *ctx, double rho, const double *u_mean, mm_update_stats *out) {
+    if (!ctx || !u_mean || !out) return MM_ERR_PARAM;
+    if (!(rho > 0.0) || !isfinite(rho))
+        return mm_fail(ctx, MM_ERR_PARAM, "rho must be positive and finite, got %g", rho);
+    if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
+    if (!ctx->have_sym) return mm_fail(ctx, MM_ERR_CONFIG, "symbols were never set");
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    int rc = mm_flush_pending(ctx);
+    if (rc) return rc;
+    return mm_run_project(ctx, rho, u_mean, 2, out);
+}
+
+int mm_update_multiplier(mm_ctx *ctx, mm_update_stats *out) {
+    if (!ctx || !out) return MM_ERR_PARAM;
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    return mm_run_update(ctx, 0, 0.0, 0.0, 0, 0.0, 0, nullptr, out);
+}
+
+int mm_update_and_sweep(mm_ctx *ctx, int material, double rho_next, double tol,
+                        int64_t max_sweeps, double phi_scale, int want_points,
+                        mm_local_stats *ls, mm_update_stats *us) {
+    if (!ctx || !ls || !us) return MM_ERR_PARAM;
+    if (!(rho_next > 0.0) || !isfinite(rho_next))
+        return mm_fail(ctx, MM_ERR_PARAM, "rho must be positive and finite, got %g", rho_next);
+    if (max_sweeps < 0) return mm_fail(ctx, MM_ERR_PARAM, "max_sweeps must be >= 0");
+    if ((material == MM_MAT_MR || material == MM_MAT_MR_DESCENT || material == MM_MAT_QUADRATIC) &&
+        !ctx->modA)
+        return mm_fail(ctx, MM_ERR_CONFIG, "material moduli were never uploaded");
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    memset(ls, 0, sizeof *ls);
+    return mm_run_update(ctx, material, rho_next, tol, max_sweeps, phi_scale, want_points, ls, us);
 }
 
 int mm_project_update(mm_ctx *ctx, double rho, const double *u_mean, mm_update_stats *out) {
@@ -548,6 +604,8 @@ int mm_project_update(mm_ctx *ctx, double rho, const double *u_mean, mm_update_s
     if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
     if (!ctx->have_sym) return mm_fail(ctx, MM_ERR_CONFIG, "symbols were never set");
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    int rc = mm_flush_pending(ctx);
+    if (rc) return rc;
     return mm_run_project(ctx, rho, u_mean, 1, out);
 }
 

@@ -11,7 +11,7 @@
 
 #include "../../include/mm_admm.h"
 
-#define MM_MAX_PARTIALS 16  // doubles reduced per block by any kernel
+#define MM_MAX_PARTIALS 24  // doubles reduced per block by any kernel
 
 struct mm_ctx {
     int dim = 0, n = 0;
@@ -22,6 +22,7 @@ struct mm_ctx {
     int P = 0;           // spectral row pitch (complex), multiple of 8
     int64_t nrows = 0;   // M / n rows along the contiguous axis
     int device = 0;
+    int num_sms = 148;
     cudaStream_t stream = nullptr;
 
     // device fields, SoA (component-major): comp c of point p at c*M + p
@@ -74,6 +75,8 @@ struct mm_ctx {
     // as ubar + D u_tilde (the gradient field is not stored); G is then a
     // cache filled on demand (downloads, LCE local step).
     bool opt_implicit_g = false;  // MM_OPT_IMPLICIT_GRAD
+    bool lam_pending = false;     // multiplier ascent deferred by mm_project_residuals
+    double pending_rho = 0.0;
     bool g_implicit = false;
     bool g_buf_valid = true;
     double ubar[9] = {0};
@@ -279,3 +282,7 @@ int mm_run_frank_of_ff(mm_ctx *ctx);
 int mm_ilog2(int n);
 GSrc mm_gsrc(mm_ctx *ctx);
 int mm_materialize_G(mm_ctx *ctx);
+int mm_ensure_points(mm_ctx *ctx);
+int mm_flush_pending(mm_ctx *ctx);
+int mm_run_update(mm_ctx *ctx, int material, double rho_next, double tol, int64_t max_sweeps,
+                  double phi_scale, int want_points, mm_local_stats *ls, mm_update_stats *us);

@@ -38,6 +38,97 @@ inline int local_blocks(int64_t M) {
     return (int)std::min<int64_t>(b, 148 * 16);
 }
 
+// One point of the compiled 2D kernel (mooney_rivlin.py:169-255).
+__device__ __forceinline__ void mr2d_point(double &a, double &b, double &c, double &d,
+                                           const double (&gv)[4], double l00, double l01,
+                                           double l10, double l11, double m, double k,
+                                           double rho, double tol, int64_t max_sweeps,
+                                           double phi_scale, double &res, int64_t &nsw) {
+    const double g00 = gv[0], g01 = gv[1], g10 = gv[2], g11 = gv[3];
+    double t = 1.0 / (rho + m + 4.0 * k);
+    const double tmax = 16.0 * t;
+    bool freemode = false;
+    double res_prev = 1e300;
+    res = 0.0;
+    nsw = 0;
+    for (int64_t it = 0; it < max_sweeps + 1; ++it) {
+        const double J = a * d - b * c;
+        const double iJ = 1.0 / J;
+        const double jm1 = J - 1.0;
+        const double s00 = m * (a - d * iJ) + k * jm1 * d;
+        const double s01 = m * (b + c * iJ) - k * jm1 * c;
+        const double s10 = m * (c + b * iJ) - k * jm1 * b;
+        const double s11 = m * (d - a * iJ) + k * jm1 * a;
+        const double r00 = s00 - l00 - rho * (g00 - a);
+        const double r01 = s01 - l01 - rho * (g01 - b);
+        const double r10 = s10 - l10 - rho * (g10 - c);
+        const double r11 = s11 - l11 - rho * (g11 - d);
+        const double gsq = r00 * r00 + r01 * r01 + r10 * r10 + r11 * r11;
+        res = sqrt(gsq);
+        if (freemode) {
+            if (res > res_prev) t *= BT_SHRINK;
+            else t = fmin(t * 1.3, tmax);
+            res_prev = res;
+        }
+        if (res < tol || nsw >= max_sweeps) break;
+        nsw += 1;
+        bool did = false;
+        if (!freemode) {
+            const double W = 0.5 * m * (a * a + b * b + c * c + d * d - 2.0 * log(J) - 2.0) +
+                             0.5 * k * jm1 * jm1;
+            const double phi0 =
+                W - (l00 * a + l01 * b + l10 * c + l11 * d) +
+                0.5 * rho * ((g00 - a) * (g00 - a) + (g01 - b) * (g01 - b) +
+                             (g10 - c) * (g10 - c) + (g11 - d) * (g11 - d));
+            if (BT_DECREASE * t * gsq <= MEAS_EPS * (fabs(phi0) + phi_scale)) {
+                freemode = true;
+                res_prev = res;
+            } else {
+                const double t_in = t;
+                for (int bt = 0; bt < MAX_BT; ++bt) {
+                    const double a2 = a - t * r00, b2 = b - t * r01;
+                    const double c2 = c - t * r10, d2 = d - t * r11;
+                    const double J2 = a2 * d2 - b2 * c2;
+                    if (J2 > 1e-12) {
+                        const double jm2 = J2 - 1.0;
+                        const double W2 =
+                            0.5 * m * (a2 * a2 + b2 * b2 + c2 * c2 + d2 * d2 - 2.0 * log(J2) - 2.0) +
+                            0.5 * k * jm2 * jm2;
+                        const double phi2 =
+                            W2 - (l00 * a2 + l01 * b2 + l10 * c2 + l11 * d2) +
+                            0.5 * rho * ((g00 - a2) * (g00 - a2) + (g01 - b2) * (g01 - b2) +
+                                         (g10 - c2) * (g10 - c2) + (g11 - d2) * (g11 - d2));
+                        if (phi2 <= phi0 - BT_DECREASE * t * gsq) {
+                            a = a2; b = b2; c = c2; d = d2;
+                            did = true;
+                            break;
+                        }
+                    }
+                    t *= BT_SHRINK;
+                }
+                if (did) {
+                    t = fmin(t * 1.6, tmax);
+                } else {
+                    freemode = true;
+                    t = t_in;
+                    res_prev = res;
+                }
+            }
+        }
+        if (freemode && !did) {
+            for (int bt = 0; bt < 12; ++bt) {
+                const double a2 = a - t * r00, b2 = b - t * r01;
+                const double c2 = c - t * r10, d2 = d - t * r11;
+                if (a2 * d2 - b2 * c2 > 1e-12) {
+                    a = a2; b = b2; c = c2; d = d2;
+                    break;
+                }
+                t *= BT_SHRINK;
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // 2D compiled kernel (mooney_rivlin.py:169-255)
 // slots: 0 sum res^2, 1 n_conv, 2 max nsw, 3..6 sum F
@@ -54,90 +145,12 @@ k_mr2d(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
         double a = F[p], b = F[M + p], c = F[2 * M + p], d = F[3 * M + p];
         double gv[4];
         gsrc_load<2>(gs, p, gv);
-        const double g00 = gv[0], g01 = gv[1], g10 = gv[2], g11 = gv[3];
         const double l00 = Lam[p], l01 = Lam[M + p], l10 = Lam[2 * M + p], l11 = Lam[3 * M + p];
         const double m = mu[p], k = kap[p];
-        double t = 1.0 / (rho + m + 4.0 * k);
-        const double tmax = 16.0 * t;
-        bool freemode = false;
-        double res_prev = 1e300, res = 0.0;
-        int64_t nsw = 0;
-        for (int64_t it = 0; it < max_sweeps + 1; ++it) {
-            const double J = a * d - b * c;
-            const double iJ = 1.0 / J;
-            const double jm1 = J - 1.0;
-            const double s00 = m * (a - d * iJ) + k * jm1 * d;
-            const double s01 = m * (b + c * iJ) - k * jm1 * c;
-            const double s10 = m * (c + b * iJ) - k * jm1 * b;
-            const double s11 = m * (d - a * iJ) + k * jm1 * a;
-            const double r00 = s00 - l00 - rho * (g00 - a);
-            const double r01 = s01 - l01 - rho * (g01 - b);
-            const double r10 = s10 - l10 - rho * (g10 - c);
-            const double r11 = s11 - l11 - rho * (g11 - d);
-            const double gsq = r00 * r00 + r01 * r01 + r10 * r10 + r11 * r11;
-            res = sqrt(gsq);
-            if (freemode) {
-                if (res > res_prev) t *= BT_SHRINK;
-                else t = fmin(t * 1.3, tmax);
-                res_prev = res;
-            }
-            if (res < tol || nsw >= max_sweeps) break;
-            nsw += 1;
-            bool did = false;
-            if (!freemode) {
-                const double W = 0.5 * m * (a * a + b * b + c * c + d * d - 2.0 * log(J) - 2.0) +
-                                 0.5 * k * jm1 * jm1;
-                const double phi0 =
-                    W - (l00 * a + l01 * b + l10 * c + l11 * d) +
-                    0.5 * rho * ((g00 - a) * (g00 - a) + (g01 - b) * (g01 - b) +
-                                 (g10 - c) * (g10 - c) + (g11 - d) * (g11 - d));
-                if (BT_DECREASE * t * gsq <= MEAS_EPS * (fabs(phi0) + phi_scale)) {
-                    freemode = true;
-                    res_prev = res;
-                } else {
-                    const double t_in = t;
-                    for (int bt = 0; bt < MAX_BT; ++bt) {
-                        const double a2 = a - t * r00, b2 = b - t * r01;
-                        const double c2 = c - t * r10, d2 = d - t * r11;
-                        const double J2 = a2 * d2 - b2 * c2;
-                        if (J2 > 1e-12) {
-                            const double jm2 = J2 - 1.0;
-                            const double W2 =
-                                0.5 * m * (a2 * a2 + b2 * b2 + c2 * c2 + d2 * d2 - 2.0 * log(J2) - 2.0) +
-                                0.5 * k * jm2 * jm2;
-                            const double phi2 =
-                                W2 - (l00 * a2 + l01 * b2 + l10 * c2 + l11 * d2) +
-                                0.5 * rho * ((g00 - a2) * (g00 - a2) + (g01 - b2) * (g01 - b2) +
-                                             (g10 - c2) * (g10 - c2) + (g11 - d2) * (g11 - d2));
-                            if (phi2 <= phi0 - BT_DECREASE * t * gsq) {
-                                a = a2; b = b2; c = c2; d = d2;
-                                did = true;
-                                break;
-                            }
-                        }
-                        t *= BT_SHRINK;
-                    }
-                    if (did) {
-                        t = fmin(t * 1.6, tmax);
-                    } else {
-                        freemode = true;
-                        t = t_in;
-                        res_prev = res;
-                    }
-                }
-            }
-            if (freemode && !did) {
-                for (int bt = 0; bt < 12; ++bt) {
-                    const double a2 = a - t * r00, b2 = b - t * r01;
-                    const double c2 = c - t * r10, d2 = d - t * r11;
-                    if (a2 * d2 - b2 * c2 > 1e-12) {
-                        a = a2; b = b2; c = c2; d = d2;
-                        break;
-                    }
-                    t *= BT_SHRINK;
-                }
-            }
-        }
+        double res;
+        int64_t nsw;
+        mr2d_point(a, b, c, d, gv, l00, l01, l10, l11, m, k, rho, tol, max_sweeps, phi_scale, res,
+                   nsw);
         F[p] = a; F[M + p] = b; F[2 * M + p] = c; F[3 * M + p] = d;
         if (res_out) res_out[p] = res;
         if (nsw_out) nsw_out[p] = (int32_t)nsw;
@@ -245,6 +258,107 @@ __device__ __forceinline__ bool admissible(const double (&X)[D]) {
     return det_t<D>(X) > 0.0;
 }
 
+// One point of the vectorised descent (base.py:124-230) for global sweeps
+// [s0, s1): X updated in place; t, freem, nsw persist across segments.
+template <int MAT, int D>
+__device__ __forceinline__ void descent_point(double (&X)[D], const double (&B)[D], double cG,
+                                              double m, double k, double rho, double tol,
+                                              double phi_scale, int s0, int s1, double tmax,
+                                              double &t, bool &freem, int &nsw, double &res,
+                                              bool &moved) {
+    double g[D], Xt[D];
+    gradient<MAT, D>(X, B, m, k, rho, g);
+    double gs = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) gs += g[i] * g[i];
+    res = sqrt(gs);
+    moved = false;
+    bool have_phi = false;
+    double phi_cur = 0.0;
+    // a point is active at global sweep s iff it was active at every
+    // earlier sweep (nsw == s) and res > tol; once inactive it stays so
+    for (int s = s0; s < s1; ++s) {
+        if (nsw != s || !(res > tol)) break;
+        nsw += 1;
+        moved = true;
+        bool in_free = freem, in_arm = false;
+        double phi0 = 0.0, gsq = 0.0;
+        if (!freem) {
+            // phi at the current X is known when the previous sweep ended on
+            // an accepted Armijo step or took no step (same X, same bits)
+            phi0 = have_phi ? phi_cur : objective<MAT, D>(X, B, cG, m, k, rho);
+            phi_cur = phi0;
+            have_phi = true;
+#pragma unroll
+            for (int i = 0; i < D; ++i) gsq += g[i] * g[i];
+            // base.py:168-171: unmeasurable decrease -> free mode, and the
+            // point takes this sweep's free step
+            const bool meas = BT_DECREASE * t * gsq > MEAS_EPS * (fabs(phi0) + phi_scale);
+            if (!meas) {
+                freem = true;
+                in_free = true;
+            } else {
+                in_arm = true;
+            }
+        }
+        const double res_before = res;
+        if (in_arm) {
+            const double t_in = t;
+            bool accepted = false;
+            for (int bt = 0; bt < MAX_BT; ++bt) {
+#pragma unroll
+                for (int i = 0; i < D; ++i) Xt[i] = X[i] - t * g[i];
+                double phi_try = INFINITY;
+                if constexpr (MAT == MAT_QUAD) {
+                    phi_try = objective<MAT, D>(Xt, B, cG, m, k, rho);
+                } else {
+                    const double Jt = det_t<D>(Xt);  // admissibility and objective share J
+                    if (Jt > 0.0) phi_try = objective_J<MAT, D>(Xt, Jt, B, cG, m, k, rho);
+                }
+                if (phi_try <= phi0 - BT_DECREASE * t * gsq) {
+#pragma unroll
+                    for (int i = 0; i < D; ++i) X[i] = Xt[i];
+                    phi_cur = phi_try;
+                    accepted = true;
+                    break;
+                }
+                t *= BT_SHRINK;
+            }
+            if (accepted) {
+                t = fmin(t * 1.6, tmax);
+            } else {
+                freem = true;
+                t = t_in;
+            }
+        }
+        if (in_free) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) Xt[i] = X[i] - t * g[i];
+            bool took = admissible<MAT, D>(Xt);
+            for (int bt = 0; bt < 12 && !took; ++bt) {
+                t *= BT_SHRINK;
+#pragma unroll
+                for (int i = 0; i < D; ++i) Xt[i] = X[i] - t * g[i];
+                took = admissible<MAT, D>(Xt);
+            }
+            if (took) {
+#pragma unroll
+                for (int i = 0; i < D; ++i) X[i] = Xt[i];
+                have_phi = false;
+            }
+        }
+        gradient<MAT, D>(X, B, m, k, rho, g);
+        gs = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) gs += g[i] * g[i];
+        res = sqrt(gs);
+        if (in_free) {
+            if (res > res_before) t *= BT_SHRINK;
+            else t = fmin(t * 1.3, tmax);
+        }
+    }
+}
+
 // slots: 0 sum res^2, 1 n_conv (res < tol), 2 max nsw (cumulative),
 //        3 guard sum (sum res where res > tol), 4..4+D sum F
 template <int MAT, int D>
@@ -261,7 +375,7 @@ k_descent(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
     for (int k = 0; k < K; ++k) acc[k] = 0.0;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
          p += (int64_t)gridDim.x * blockDim.x) {
-        double X[D], B[D], g[D], Xt[D];
+        double X[D], B[D];
         double cG = 0.0;
         gsrc_load<(D == 4 ? 2 : 3)>(gs, p, B);  // B holds grad_u until the next line
 #pragma unroll
@@ -285,96 +399,10 @@ k_descent(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
             freem = freestate[p] != 0;
             nsw = nsw_io[p];
         }
-        gradient<MAT, D>(X, B, m, k, rho, g);
-        double gs = 0.0;
-#pragma unroll
-        for (int i = 0; i < D; ++i) gs += g[i] * g[i];
-        double res = sqrt(gs);
+        double res = 0.0;
         bool moved = false;
-        bool have_phi = false;
-        double phi_cur = 0.0;
-        // a point is active at global sweep s iff it was active at every
-        // earlier sweep (nsw == s) and res > tol; once inactive it stays so
-        for (int s = s0; s < s1; ++s) {
-            if (nsw != s || !(res > tol)) break;
-            nsw += 1;
-            moved = true;
-            bool in_free = freem, in_arm = false;
-            double phi0 = 0.0, gsq = 0.0;
-            if (!freem) {
-                // phi at the current X is known when the previous sweep ended on
-                // an accepted Armijo step or took no step (same X, same bits)
-                phi0 = have_phi ? phi_cur : objective<MAT, D>(X, B, cG, m, k, rho);
-                phi_cur = phi0;
-                have_phi = true;
-#pragma unroll
-                for (int i = 0; i < D; ++i) gsq += g[i] * g[i];
-                // base.py:168-171: unmeasurable decrease -> free mode, and the
-                // point takes this sweep's free step
-                const bool meas = BT_DECREASE * t * gsq > MEAS_EPS * (fabs(phi0) + phi_scale);
-                if (!meas) {
-                    freem = true;
-                    in_free = true;
-                } else {
-                    in_arm = true;
-                }
-            }
-            const double res_before = res;
-            if (in_arm) {
-                const double t_in = t;
-                bool accepted = false;
-                for (int bt = 0; bt < MAX_BT; ++bt) {
-#pragma unroll
-                    for (int i = 0; i < D; ++i) Xt[i] = X[i] - t * g[i];
-                    double phi_try = INFINITY;
-                    if constexpr (MAT == MAT_QUAD) {
-                        phi_try = objective<MAT, D>(Xt, B, cG, m, k, rho);
-                    } else {
-                        const double Jt = det_t<D>(Xt);  // admissibility and objective share J
-                        if (Jt > 0.0) phi_try = objective_J<MAT, D>(Xt, Jt, B, cG, m, k, rho);
-                    }
-                    if (phi_try <= phi0 - BT_DECREASE * t * gsq) {
-#pragma unroll
-                        for (int i = 0; i < D; ++i) X[i] = Xt[i];
-                        phi_cur = phi_try;
-                        accepted = true;
-                        break;
-                    }
-                    t *= BT_SHRINK;
-                }
-                if (accepted) {
-                    t = fmin(t * 1.6, tmax);
-                } else {
-                    freem = true;
-                    t = t_in;
-                }
-            }
-            if (in_free) {
-#pragma unroll
-                for (int i = 0; i < D; ++i) Xt[i] = X[i] - t * g[i];
-                bool took = admissible<MAT, D>(Xt);
-                for (int bt = 0; bt < 12 && !took; ++bt) {
-                    t *= BT_SHRINK;
-#pragma unroll
-                    for (int i = 0; i < D; ++i) Xt[i] = X[i] - t * g[i];
-                    took = admissible<MAT, D>(Xt);
-                }
-                if (took) {
-#pragma unroll
-                    for (int i = 0; i < D; ++i) X[i] = Xt[i];
-                    have_phi = false;
-                }
-            }
-            gradient<MAT, D>(X, B, m, k, rho, g);
-            gs = 0.0;
-#pragma unroll
-            for (int i = 0; i < D; ++i) gs += g[i] * g[i];
-            res = sqrt(gs);
-            if (in_free) {
-                if (res > res_before) t *= BT_SHRINK;
-                else t = fmin(t * 1.3, tmax);
-            }
-        }
+        descent_point<MAT, D>(X, B, cG, m, k, rho, tol, phi_scale, s0, s1, tmax, t, freem, nsw,
+                              res, moved);
         if (moved) {
 #pragma unroll
             for (int i = 0; i < D; ++i) F[i * M + p] = X[i];
@@ -400,6 +428,101 @@ k_descent(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
     grid_finalize<K>(acc, ops, partials, red_out, count, smem);
 }
 
+
+
+// ---------------------------------------------------------------------------
+// Multiplier ascent of outer iteration k fused with the first local chunk of
+// iteration k+1 (solver.py:279, then :255-264 of the next call).  The
+// projection already left u_{k+1} current and ubar = <grad u>_{k+1}, so
+// grad_u_{k+1} = ubar + D u is rebuilt in registers; lam_{k+1} =
+// lam_k + rho_k (grad_u - F) is stored; then (SWEEP) the point runs the
+// local sweeps with rho_{k+1} and the policy tolerance, exactly as a
+// standalone first chunk would.  One pass over (u, F, lam, mu, kappa)
+// instead of a gradient pass plus a local pass, and the FP64-heavy sweeps
+// overlap the memory traffic of the update.
+// slots: 0 sum res^2, 1 n_conv, 2 max nsw, 3 guard sum, 4.. sum F (D), then sum lam (D)
+// ALGO: 0 = descent (3D MR, quadratic), 1 = compiled 2D MR kernel
+// ---------------------------------------------------------------------------
+template <int MAT, int D, int ALGO, bool SWEEP>
+__global__ void __launch_bounds__(LOCAL_THREADS, LOCAL_MIN_BLOCKS)
+k_update_local(double *__restrict__ F, double *__restrict__ Lam, const GSrc gs,
+               const double *__restrict__ modA, const double *__restrict__ modB, int64_t M,
+               double rho_k, double rho, double tol, double phi_scale, int chunk,
+               double *__restrict__ res_out, int32_t *__restrict__ nsw_out, double *partials,
+               double *red_out, unsigned int *count) {
+    constexpr int K = 4 + 2 * D;
+    __shared__ double smem[32 * K];
+    double acc[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) acc[q] = 0.0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        double G[D], X[D], L[D];
+        gsrc_load<(D == 4 ? 2 : 3)>(gs, p, G);
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            X[i] = F[i * M + p];
+            L[i] = Lam[i * M + p];
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            L[i] = L[i] + rho_k * (G[i] - X[i]);  // solver.py:277-279
+            Lam[i * M + p] = L[i];
+            acc[4 + D + i] += L[i];
+        }
+        if (SWEEP) {
+            const double m = modA[p];
+            const double k = (MAT == MAT_MR) ? modB[p] : 0.0;
+            double res = 0.0;
+            int nsw = 0;
+            bool moved = false;
+            if constexpr (ALGO == 1) {
+                int64_t nsw64 = 0;
+                double a = X[0], b = X[1], c = X[2], d = X[3];
+                const double gv[4] = {G[0], G[1], G[2], G[3]};
+                mr2d_point(a, b, c, d, gv, L[0], L[1], L[2], L[3], m, k, rho, tol, chunk,
+                           phi_scale, res, nsw64);
+                nsw = (int)nsw64;
+                moved = nsw > 0;
+                X[0] = a; X[1] = b; X[2] = c; X[3] = d;
+            } else {
+                double B[D];
+                double cG = 0.0;
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                    B[i] = L[i] + rho * G[i];
+                    cG += G[i] * G[i];
+                }
+                cG *= 0.5 * rho;
+                const double t0 = (MAT == MAT_MR) ? 1.0 / (rho + m + 4.0 * k) : 1.0 / (rho + m);
+                double t = t0;
+                bool freem = false;
+                descent_point<MAT, D>(X, B, cG, m, k, rho, tol, phi_scale, 0, chunk, t0 * 16.0, t,
+                                      freem, nsw, res, moved);
+            }
+            if (moved) {
+#pragma unroll
+                for (int i = 0; i < D; ++i) F[i * M + p] = X[i];
+            }
+            if (res_out) {
+                res_out[p] = res;
+                nsw_out[p] = nsw;
+            }
+            acc[0] += res * res;
+            acc[1] += (res < tol) ? 1.0 : 0.0;
+            acc[2] = fmax(acc[2], (double)nsw);
+            acc[3] += (res > tol) ? res : 0.0;
+#pragma unroll
+            for (int i = 0; i < D; ++i) acc[4 + i] += X[i];
+        }
+    }
+    int ops[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) ops[q] = RED_SUM;
+    ops[2] = RED_MAX;
+    block_reduce<K>(acc, ops, smem);
+    grid_finalize<K>(acc, ops, partials, red_out, count, smem);
+}
 
 // ---------------------------------------------------------------------------
 // det F > 0 pre-check (base.py:116-121), run once after F is uploaded
@@ -492,7 +615,7 @@ int mm_check_det(mm_ctx *ctx, int *bad) {
     return MM_OK;
 }
 
-static int ensure_points(mm_ctx *ctx) {
+int mm_ensure_points(mm_ctx *ctx) {
     int rc;
     if (!ctx->res && (rc = mm_alloc(ctx, (void **)&ctx->res, sizeof(double) * ctx->M))) return rc;
     if (!ctx->nsw && (rc = mm_alloc(ctx, (void **)&ctx->nsw, sizeof(int32_t) * ctx->M))) return rc;
@@ -537,7 +660,7 @@ int mm_run_local(mm_ctx *ctx, int material, double rho, double tol, int64_t max_
     int rc;
     const int D = ctx->D;
     memset(out, 0, sizeof *out);
-    if (want_points && (rc = ensure_points(ctx))) return rc;
+    if (want_points && (rc = mm_ensure_points(ctx))) return rc;
     if (material == MM_MAT_LCE) return mm_run_lce(ctx, rho, tol, max_sweeps, want_points, out);
     if (material == MM_MAT_MR && ctx->dim == 2) {
         // compiled 2D kernel (mooney_rivlin.py:169-255)
@@ -612,4 +735,70 @@ int mm_run_local(mm_ctx *ctx, int material, double rho, double tol, int64_t max_
     for (int i = 0; i < D; ++i) out->sum_F[i] = r[4 + i];
     if (want_points) MM_CUDA(ctx, cudaMemsetAsync(ctx->ok, 0, ctx->M, ctx->stream));
     return MM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// fused multiplier ascent (+ first local chunk of the next iteration)
+// ---------------------------------------------------------------------------
+template <int MAT, int D, int ALGO, bool SWEEP>
+static int launch_update_local(mm_ctx *ctx, double rho_next, double tol, double phi_scale,
+                               int chunk, bool want_points) {
+    const int blocks = local_blocks(ctx->M);
+    int rc = mm_ensure_partials(ctx, blocks);
+    if (rc) return rc;
+    StageScope ss(ctx, SWEEP ? MM_STAGE_FUSED : MM_STAGE_GRAD);
+    k_update_local<MAT, D, ALGO, SWEEP><<<blocks, LOCAL_THREADS, 0, ctx->stream>>>(
+        ctx->F, ctx->Lam, mm_gsrc(ctx), ctx->modA, MAT == MAT_MR ? ctx->modB : ctx->modA, ctx->M,
+        ctx->pending_rho, rho_next, tol, phi_scale, chunk, want_points ? ctx->res : nullptr,
+        want_points ? ctx->nsw : nullptr, ctx->partials, ctx->red_out, ctx->red_count);
+    MM_LAUNCH_CHECK(ctx);
+    return MM_OK;
+}
+
+int mm_run_update(mm_ctx *ctx, int material, double rho_next, double tol, int64_t max_sweeps,
+                  double phi_scale, int want_points, mm_local_stats *ls, mm_update_stats *us) {
+    int rc;
+    const int D = ctx->D;
+    const bool sweep = ls != nullptr;
+    if (!ctx->lam_pending)
+        return mm_fail(ctx, MM_ERR_CONFIG, "no multiplier update pending (call mm_project_residuals)");
+    if (want_points && (rc = mm_ensure_points(ctx))) return rc;
+    if (!sweep) {
+        // update only; the material does not matter
+        rc = ctx->dim == 2 ? launch_update_local<MAT_QUAD, 4, 0, false>(ctx, 0, 0, 0, 0, false)
+                           : launch_update_local<MAT_QUAD, 9, 0, false>(ctx, 0, 0, 0, 0, false);
+    } else {
+        if (max_sweeps > 64)
+            return mm_fail(ctx, MM_ERR_CONFIG, "fused local chunk limited to 64 sweeps");
+        if (material == MM_MAT_MR_DESCENT || (material == MM_MAT_MR && ctx->dim == 3))
+            rc = ctx->dim == 2 ? launch_update_local<MAT_MR, 4, 0, true>(ctx, rho_next, tol, phi_scale, (int)max_sweeps, want_points)
+                               : launch_update_local<MAT_MR, 9, 0, true>(ctx, rho_next, tol, phi_scale, (int)max_sweeps, want_points);
+        else if (material == MM_MAT_MR)
+            rc = launch_update_local<MAT_MR, 4, 1, true>(ctx, rho_next, tol, phi_scale, (int)max_sweeps, want_points);
+        else if (material == MM_MAT_QUADRATIC)
+            rc = ctx->dim == 2 ? launch_update_local<MAT_QUAD, 4, 0, true>(ctx, rho_next, tol, phi_scale, (int)max_sweeps, want_points)
+                               : launch_update_local<MAT_QUAD, 9, 0, true>(ctx, rho_next, tol, phi_scale, (int)max_sweeps, want_points);
+        else
+            return mm_fail(ctx, MM_ERR_CONFIG, "material %d has no fused local chunk", material);
+    }
+    if (rc) return rc;
+    ctx->lam_pending = false;
+    double r[MM_MAX_PARTIALS];
+    const int K = 4 + 2 * D;
+    if ((rc = mm_fetch_reduction(ctx, K, r))) return rc;
+    for (int i = 0; i < 9; ++i) us->sum_lam[i] = i < D ? r[4 + D + i] : 0.0;
+    if (sweep) {
+        ls->sum_res2 = r[0];
+        ls->n_conv = (int64_t)r[1];
+        ls->sweeps = ctx->M ? (int64_t)r[2] : 0;
+        for (int i = 0; i < 9; ++i) ls->sum_F[i] = i < D ? r[4 + i] : 0.0;
+        if (want_points) MM_CUDA(ctx, cudaMemsetAsync(ctx->ok, 0, ctx->M, ctx->stream));
+    }
+    return MM_OK;
+}
+
+int mm_flush_pending(mm_ctx *ctx) {
+    if (!ctx->lam_pending) return MM_OK;
+    mm_update_stats us;
+    return mm_run_update(ctx, 0, 0.0, 0.0, 0, 0.0, 0, nullptr, &us);
 }

@@ -247,37 +247,41 @@ __device__ __forceinline__ double div_at(const double *__restrict__ F, const dou
     return s;
 }
 
-template <int N1, int N2, int TK>
+template <int N1, int N2, int DIM, int ROWS>
 struct RowCfg {
+    static constexpr int TK = DIM * ROWS;  // lines per tile (component x row)
     static constexpr int NT0 = N1 ? TK * (N1 > N2 ? N1 : N2) : 256;
     static constexpr int NT = NT0 < 64 ? 64 : NT0;
     static constexpr int MINB0 = 65536 / (NT * 96);
     static constexpr int MINB = MINB0 < 1 ? 1 : MINB0;  // aim at <= 96 registers
+    static constexpr int NC = N1 * N2;                  // compile-time line length (0: runtime)
 };
 
-template <int N1, int N2, int TK>
-__global__ void __launch_bounds__(RowCfg<N1, N2, TK>::NT, RowCfg<N1, N2, TK>::MINB)
+// A tile holds ROWS consecutive rows x DIM components; line = c * ROWS + r.
+template <int N1, int N2, int DIM, int ROWS>
+__global__ void __launch_bounds__(RowCfg<N1, N2, DIM, ROWS>::NT, RowCfg<N1, N2, DIM, ROWS>::MINB)
 k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho,
-                          double2 *__restrict__ spec, RowGeom g,
-                          const double2 *__restrict__ tw_line,
-                          const double2 *__restrict__ tw_r2c) {
+          double2 *__restrict__ spec, RowGeom g, const double2 *__restrict__ tw_line,
+          const double2 *__restrict__ tw_r2c) {
+    using C = RowCfg<N1, N2, DIM, ROWS>;
+    constexpr int TK = C::TK, LD = TK + 1;
     extern __shared__ double2 smem_c[];
-    constexpr int LD = TK + 1;
-    const int rows = TK / g.dim;
     double2 *buf = smem_c;
-    double2 *scr = smem_c + (size_t)(g.N + 1) * LD;
-    const int64_t row0 = (int64_t)blockIdx.x * rows;
-    const int N = g.N;
-    // pack: line = c * rows + r.  A work item is (row r, complex slot m) and
-    // produces the slot for every component, so the neighbour-row offsets
-    // are computed once and all loads are issued before any arithmetic.
+    const int N = C::NC ? C::NC : g.N;  // compile-time for power-of-two lines
+    const bool packed = C::NC ? true : (g.packed != 0);
+    double2 *scr = smem_c + (size_t)(N + 1) * LD;
+    const int64_t row0 = (int64_t)blockIdx.x * ROWS;
+    const int64_t M = g.M;
     const double irho = 1.0 / rho;
-    if (g.packed) {
-        for (int w = threadIdx.x; w < rows * N; w += blockDim.x) {
+    // pack: a work item (row r, complex slot m) produces the slot of every
+    // component; all loads of a component are issued before its arithmetic
+    if (packed) {
+        for (int w = threadIdx.x; w < ROWS * N; w += C::NT) {
             const int r = w / N, m = w - r * N;
             const int64_t row = row0 + r;
             if (row >= g.nrows) {
-                for (int c = 0; c < g.dim; ++c) buf[m * LD + c * rows + r] = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int c = 0; c < DIM; ++c) buf[m * LD + c * ROWS + r] = make_double2(0.0, 0.0);
                 continue;
             }
             const RowNbr nb = row_nbrs(g, (int)row);
@@ -285,12 +289,11 @@ k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho
             const int x0 = 2 * m, x1 = 2 * m + 1;
             const int xm = (x0 == 0) ? n - 1 : x0 - 1;
             const int xp = (x1 + 1 == n) ? 0 : x1 + 1;
-            for (int c = 0; c < g.dim; ++c) {
-                const int d = g.dim;
-                const int64_t cz = (int64_t)(c * d) * g.M;          // T_c0 (axis 0)
-                const int64_t cy = (int64_t)(c * d + 1) * g.M;      // T_c1 (axis 1, 3D)
-                const int64_t cx = (int64_t)(c * d + d - 1) * g.M + nb.self;  // contiguous
-                // all loads first
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) {
+                const int64_t cz = (int64_t)(c * DIM) * M;                  // T_c0 (axis 0)
+                const int64_t cy = (int64_t)(c * DIM + 1) * M;              // T_c1 (axis 1, 3D)
+                const int64_t cx = (int64_t)(c * DIM + DIM - 1) * M + nb.self;  // contiguous
                 const double fxm = __ldg(&F[cx + xm]), lxm = __ldg(&L[cx + xm]);
                 const double fx0 = __ldg(&F[cx + x0]), lx0 = __ldg(&L[cx + x0]);
                 const double fx1 = __ldg(&F[cx + x1]), lx1 = __ldg(&L[cx + x1]);
@@ -300,7 +303,7 @@ k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho
                 const double fzm0 = __ldg(&F[cz + nb.zm + x0]), lzm0 = __ldg(&L[cz + nb.zm + x0]);
                 const double fzm1 = __ldg(&F[cz + nb.zm + x1]), lzm1 = __ldg(&L[cz + nb.zm + x1]);
                 double y0 = 0.0, y1 = 0.0;
-                if (d == 3) {
+                if (DIM == 3) {
                     const double fyp0 = __ldg(&F[cy + nb.yp + x0]), lyp0 = __ldg(&L[cy + nb.yp + x0]);
                     const double fyp1 = __ldg(&F[cy + nb.yp + x1]), lyp1 = __ldg(&L[cy + nb.yp + x1]);
                     const double fym0 = __ldg(&F[cy + nb.ym + x0]), lym0 = __ldg(&L[cy + nb.ym + x0]);
@@ -314,13 +317,13 @@ k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho
                       ((fx1 - lx1 * irho) - (fxm - lxm * irho));
                 z.y = ((fzp1 - lzp1 * irho) - (fzm1 - lzm1 * irho)) + y1 +
                       ((fxp - lxp * irho) - (fx0 - lx0 * irho));
-                buf[m * LD + c * rows + r] = z;
+                buf[m * LD + c * ROWS + r] = z;
             }
         }
     } else {
-        for (int w = threadIdx.x; w < TK * N; w += blockDim.x) {
+        for (int w = threadIdx.x; w < TK * N; w += C::NT) {
             const int line = w / N, m = w - line * N;
-            const int c = line / rows, r = line - c * rows;
+            const int c = line / ROWS, r = line - c * ROWS;
             const int64_t row = row0 + r;
             double2 z = make_double2(0.0, 0.0);
             if (row < g.nrows) z.x = div_at(F, L, rho, g, c, row_nbrs(g, (int)row), m);
@@ -330,14 +333,14 @@ k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho
     __syncthreads();
     line_transform<N1, N2, TK, false>(buf, scr, N, tw_line);
     // split (packed) and store k = 0 .. n/2
-    const int nh = g.n / 2 + 1;
-    for (int w = threadIdx.x; w < TK * nh; w += blockDim.x) {
+    const int nh = packed ? N + 1 : g.n / 2 + 1;
+    for (int w = threadIdx.x; w < TK * nh; w += C::NT) {
         const int line = w / nh, k = w - line * nh;
-        const int c = line / rows, r = line - c * rows;
+        const int c = line / ROWS, r = line - c * ROWS;
         const int64_t row = row0 + r;
         if (row >= g.nrows) continue;
         double2 X;
-        if (g.packed) {
+        if (packed) {
             const double2 Zk = buf[(k == N ? 0 : k) * LD + line];
             const double2 Zc = cconj(buf[(k == 0 ? 0 : N - k) * LD + line]);
             const double2 E = cscale(cadd(Zk, Zc), 0.5);
@@ -355,32 +358,32 @@ k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho
 // ---------------------------------------------------------------------------
 // E: inverse C2R along rows -> u_tilde (unnormalised; 1/n^d folded into C)
 // ---------------------------------------------------------------------------
-template <int N1, int N2, int TK>
-__global__ void __launch_bounds__(RowCfg<N1, N2, TK>::NT, RowCfg<N1, N2, TK>::MINB)
+template <int N1, int N2, int DIM, int ROWS>
+__global__ void __launch_bounds__(RowCfg<N1, N2, DIM, ROWS>::NT, RowCfg<N1, N2, DIM, ROWS>::MINB)
 k_row_inv(const double2 *__restrict__ spec, double *__restrict__ Ut, RowGeom g,
-                          const double2 *__restrict__ tw_line,
-                          const double2 *__restrict__ tw_r2c) {
+          const double2 *__restrict__ tw_line, const double2 *__restrict__ tw_r2c) {
+    using C = RowCfg<N1, N2, DIM, ROWS>;
+    constexpr int TK = C::TK, LD = TK + 1;
     extern __shared__ double2 smem_c[];
-    constexpr int LD = TK + 1;
-    const int rows = TK / g.dim;
     double2 *buf = smem_c;
-    double2 *scr = smem_c + (size_t)(g.N + 1) * LD;
-    const int64_t row0 = (int64_t)blockIdx.x * rows;
-    const int N = g.N;
-    const int nh = g.n / 2 + 1;
-    for (int w = threadIdx.x; w < TK * nh; w += blockDim.x) {
+    const int N = C::NC ? C::NC : g.N;
+    const bool packed = C::NC ? true : (g.packed != 0);
+    double2 *scr = smem_c + (size_t)(N + 1) * LD;
+    const int64_t row0 = (int64_t)blockIdx.x * ROWS;
+    const int nh = packed ? N + 1 : g.n / 2 + 1;
+    for (int w = threadIdx.x; w < TK * nh; w += C::NT) {
         const int line = w / nh, k = w - line * nh;
-        const int c = line / rows, r = line - c * rows;
+        const int c = line / ROWS, r = line - c * ROWS;
         const int64_t row = row0 + r;
         double2 X = make_double2(0.0, 0.0);
         if (row < g.nrows) X = spec[((int64_t)c * g.nrows + row) * g.P + k];
         buf[k * LD + line] = X;
     }
     __syncthreads();
-    if (g.packed) {
+    if (packed) {
         // Z[k] = A[k] + i B[k], A = X[k] + conj X[N-k], B = (X[k] - conj X[N-k]) conj(W^k)
         const int npair = N / 2 + 1;
-        for (int w = threadIdx.x; w < TK * npair; w += blockDim.x) {
+        for (int w = threadIdx.x; w < TK * npair; w += C::NT) {
             const int line = w / npair, k = w - line * npair;
             const int kc = N - k;
             const double2 Xk = buf[k * LD + line];
@@ -397,25 +400,27 @@ k_row_inv(const double2 *__restrict__ spec, double *__restrict__ Ut, RowGeom g,
         }
     } else {
         // odd n: full Hermitian spectrum
-        for (int w = threadIdx.x; w < TK * (N - nh); w += blockDim.x) {
+        for (int w = threadIdx.x; w < TK * (N - nh); w += C::NT) {
             const int line = w / (N - nh), k = nh + (w - line * (N - nh));
             buf[k * LD + line] = cconj(buf[(N - k) * LD + line]);
         }
     }
     __syncthreads();
     line_transform<N1, N2, TK, true>(buf, scr, N, tw_line);
-    for (int w = threadIdx.x; w < TK * N; w += blockDim.x) {
-        const int line = w / N, m = w - line * N;
-        const int c = line / rows, r = line - c * rows;
+    // store: a work item (row r, slot m) writes every component of the slot
+    for (int w = threadIdx.x; w < ROWS * N; w += C::NT) {
+        const int r = w / N, m = w - r * N;
         const int64_t row = row0 + r;
         if (row >= g.nrows) continue;
-        const double2 z = buf[m * LD + line];
-        double *dst = Ut + (int64_t)c * g.M + row * g.n;
-        if (g.packed) {
-            dst[2 * m] = z.x;
-            dst[2 * m + 1] = z.y;
-        } else {
-            dst[m] = z.x;
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+            const double2 z = buf[m * LD + c * ROWS + r];
+            double *dst = Ut + (int64_t)c * g.M + row * g.n;
+            if (packed) {
+                *reinterpret_cast<double2 *>(dst + 2 * m) = z;
+            } else {
+                dst[m] = z.x;
+            }
         }
     }
 }
@@ -523,6 +528,104 @@ k_col(double2 *__restrict__ spec, ColGeom g, const double2 *__restrict__ tw) {
     }
 }
 
+// Persistent, software-pipelined variant for power-of-two lines: each block
+// walks tiles t = blockIdx.x, +gridDim.x, ...; while it transforms tile t in
+// one shared buffer, the cp.async (LDGSTS) copies of tile t+gridDim.x land in
+// the other, so global loads are always in flight (the plain variant above is
+// load-latency bound: ncu long_scoreboard stalls dominate).
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc, int src_bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc),
+                 "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND));
+}
+
+struct TileMap {
+    int ntk, n_outer;  // column tiles per line set, outer lines
+};
+
+template <int N1, int N2, int MODE>
+__global__ void __launch_bounds__(ColCfg<N1, N2>::NT, 3)
+k_colp(double2 *__restrict__ spec, ColGeom g, const double2 *__restrict__ tw, TileMap tm,
+       int ntiles) {
+    using C = ColCfg<N1, N2>;
+    constexpr int TK = C::TK, LD = TK + 1, NT = C::NT, N = N1 * N2;
+    constexpr int IT = (N * TK + NT - 1) / NT;
+    extern __shared__ double2 smem_c[];
+    double2 *bufs[2] = {smem_c, smem_c + (size_t)N * LD};
+    auto tile_base = [&](int t, int &k0, int &outer) -> double2 * {
+        const int tk = t % tm.ntk;
+        const int rest = t / tm.ntk;
+        outer = rest % tm.n_outer;
+        const int comp = rest / tm.n_outer;
+        k0 = tk * TK;
+        return spec + comp * g.cs + outer * g.os + k0;
+    };
+    auto issue = [&](int t, double2 *dst) {
+        int k0, outer;
+        const double2 *base = tile_base(t, k0, outer);
+#pragma unroll 2
+        for (int it = 0; it < IT; ++it) {
+            const int w = it * NT + threadIdx.x;
+            if (w < N * TK) {
+                const int n = w / TK, c = w % TK;
+                const bool ok = k0 + c < g.ncol;
+                cp_async16(&dst[n * LD + c], ok ? (const void *)&base[n * g.es + c] : (const void *)base,
+                           ok ? 16 : 0);
+            }
+        }
+        cp_async_commit();
+    };
+    int t = blockIdx.x;
+    if (t < ntiles) issue(t, bufs[0]);
+    for (int iter = 0; t < ntiles; t += gridDim.x, ++iter) {
+        double2 *buf = bufs[iter & 1];
+        const int tn = t + gridDim.x;
+        if (tn < ntiles) issue(tn, bufs[(iter + 1) & 1]);
+        else cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        int k0, outer;
+        double2 *base = tile_base(t, k0, outer);
+        if constexpr (MODE == COL_FWD || MODE == COL_SOLVE)
+            tile_fft<N1, N2, TK, false>(buf, tw);
+        else
+            tile_fft<N1, N2, TK, true>(buf, tw);
+        if constexpr (MODE == COL_SOLVE) {
+            const double *s0 = g.sym;
+            const double *slast = g.sym + (int64_t)(g.dim - 1) * g.n;
+            const double s1 = (g.dim == 3) ? g.sym[g.n + outer] : 0.0;
+#pragma unroll 2
+            for (int it = 0; it < IT; ++it) {
+                const int w = it * NT + threadIdx.x;
+                if (w < N * TK) {
+                    const int kl = w / TK, c = w % TK;
+                    double gsq = s0[kl];
+                    if (g.dim == 3) gsq = gsq + s1;
+                    gsq = gsq + slast[min(k0 + c, g.n - 1)];
+                    const double inv = (gsq > g.thresh) ? 1.0 / gsq : 0.0;
+                    buf[kl * LD + c] = cscale(buf[kl * LD + c], -inv * g.scale);
+                }
+            }
+            __syncthreads();
+            tile_fft<N1, N2, TK, true>(buf, tw);
+        }
+        const bool full = k0 + TK <= g.ncol;
+#pragma unroll 4
+        for (int it = 0; it < IT; ++it) {
+            const int w = it * NT + threadIdx.x;
+            const int n = w / TK, c = w % TK;
+            if (w < N * TK && (full || k0 + c < g.ncol)) base[n * g.es + c] = buf[n * LD + c];
+        }
+        __syncthreads();  // this buffer is refilled two tiles later
+    }
+    cp_async_wait<0>();
+}
+
 // ---------------------------------------------------------------------------
 // F: gradient of u_tilde, multiplier ascent and residual sums
 // slots: 0 sum dG^2, 1 sum misfit^2, 2.. sum lam (D)
@@ -536,7 +639,10 @@ struct Mean9 {
 //       GRAD_IMPL   solver tail with grad_u_old = ubar_old + D u_old implicit
 // The solver modes do not write G: afterwards grad_u is implicit.
 //       GRAD_EXPLW  solver tail, explicit grad_u in and out (reads and writes G)
-enum { GRAD_WRITE = 0, GRAD_EXPL = 1, GRAD_IMPL = 2, GRAD_EXPLW = 3 };
+//       GRAD_RES_EXPL / GRAD_RES_IMPL  residual sums only (r_d, r_p); the ascent is
+//                   deferred to the fused update + local pass (mm_local.cu)
+enum { GRAD_WRITE = 0, GRAD_EXPL = 1, GRAD_IMPL = 2, GRAD_EXPLW = 3, GRAD_RES_EXPL = 4,
+       GRAD_RES_IMPL = 5 };
 
 template <int DIM, int MODE>
 __global__ void __launch_bounds__(256)
@@ -566,7 +672,8 @@ k_grad(const double *__restrict__ Ut, const double *__restrict__ Uold, double *_
             }
         }
         double gold[D], fv[D], lv[D];
-        if (MODE == GRAD_IMPL) {
+        constexpr bool RES = MODE == GRAD_RES_EXPL || MODE == GRAD_RES_IMPL;
+        if (MODE == GRAD_IMPL || MODE == GRAD_RES_IMPL) {
 #pragma unroll
             for (int i = 0; i < DIM; ++i) {
                 const double *u = Uold + (int64_t)i * M + p;
@@ -580,16 +687,21 @@ k_grad(const double *__restrict__ Ut, const double *__restrict__ Uold, double *_
 #pragma unroll
             for (int c = 0; c < D; ++c) {
                 const int64_t o = (int64_t)c * M + p;
-                if (MODE == GRAD_EXPL || MODE == GRAD_EXPLW) gold[c] = G[o];
+                if (MODE == GRAD_EXPL || MODE == GRAD_EXPLW || MODE == GRAD_RES_EXPL) gold[c] = G[o];
                 fv[c] = __ldg(&F[o]);
-                lv[c] = Lam[o];
+                if (!RES) lv[c] = Lam[o];
             }
         }
 #pragma unroll
         for (int c = 0; c < D; ++c) {
             const double gnew = (up[c] - dn[c]) * inv2h + um.v[c];  // projection.py:168
             const int64_t o = (int64_t)c * M + p;
-            if (MODE != GRAD_WRITE) {
+            if (RES) {
+                const double dg = gnew - gold[c];          // solver.py:271
+                const double mis = gnew - fv[c];           // solver.py:277
+                acc[0] += dg * dg;
+                acc[1] += mis * mis;
+            } else if (MODE != GRAD_WRITE) {
                 const double dg = gnew - gold[c];          // solver.py:271
                 const double mis = gnew - fv[c];           // solver.py:277
                 const double lnew = lv[c] + rho * mis;     // solver.py:279
@@ -677,21 +789,21 @@ int launch_smem(mm_ctx *ctx, Kern kern, dim3 grid, int threads, size_t smem) {
     return MM_OK;
 }
 
-template <int N1, int N2, int TK>
+template <int N1, int N2, int DIM, int ROWS>
 int run_rows_t(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double2 *tw_line,
                double *u_out) {
-    const int rows = TK / g.dim;
-    const int threads = RowCfg<N1, N2, TK>::NT;
-    const size_t smem = sizeof(double2) * (size_t)(g.N + 1) * (TK + 1) * (N1 ? 1 : 2);
-    dim3 grid((unsigned)((g.nrows + rows - 1) / rows));
+    using C = RowCfg<N1, N2, DIM, ROWS>;
+    const int threads = C::NT;
+    const size_t smem = sizeof(double2) * (size_t)(g.N + 1) * (C::TK + 1) * (N1 ? 1 : 2);
+    dim3 grid((unsigned)((g.nrows + ROWS - 1) / ROWS));
     if (fwd) {
-        auto kern = k_row_fwd<N1, N2, TK>;
+        auto kern = k_row_fwd<N1, N2, DIM, ROWS>;
         int rc = launch_smem(ctx, kern, grid, threads, smem);
         if (rc) return rc;
         kern<<<grid, threads, smem, ctx->stream>>>(ctx->F, ctx->Lam, rho, ctx->spec, g, tw_line,
                                                    ctx->tw_r2c);
     } else {
-        auto kern = k_row_inv<N1, N2, TK>;
+        auto kern = k_row_inv<N1, N2, DIM, ROWS>;
         int rc = launch_smem(ctx, kern, grid, threads, smem);
         if (rc) return rc;
         kern<<<grid, threads, smem, ctx->stream>>>(ctx->spec, u_out, g, tw_line, ctx->tw_r2c);
@@ -703,14 +815,10 @@ int run_rows_t(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double
 template <int N1, int N2>
 int run_rows_n(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double2 *tw,
                double *u_out) {
-    // lines per tile: TK = dim * rows, bounded so TK*max(N1,N2) <= 512 threads
-    // lines per tile TK = dim * rows: 4 rows (2 for 32-point register FFTs)
-    const bool big = N1 >= 32;
-    if (g.dim == 2)
-        return big ? run_rows_t<N1, N2, 4>(ctx, fwd, rho, g, tw, u_out)
-                   : run_rows_t<N1, N2, 8>(ctx, fwd, rho, g, tw, u_out);
-    return big ? run_rows_t<N1, N2, 6>(ctx, fwd, rho, g, tw, u_out)
-               : run_rows_t<N1, N2, 12>(ctx, fwd, rho, g, tw, u_out);
+    // 4 rows per tile (2 for 32-point register FFTs): <= 384 threads, 3-4 tiles per SM
+    constexpr bool big = N1 >= 32;
+    if (g.dim == 2) return run_rows_t<N1, N2, 2, big ? 2 : 4>(ctx, fwd, rho, g, tw, u_out);
+    return run_rows_t<N1, N2, 3, big ? 2 : 4>(ctx, fwd, rho, g, tw, u_out);
 }
 
 int run_rows(mm_ctx *ctx, bool fwd, double rho, double *u_out = nullptr) {
@@ -739,6 +847,22 @@ template <int N1, int N2, int MODE>
 int run_col_t(mm_ctx *ctx, const ColGeom &g, int n_outer) {
     constexpr int TK = ColCfg<N1, N2>::TK;
     const int threads = ColCfg<N1, N2>::NT;
+    if constexpr (N1 * N2 >= 16) {
+        // persistent pipelined variant
+        const size_t smem2 = sizeof(double2) * (size_t)g.N * (TK + 1) * 2;
+        auto kern = k_colp<N1, N2, MODE>;
+        int rc = launch_smem(ctx, kern, dim3(1), threads, smem2);
+        if (rc) return rc;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem2);
+        if (per_sm < 1) per_sm = 1;
+        TileMap tm{(g.ncol + TK - 1) / TK, n_outer};
+        const int ntiles = tm.ntk * n_outer * ctx->dim;
+        const int blocks = std::min(ntiles, per_sm * ctx->num_sms);
+        kern<<<blocks, threads, smem2, ctx->stream>>>(ctx->spec, g, ctx->tw_full, tm, ntiles);
+        MM_LAUNCH_CHECK(ctx);
+        return MM_OK;
+    }
     const size_t smem = sizeof(double2) * (size_t)g.N * (TK + 1) * (N1 ? 1 : 2);
     dim3 grid((unsigned)((g.ncol + TK - 1) / TK), (unsigned)n_outer, (unsigned)ctx->dim);
     auto kern = k_col<N1, N2, MODE>;
@@ -832,7 +956,7 @@ int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
     }
     // E: C2R rows -> u (new buffer on the solver path)
     double *u_new = ctx->Ut;
-    if (update && ctx->opt_implicit_g) {
+    if (update == 2 || (update && ctx->opt_implicit_g)) {
         if (!ctx->Ut2 && (rc = mm_alloc(ctx, (void **)&ctx->Ut2, sizeof(double) * d * ctx->M)))
             return rc;
         u_new = ctx->Ut2;
@@ -853,6 +977,7 @@ int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
     const double inv2h = 1.0 / (2.0 * ctx->h);
     const int lgn = ilog2_(n);
     const int mode = !update ? GRAD_WRITE
+                     : update == 2 ? (ctx->g_implicit ? GRAD_RES_IMPL : GRAD_RES_EXPL)
                      : !ctx->opt_implicit_g ? GRAD_EXPLW
                      : (ctx->g_implicit ? GRAD_IMPL : GRAD_EXPL);
 #define LAUNCH(DIM, MODE)                                                                       \
@@ -866,11 +991,15 @@ int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
             if (mode == GRAD_WRITE) LAUNCH(2, GRAD_WRITE);
             else if (mode == GRAD_EXPL) LAUNCH(2, GRAD_EXPL);
             else if (mode == GRAD_EXPLW) LAUNCH(2, GRAD_EXPLW);
+            else if (mode == GRAD_RES_EXPL) LAUNCH(2, GRAD_RES_EXPL);
+            else if (mode == GRAD_RES_IMPL) LAUNCH(2, GRAD_RES_IMPL);
             else LAUNCH(2, GRAD_IMPL);
         } else {
             if (mode == GRAD_WRITE) LAUNCH(3, GRAD_WRITE);
             else if (mode == GRAD_EXPL) LAUNCH(3, GRAD_EXPL);
             else if (mode == GRAD_EXPLW) LAUNCH(3, GRAD_EXPLW);
+            else if (mode == GRAD_RES_EXPL) LAUNCH(3, GRAD_RES_EXPL);
+            else if (mode == GRAD_RES_IMPL) LAUNCH(3, GRAD_RES_IMPL);
             else LAUNCH(3, GRAD_IMPL);
         }
     }
@@ -883,7 +1012,7 @@ int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
         ctx->g_buf_valid = true;
         return MM_OK;
     }
-    if (ctx->opt_implicit_g) {
+    if (update == 2 || ctx->opt_implicit_g) {
         // new u becomes current; grad_u is now ubar + D u (implicit)
         std::swap(ctx->Ut, ctx->Ut2);
         ctx->g_implicit = true;
@@ -892,12 +1021,16 @@ int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
         ctx->g_implicit = false;
         ctx->g_buf_valid = true;
     }
+    if (update == 2) {
+        ctx->lam_pending = true;  // lam += rho (grad_u - F) deferred (mm_run_update)
+        ctx->pending_rho = rho;
+    }
     double r[MM_MAX_PARTIALS];
     const int K = 2 + ctx->D;
     if ((rc = mm_fetch_reduction(ctx, K, r))) return rc;
     out->sum_dG2 = r[0];
     out->sum_mis2 = r[1];
-    for (int i = 0; i < 9; ++i) out->sum_lam[i] = i < ctx->D ? r[2 + i] : 0.0;
+    for (int i = 0; i < 9; ++i) out->sum_lam[i] = (i < ctx->D && update != 2) ? r[2 + i] : 0.0;
     return MM_OK;
 }
 

@@ -88,6 +88,10 @@ class MooneyRivlin(MaterialModel):
             self._phi_cache = cached
         return cached[1]
 
+    def _fused_material(self):
+        """Material id and energy scale for the fused ascent + first chunk."""
+        return _lib.MAT_MR, self._phi_scale()
+
     def _device_bind(self, ctx, npts):
         mu, kap = self._flat_moduli(npts)
         ctx.upload(_lib.FIELD_MOD_A, mu)

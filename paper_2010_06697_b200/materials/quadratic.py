@@ -43,17 +43,23 @@ class QuadraticMaterial(MaterialModel):
         c = np.broadcast_to(self.c, lead)
         return c[..., None, None, None, None] * np.einsum("ik,jl->ijkl", eye, eye)
 
+    def _cmax(self):
+        cached = getattr(self, "_cmax_cache", None)
+        if cached is None or cached[0] != id(self.c):
+            cached = (id(self.c), float(np.max(self.c)))
+            self._cmax_cache = cached
+        return cached[1]
+
+    def _fused_material(self):
+        return _lib.MAT_QUADRATIC, self._cmax()
+
     def _device_bind(self, ctx, npts):
         ctx.upload(_lib.FIELD_MOD_A, np.ascontiguousarray(np.broadcast_to(self.c, (npts,)),
                                                           dtype=float))
 
     def _device_local(self, ctx, npts, rho, dt, max_sweeps, point_tol, want_points=False):
         tol = point_tol * self.mu_rep
-        cached = getattr(self, "_cmax", None)
-        if cached is None or cached[0] != id(self.c):
-            cached = (id(self.c), float(np.max(self.c)))
-            self._cmax = cached
-        st = ctx.local_sweeps(self._material_id, rho, tol, max_sweeps, cached[1], want_points)
+        st = ctx.local_sweeps(self._material_id, rho, tol, max_sweeps, self._cmax(), want_points)
         res = None
         if want_points:
             res, _, _ = ctx.download_points()

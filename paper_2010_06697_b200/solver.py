@@ -17,6 +17,7 @@ the same state; the host only ever sees reductions.
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass
 from typing import NamedTuple
@@ -27,6 +28,7 @@ from . import _lib
 from ._engine import STATE_FIELDS, Engine, field_shape
 from .errors import ConvergenceError, DivergenceError, ParameterError
 from .grid import Grid, forward_transform, mean_field, modified_symbols
+from .materials.base import DeviceLocalStats
 from .projection import MacroBC, macro_gradient
 
 __all__ = [
@@ -421,19 +423,118 @@ def solve(grid: Grid, model, bc: MacroBC, params: SolverParams,
                                                                    params.r_d_tol)
     converged = False
     resid = None
-    for _ in range(params.max_outer):
-        resid = outer_iteration(grid, model, state, params, bc, policy, dt=dt)
-        if callback is not None:
-            callback(state, resid)
-        if resid.r_p <= params.r_p_tol and resid.r_d <= params.r_d_tol and resid.r_l <= r_l_tol:
-            converged = True
-            break
+    if callback is None and _fusable(model, policy, bc, grid) and os.environ.get(
+            "MM_FUSE", "1") != "0":
+        converged, resid = _solve_fused(grid, model, bc, params, policy, state, r_l_tol)
+    else:
+        for _ in range(params.max_outer):
+            resid = outer_iteration(grid, model, state, params, bc, policy, dt=dt)
+            if callback is not None:
+                callback(state, resid)
+            if (resid.r_p <= params.r_p_tol and resid.r_d <= params.r_d_tol
+                    and resid.r_l <= r_l_tol):
+                converged = True
+                break
     if not converged and raise_on_max:
         raise ConvergenceError(
             f"no convergence in {params.max_outer} outer iterations "
             f"(r_p={resid.r_p:.3e}, r_d={resid.r_d:.3e})" if resid is not None else
             "no outer iterations allowed", history=state.history)
     return state, converged
+
+
+# ---------------------------------------------------------------------------
+# fused schedule: ascent of iteration k + first local chunk of iteration k+1
+# ---------------------------------------------------------------------------
+
+def _fusable(model, policy, bc, grid) -> bool:
+    """The fused pass covers the Mooney-Rivlin and quadratic local steps with
+    a built-in policy whose chunk fits one launch; no callback may observe
+    the state between iterations (solve() checks that)."""
+    if getattr(model, "_fused_material", None) is None or model._fused_material() is None:
+        return False
+    if type(policy) not in _BUILTIN_POLICIES or policy.chunk > 64:
+        return False
+    return bc.dim == grid.dim
+
+
+def _solve_fused(grid, model, bc, params, policy, state, r_l_tol):
+    """solve()'s loop with the multiplier ascent of iteration k and the first
+    local chunk of iteration k+1 in one device pass (mm_update_and_sweep).
+
+    Every decision the reference takes between those two steps (divergence
+    guard, history, convergence test, penalty update, the policy tolerance
+    from the new r_d) only needs r_p and r_d, which mm_project_residuals
+    returns before the ascent is applied; the per-point arithmetic is the
+    reference's, in the same order.  The last iteration (converged or at
+    max_outer) applies the ascent alone, so the state on return is exactly
+    the unfused one."""
+    eng = state._attach(grid, model)
+    ctx = eng.ctx
+    d = grid.dim
+    npts = grid.npoints
+    mu_rep = model.mu_rep
+    mat, phi_scale = model._fused_material()
+    pending = None  # stats of a first local chunk already run by the fused pass
+    converged = False
+    resid = None
+    for it in range(params.max_outer):
+        t_start = time.perf_counter()
+        tol_pt = policy.target_tol(params, state.r_d_prev)
+        sweeps_total = 0
+        stats = None
+        while True:
+            chunk = min(policy.chunk, params.max_local - sweeps_total)
+            if pending is not None:
+                stats, pending = pending, None
+            else:
+                stats = model._device_local(ctx, npts, state.rho, 0.0, chunk, tol_pt, False)
+            sweeps_total += stats.sweeps
+            if (policy.is_done(stats, sweeps_total) or stats.sweeps < chunk
+                    or sweeps_total >= params.max_local):
+                break
+        state.total_sweeps += sweeps_total
+        state._mark_device("F")
+        r_l = float(np.sqrt(stats.sum_res2 / npts)) / mu_rep
+        F_mean = (stats.sum_F[: d * d] / npts).reshape(d, d)
+        u_mean = macro_gradient(bc, F_mean, eng.lam_mean(), state.rho)
+        up = ctx.project_residuals(state.rho, u_mean)
+        state._mark_device("grad_u", "u_tilde", "lam")
+        r_d = state.rho * float(np.sqrt(up.sum_dG2 / npts)) / mu_rep
+        r_p = float(np.sqrt(up.sum_mis2 / npts))
+        state.u_mean = u_mean
+        state.outer_iter += 1
+        state.r_d_prev = r_d
+        if not np.isfinite(r_p) or r_p > params.divergence_limit:
+            eng.lam_sum = np.array(ctx.update_multiplier().sum_lam[: d * d])
+            raise DivergenceError(
+                f"primal residual {r_p:.3e} at outer iteration {state.outer_iter}")
+        if params.adapt and state.outer_iter > 1:
+            rho_ref = params.rho_init if params.rho_init is not None else model.mu_rep
+            if r_p > params.tau_adapt * r_d:
+                state.rho *= params.kappa_adapt
+            elif r_d > params.tau_adapt * r_p:
+                state.rho = max(state.rho / params.kappa_adapt, params.rho_min_factor * rho_ref)
+        done = r_p <= params.r_p_tol and r_d <= params.r_d_tol and r_l <= r_l_tol
+        last = done or it == params.max_outer - 1
+        if last:
+            eng.lam_sum = np.array(ctx.update_multiplier().sum_lam[: d * d])
+        else:
+            # ascent of this iteration + first local chunk of the next one
+            tol_next = policy.target_tol(params, r_d)
+            chunk = min(policy.chunk, params.max_local)
+            ls, us = ctx.update_and_sweep(mat, state.rho, tol_next * mu_rep, chunk, phi_scale)
+            eng.lam_sum = np.array(us.sum_lam[: d * d])
+            pending = DeviceLocalStats(None, ls.sweeps, float(ls.n_conv) / npts if npts else 1.0,
+                                       ls.sum_res2, list(ls.sum_F))
+        wall_ms = (time.perf_counter() - t_start) * 1e3
+        resid = Residuals(state.outer_iter, float(r_p), float(r_d), float(r_l), float(state.rho),
+                          wall_ms)
+        state.history.append(resid)
+        if done:
+            converged = True
+            break
+    return converged, resid
 
 
 # ---------------------------------------------------------------------------

@@ -1,0 +1,5 @@
+timeout 600 python -m pytest tests -q -m gpu -x > gpurun_out/f_tests.log 2>&1
+MM_FUSE=0 timeout 600 python -m pytest tests/test_gpu_parity.py -q -x > gpurun_out/f_tests_nofuse.log 2>&1
+python tools/profile_solve.py 256 10 > gpurun_out/f_prof.log 2>&1
+MM_FUSE=0 python tools/profile_solve.py 256 10 >> gpurun_out/f_prof.log 2>&1
+python bench.py --steps 10 --warmup 5 --no-cpu-baseline > gpurun_out/f_bench.log 2>&1
