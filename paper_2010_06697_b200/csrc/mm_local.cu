@@ -164,6 +164,26 @@ k_mr2d(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
     grid_finalize<7>(acc, ops, partials, red_out, count, smem);
 }
 
+// Per-thread batch accumulators kept in shared memory ([slot][thread]) so
+// they do not occupy registers across the sweep loop; touched once per point.
+template <int K>
+struct SmemAcc {
+    double *p;
+    __device__ __forceinline__ void init(double *base) {
+        p = base + threadIdx.x;
+#pragma unroll
+        for (int q = 0; q < K; ++q) p[q * LOCAL_THREADS] = 0.0;
+    }
+    __device__ __forceinline__ void add(int q, double v) { p[q * LOCAL_THREADS] += v; }
+    __device__ __forceinline__ void max(int q, double v) {
+        p[q * LOCAL_THREADS] = fmax(p[q * LOCAL_THREADS], v);
+    }
+    __device__ __forceinline__ void load(double (&acc)[K]) const {
+#pragma unroll
+        for (int q = 0; q < K; ++q) acc[q] = p[q * LOCAL_THREADS];
+    }
+};
+
 // ---------------------------------------------------------------------------
 // vectorised descent restated per point (base.py:124-230)
 // ---------------------------------------------------------------------------
@@ -252,6 +272,23 @@ __device__ __forceinline__ void gradient(const double (&X)[D], const double (&B)
     }
 }
 
+// gradient at X with det X = J already known (the accepted trial's det)
+template <int MAT, int D>
+__device__ __forceinline__ void gradient_J(const double (&X)[D], double J, const double (&B)[D],
+                                           double m, double k, double rho, double (&g)[D]) {
+    if constexpr (MAT == MAT_QUAD) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) g[i] = (m + rho) * X[i] - B[i];
+    } else {
+        double C[D];
+        cof_t<D>(X, C);
+        const double iJ = 1.0 / J;
+        const double c2 = k * (J * J - J) - m;
+#pragma unroll
+        for (int i = 0; i < D; ++i) g[i] = (m + rho) * X[i] + c2 * (C[i] * iJ) - B[i];
+    }
+}
+
 template <int MAT, int D>
 __device__ __forceinline__ bool admissible(const double (&X)[D]) {
     if (MAT == MAT_QUAD) return true;
@@ -283,14 +320,15 @@ __device__ __forceinline__ void descent_point(double (&X)[D], const double (&B)[
         moved = true;
         bool in_free = freem, in_arm = false;
         double phi0 = 0.0, gsq = 0.0;
+        double Jacc = 0.0;      // det of the accepted trial point (reused by the gradient)
+        bool armijo_step = false, x_changed = false;
         if (!freem) {
             // phi at the current X is known when the previous sweep ended on
             // an accepted Armijo step or took no step (same X, same bits)
             phi0 = have_phi ? phi_cur : objective<MAT, D>(X, B, cG, m, k, rho);
             phi_cur = phi0;
             have_phi = true;
-#pragma unroll
-            for (int i = 0; i < D; ++i) gsq += g[i] * g[i];
+            gsq = gs;  // same g, same summation order as res (base.py:167 vs :156)
             // base.py:168-171: unmeasurable decrease -> free mode, and the
             // point takes this sweep's free step
             const bool meas = BT_DECREASE * t * gsq > MEAS_EPS * (fabs(phi0) + phi_scale);
@@ -309,15 +347,18 @@ __device__ __forceinline__ void descent_point(double (&X)[D], const double (&B)[
 #pragma unroll
                 for (int i = 0; i < D; ++i) Xt[i] = X[i] - t * g[i];
                 double phi_try = INFINITY;
+                double Jt = 0.0;
                 if constexpr (MAT == MAT_QUAD) {
                     phi_try = objective<MAT, D>(Xt, B, cG, m, k, rho);
                 } else {
-                    const double Jt = det_t<D>(Xt);  // admissibility and objective share J
+                    Jt = det_t<D>(Xt);  // admissibility and objective share J
                     if (Jt > 0.0) phi_try = objective_J<MAT, D>(Xt, Jt, B, cG, m, k, rho);
                 }
                 if (phi_try <= phi0 - BT_DECREASE * t * gsq) {
 #pragma unroll
                     for (int i = 0; i < D; ++i) X[i] = Xt[i];
+                    Jacc = Jt;
+                    armijo_step = x_changed = true;
                     phi_cur = phi_try;
                     accepted = true;
                     break;
@@ -345,13 +386,18 @@ __device__ __forceinline__ void descent_point(double (&X)[D], const double (&B)[
 #pragma unroll
                 for (int i = 0; i < D; ++i) X[i] = Xt[i];
                 have_phi = false;
+                x_changed = true;
             }
         }
-        gradient<MAT, D>(X, B, m, k, rho, g);
-        gs = 0.0;
+        // an unchanged X keeps its gradient, |g|^2 and residual bit for bit
+        if (x_changed) {
+            if (armijo_step) gradient_J<MAT, D>(X, Jacc, B, m, k, rho, g);
+            else gradient<MAT, D>(X, B, m, k, rho, g);
+            gs = 0.0;
 #pragma unroll
-        for (int i = 0; i < D; ++i) gs += g[i] * g[i];
-        res = sqrt(gs);
+            for (int i = 0; i < D; ++i) gs += g[i] * g[i];
+            res = sqrt(gs);
+        }
         if (in_free) {
             if (res > res_before) t *= BT_SHRINK;
             else t = fmin(t * 1.3, tmax);
@@ -370,9 +416,9 @@ k_descent(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
           int32_t *__restrict__ nsw_io, double *partials, double *red_out, unsigned int *count) {
     constexpr int K = 4 + D;
     __shared__ double smem[32 * K];
-    double acc[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) acc[k] = 0.0;
+    __shared__ double sacc[K * LOCAL_THREADS];
+    SmemAcc<K> A;
+    A.init(sacc);
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
          p += (int64_t)gridDim.x * blockDim.x) {
         double X[D], B[D];
@@ -413,13 +459,15 @@ k_descent(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
         }
         if (nsw_io) nsw_io[p] = nsw;
         if (res_out) res_out[p] = res;
-        acc[0] += res * res;
-        acc[1] += (res < tol) ? 1.0 : 0.0;
-        acc[2] = fmax(acc[2], (double)nsw);
-        acc[3] += (res > tol) ? res : 0.0;
+        A.add(0, res * res);
+        A.add(1, (res < tol) ? 1.0 : 0.0);
+        A.max(2, (double)nsw);
+        A.add(3, (res > tol) ? res : 0.0);
 #pragma unroll
-        for (int i = 0; i < D; ++i) acc[4 + i] += X[i];
+        for (int i = 0; i < D; ++i) A.add(4 + i, X[i]);
     }
+    double acc[K];
+    A.load(acc);
     int ops[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) ops[k] = RED_SUM;
@@ -452,9 +500,9 @@ k_update_local(double *__restrict__ F, double *__restrict__ Lam, const GSrc gs,
                double *red_out, unsigned int *count) {
     constexpr int K = 4 + 2 * D;
     __shared__ double smem[32 * K];
-    double acc[K];
-#pragma unroll
-    for (int q = 0; q < K; ++q) acc[q] = 0.0;
+    __shared__ double sacc[K * LOCAL_THREADS];
+    SmemAcc<K> A;
+    A.init(sacc);
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
          p += (int64_t)gridDim.x * blockDim.x) {
         double G[D], X[D], L[D];
@@ -468,7 +516,7 @@ k_update_local(double *__restrict__ F, double *__restrict__ Lam, const GSrc gs,
         for (int i = 0; i < D; ++i) {
             L[i] = L[i] + rho_k * (G[i] - X[i]);  // solver.py:277-279
             Lam[i * M + p] = L[i];
-            acc[4 + D + i] += L[i];
+            A.add(4 + D + i, L[i]);
         }
         if (SWEEP) {
             const double m = modA[p];
@@ -508,14 +556,16 @@ k_update_local(double *__restrict__ F, double *__restrict__ Lam, const GSrc gs,
                 res_out[p] = res;
                 nsw_out[p] = nsw;
             }
-            acc[0] += res * res;
-            acc[1] += (res < tol) ? 1.0 : 0.0;
-            acc[2] = fmax(acc[2], (double)nsw);
-            acc[3] += (res > tol) ? res : 0.0;
+            A.add(0, res * res);
+            A.add(1, (res < tol) ? 1.0 : 0.0);
+            A.max(2, (double)nsw);
+            A.add(3, (res > tol) ? res : 0.0);
 #pragma unroll
-            for (int i = 0; i < D; ++i) acc[4 + i] += X[i];
+            for (int i = 0; i < D; ++i) A.add(4 + i, X[i]);
         }
     }
+    double acc[K];
+    A.load(acc);
     int ops[K];
 #pragma unroll
     for (int q = 0; q < K; ++q) ops[q] = RED_SUM;

@@ -847,7 +847,7 @@ template <int N1, int N2, int MODE>
 int run_col_t(mm_ctx *ctx, const ColGeom &g, int n_outer) {
     constexpr int TK = ColCfg<N1, N2>::TK;
     const int threads = ColCfg<N1, N2>::NT;
-    if constexpr (N1 * N2 >= 16) {
+    if constexpr (N1 * N2 >= 16 && MODE != COL_SOLVE) {
         // persistent pipelined variant
         const size_t smem2 = sizeof(double2) * (size_t)g.N * (TK + 1) * 2;
         auto kern = k_colp<N1, N2, MODE>;
