@@ -305,6 +305,82 @@ def run_ours(args, rank, world, dist):
         print(json.dumps(line), flush=True)
 
 
+def run_slab(args, rank, world, dist):
+    """N > 1: the same n^3 problem split into N slabs along axis 0 (one per
+    GPU), projection transposes as NCCL all-to-alls (paper_2010_06697_b200/
+    slab.py); total work fixed => strong scaling."""
+    import torch
+
+    import paper_2010_06697_b200 as mm
+    from paper_2010_06697_b200.slab import SlabLayout, SlabSolver, TorchComm
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    n = args.n
+    lay = SlabLayout(n, world, rank, 0.5)
+    mu, kap = laminate(n, 3)
+    pts = slice(rank * lay.npts_local, (rank + 1) * lay.npts_local)
+    model = mm.MooneyRivlin(mu[pts].copy(), kap[pts].copy(), dim=3, mu_rep=1.0)
+    bc = mm.MacroBC.strain(np.diag([0.95, 1.0, 1.0]))
+    # the global seeded perturbation, this rank's planes
+    rng = np.random.default_rng(0)
+    pert = rng.standard_normal((n, n, n, 3, 3))[lay.plane_slice()]
+    F = np.broadcast_to(bc.value, lay.local_shape + (3, 3)) + 1e-4 * pert
+    del pert
+    G = np.broadcast_to(bc.value, lay.local_shape + (3, 3)).copy()
+    lam = np.zeros(lay.local_shape + (3, 3))
+    comm = TorchComm(dist, device=f"cuda:{dev}")
+    params = mm.SolverParams(r_p_tol=1e-300, r_d_tol=1e-300)
+    sv = SlabSolver(lay, model, bc, params, mm.RatioToDual(0.3), comm, np.ascontiguousarray(F), G,
+                    lam, device=dev)
+    sv.solve(max_outer=args.warmup)
+    sv.ctx.synchronize()
+    sv.ctx.profile_read(reset=True)
+    sv.ctx.profile_enable(True)
+    sampler = ClockSampler(dev)
+    dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    w0 = time.perf_counter()
+    sv.solve(max_outer=args.steps)
+    sv.ctx.synchronize()
+    torch.cuda.synchronize()
+    dist.barrier()
+    w1 = time.perf_counter()
+    clocks = sampler.stop()
+    ms_total = (w1 - w0) * 1e3
+    t = torch.tensor([ms_total], device=f"cuda:{dev}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    stage_ms, stage_launch = sv.ctx.profile_read(reset=True)
+    M = n ** 3
+    value = M * args.steps / (ms_total / 1e3)
+    peak, peak_kind = measured_peak()
+    it_ms = ms_total / args.steps
+    line = {
+        "metric": "voxel-ADMM-iterations/sec (fp64)", "value": value, "unit": "voxel-iter/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": it_ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (config-2 laminate inputs, seeded)",
+        "config": {"workload": f"3D neo-Hookean laminate {n}^3 split into {world} slabs "
+                               "(SURVEY 8(e): NCCL all-to-all transposes)", "grid": n,
+                   "policy": "RatioToDual(0.3)", "parallelism": f"slab x{world}",
+                   "l2": "inputs larger than L2"},
+        "stages_rank0_ms": {k: round(v / args.steps, 4) for k, v in stage_ms.items() if v},
+        "roofline_iteration": {"bound": "hbm", "B_alg_per_voxel": B_ALG_MR3,
+                               "achieved": round(B_ALG_MR3 * M / (it_ms / 1e3) / 1e9, 1),
+                               "peak": peak * world, "unit": "GB/s",
+                               "frac": round(B_ALG_MR3 * M / (it_ms / 1e3) / 1e9 / (peak * world), 4)},
+        "gpu_launches": int(sum(stage_launch.values())),
+        "clocks": clocks,
+        "e2e": {"value": None, "unit": "voxel-iter/s", "h2d_bytes_per_step": None,
+                "d2h_bytes_per_step": None, "how": "not measured on the multi-GPU path"},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+
 def cpu_baseline(n, steps, warm=1):
     """Oracle port on the host cores, bounded sample of the same workload."""
     import oracle
@@ -400,7 +476,10 @@ def main():
         if args.impl == "reference":
             run_reference(args, rank)
         else:
-            run_ours(args, rank, world, dist)
+            if world > 1:
+                run_slab(args, rank, world, dist)
+            else:
+                run_ours(args, rank, world, dist)
     finally:
         if dist is not None:
             dist.destroy_process_group()

@@ -202,6 +202,29 @@ int mm_update_and_sweep(mm_ctx *ctx, int material, double rho_next, double tol,
                         int64_t max_sweeps, double phi_scale, int want_points,
                         mm_local_stats *ls, mm_update_stats *us);
 
+/* Slab decomposition: rank `rank` of `nranks` holds planes
+ * [rank*n/nranks, (rank+1)*n/nranks) of a 3D n^3 grid (n divisible by
+ * nranks, n even).  Fields (upload/download/local_sweeps) are the local
+ * slab's.  The projection runs as the steps below, with the host moving the
+ * halo planes between neighbours (HALO_OUT -> neighbour's HALO_IN) and doing
+ * the two all-to-all exchanges of SEND -> RECV (after MM_SLAB_FWD) and RECV ->
+ * SEND (after MM_SLAB_SOLVE), e.g. NCCL via torch.distributed:
+ *   HALO_T, [exchange], FWD, [all-to-all], SOLVE, [all-to-all back], INV,
+ *   HALO_U, [exchange], UPDATE (sums[0..10] = |dG|^2, |misfit|^2, sum lam)
+ * Buffers: MM_SLAB_BUF_SEND / RECV  nranks * 3 * (n/nranks)^2 * pitch complex,
+ * [peer][c][i0l][i1l][k2]; HALO_*  3 * n^2 doubles [c][i1][i2]. */
+enum mm_slab_step {
+    MM_SLAB_HALO_T = 0, MM_SLAB_FWD = 1, MM_SLAB_SOLVE = 2, MM_SLAB_INV = 3, MM_SLAB_HALO_U = 4,
+    MM_SLAB_UPDATE = 5, MM_SLAB_GRAD = 6
+};
+enum mm_slab_buffer {
+    MM_SLAB_BUF_SEND = 0, MM_SLAB_BUF_RECV = 1, MM_SLAB_BUF_HALO_OUT_LO = 2,
+    MM_SLAB_BUF_HALO_OUT_HI = 3, MM_SLAB_BUF_HALO_IN_LO = 4, MM_SLAB_BUF_HALO_IN_HI = 5
+};
+int mm_create_slab(int n, double length, int nranks, int rank, int device, mm_ctx **out);
+int mm_slab_buffer(mm_ctx *ctx, int which, void **dev_ptr, int64_t *nbytes);
+int mm_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, double *sums);
+
 /* Options.  MM_OPT_IMPLICIT_GRAD (default 0): after a fused projection keep
  * grad_u implicitly as u_mean + D u_tilde instead of storing the 9-component
  * field (the local step and the next update rebuild it with the same

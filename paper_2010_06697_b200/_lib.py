@@ -39,7 +39,12 @@ EXPORTS = (
     "mm_prepare_frozen", "mm_project", "mm_project_update", "mm_stencil",
     "mm_profile_enable", "mm_profile_read", "mm_frank_stencil", "mm_set_option",
     "mm_project_residuals", "mm_update_multiplier", "mm_update_and_sweep",
+    "mm_create_slab", "mm_slab_buffer", "mm_slab_step",
 )
+
+SLAB_HALO_T, SLAB_FWD, SLAB_SOLVE, SLAB_INV, SLAB_HALO_U, SLAB_UPDATE, SLAB_GRAD = range(7)
+SLAB_BUF_SEND, SLAB_BUF_RECV, SLAB_BUF_HALO_OUT_LO, SLAB_BUF_HALO_OUT_HI = range(4)
+SLAB_BUF_HALO_IN_LO, SLAB_BUF_HALO_IN_HI = 4, 5
 
 STAGES = ("local", "row_fwd", "col_fwd", "col_solve", "col_inv", "row_inv", "grad", "frozen",
           "other", "fused")
@@ -108,6 +113,9 @@ def load_library():
             "mm_frank_stencil": ([P], I),
             "mm_set_option": ([P, I, I64], I),
             "mm_project_residuals": ([P, D, P, ctypes.POINTER(UpdateStatsC)], I),
+            "mm_create_slab": ([I, D, I, I, I, PP], I),
+            "mm_slab_buffer": ([P, I, PP, ctypes.POINTER(I64)], I),
+            "mm_slab_step": ([P, I, D, P, P], I),
             "mm_update_multiplier": ([P, ctypes.POINTER(UpdateStatsC)], I),
             "mm_update_and_sweep": ([P, I, D, D, I64, D, I, ctypes.POINTER(LocalStatsC),
                                      ctypes.POINTER(UpdateStatsC)], I),
@@ -143,12 +151,18 @@ def _require_device(device):
 class Context:
     """One device context (mm_ctx): a periodic grid, or a bare point set."""
 
-    def __init__(self, dim, n=None, length=None, npts=None, device=None):
+    def __init__(self, dim, n=None, length=None, npts=None, device=None, slab=None):
         self.lib = load_library()
         self.device = _require_device(device)
         self.dim = int(dim)
         h = ctypes.c_void_p()
-        if n is not None:
+        if slab is not None:
+            nranks, rank = slab
+            rc = self.lib.mm_create_slab(int(n), float(length), int(nranks), int(rank),
+                                         self.device, ctypes.byref(h))
+            self.npts = (int(n) // int(nranks)) * int(n) ** 2
+            self.n = int(n)
+        elif n is not None:
             rc = self.lib.mm_create(self.dim, int(n), float(length), self.device, ctypes.byref(h))
             self.npts = int(n) ** self.dim
             self.n = int(n)
@@ -287,3 +301,28 @@ class Context:
                                                 1 if want_points else 0, ctypes.byref(ls),
                                                 ctypes.byref(us)))
         return ls, us
+
+    # -- slab decomposition ------------------------------------------------------
+    def slab_buffer(self, which):
+        ptr = ctypes.c_void_p()
+        nbytes = ctypes.c_int64()
+        self.check(self.lib.mm_slab_buffer(self.h, int(which), ctypes.byref(ptr),
+                                           ctypes.byref(nbytes)))
+        return ptr.value, nbytes.value
+
+    def slab_step(self, step, rho, u_mean=None):
+        sums = np.zeros(11)
+        um = None if u_mean is None else np.ascontiguousarray(u_mean, dtype=np.float64).reshape(-1)
+        self.check(self.lib.mm_slab_step(self.h, int(step), float(rho),
+                                         _ptr(um) if um is not None else None, _ptr(sums)))
+        return sums
+
+
+class DeviceArray:
+    """__cuda_array_interface__ view of a device buffer owned by a Context
+    (lets torch / NCCL move it without copies)."""
+
+    def __init__(self, ptr, shape, typestr="<f8", owner=None):
+        self.__cuda_array_interface__ = {"shape": tuple(int(x) for x in shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3}
+        self._owner = owner

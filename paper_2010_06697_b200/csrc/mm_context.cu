@@ -299,6 +299,103 @@ int mm_create(int dim, int n, double length, int device, mm_ctx **out) {
     return MM_OK;
 }
 
+int mm_create_slab(int n, double length, int nranks, int rank, int device, mm_ctx **out) {
+    if (!out) return MM_ERR_PARAM;
+    *out = nullptr;
+    if (n < 4 || n % 2 || nranks < 1 || n % nranks || rank < 0 || rank >= nranks ||
+        !(length > 0.0))
+        return MM_ERR_CONFIG;
+    mm_ctx *ctx = new mm_ctx();
+    const int dim = 3;
+    ctx->dim = dim;
+    ctx->n = n;
+    ctx->L = length;
+    ctx->h = 2.0 * length / n;
+    ctx->slab_mode = true;
+    ctx->slab_P = nranks;
+    ctx->slab_rank = rank;
+    ctx->slab_nl = n / nranks;
+    ctx->M = (int64_t)ctx->slab_nl * n * n;
+    ctx->D = 9;
+    ctx->nh = n / 2 + 1;
+    ctx->P = (ctx->nh + 7) / 8 * 8;
+    ctx->nrows = (int64_t)ctx->slab_nl * n;
+    ctx->device = device;
+    *out = ctx;
+    int rc;
+#define TRY(x)             \
+    do {                   \
+        rc = (x);          \
+        if (rc) return rc; \
+    } while (0)
+    MM_CUDA(ctx, cudaSetDevice(device));
+    MM_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    MM_CUDA(ctx, cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+    const int64_t M = ctx->M;
+    const int64_t nn = (int64_t)n * n;
+    const int64_t nl = ctx->slab_nl;
+    TRY(mm_alloc(ctx, (void **)&ctx->F, sizeof(double) * 9 * M));
+    TRY(mm_alloc(ctx, (void **)&ctx->G, sizeof(double) * 9 * M));
+    TRY(mm_alloc(ctx, (void **)&ctx->Lam, sizeof(double) * 9 * M));
+    TRY(mm_alloc(ctx, (void **)&ctx->Ut, sizeof(double) * 3 * M));
+    TRY(mm_alloc(ctx, (void **)&ctx->spec, sizeof(double2) * 3 * ctx->nrows * ctx->P));
+    const int64_t bufc = (int64_t)nranks * 3 * nl * nl * ctx->P;
+    TRY(mm_alloc(ctx, (void **)&ctx->sendbuf, sizeof(double2) * bufc));
+    TRY(mm_alloc(ctx, (void **)&ctx->recvbuf, sizeof(double2) * bufc));
+    TRY(mm_alloc(ctx, (void **)&ctx->halo_in_lo, sizeof(double) * 3 * nn));
+    TRY(mm_alloc(ctx, (void **)&ctx->halo_in_hi, sizeof(double) * 3 * nn));
+    TRY(mm_alloc(ctx, (void **)&ctx->halo_out_lo, sizeof(double) * 3 * nn));
+    TRY(mm_alloc(ctx, (void **)&ctx->halo_out_hi, sizeof(double) * 3 * nn));
+    TRY(mm_alloc(ctx, (void **)&ctx->sym, sizeof(double) * dim * n));
+    TRY(mm_alloc(ctx, (void **)&ctx->red_out, sizeof(double) * MM_MAX_PARTIALS));
+    TRY(mm_alloc(ctx, (void **)&ctx->red_count, sizeof(unsigned int) * 4));
+    MM_CUDA(ctx, cudaMemset(ctx->red_count, 0, sizeof(unsigned int) * 4));
+    MM_CUDA(ctx, cudaMallocHost((void **)&ctx->host_out, sizeof(double) * MM_MAX_PARTIALS));
+    MM_CUDA(ctx, cudaMemset(ctx->F, 0, sizeof(double) * 9 * M));
+    MM_CUDA(ctx, cudaMemset(ctx->G, 0, sizeof(double) * 9 * M));
+    MM_CUDA(ctx, cudaMemset(ctx->Lam, 0, sizeof(double) * 9 * M));
+    MM_CUDA(ctx, cudaMemset(ctx->Ut, 0, sizeof(double) * 3 * M));
+    MM_CUDA(ctx, cudaMemset(ctx->spec, 0, sizeof(double2) * 3 * ctx->nrows * ctx->P));
+    MM_CUDA(ctx, cudaMemset(ctx->sendbuf, 0, sizeof(double2) * bufc));
+    MM_CUDA(ctx, cudaMemset(ctx->recvbuf, 0, sizeof(double2) * bufc));
+    TRY(upload_tw(ctx, &ctx->tw_full, n));
+    TRY(upload_tw(ctx, &ctx->tw_half, n / 2));
+    TRY(upload_tw(ctx, &ctx->tw_r2c, n));
+    TRY(mm_ensure_partials(ctx, 4096));
+#undef TRY
+    return MM_OK;
+}
+
+int mm_slab_buffer(mm_ctx *ctx, int which, void **dev_ptr, int64_t *nbytes) {
+    if (!ctx || !dev_ptr || !nbytes) return MM_ERR_PARAM;
+    if (!ctx->slab_mode) return mm_fail(ctx, MM_ERR_CONFIG, "not a slab context");
+    const int64_t nn = (int64_t)ctx->n * ctx->n;
+    const int64_t nl = ctx->slab_nl;
+    const int64_t bufb = (int64_t)ctx->slab_P * 3 * nl * nl * ctx->P * (int64_t)sizeof(double2);
+    switch (which) {
+        case MM_SLAB_BUF_SEND: *dev_ptr = ctx->sendbuf; *nbytes = bufb; break;
+        case MM_SLAB_BUF_RECV: *dev_ptr = ctx->recvbuf; *nbytes = bufb; break;
+        case MM_SLAB_BUF_HALO_OUT_LO: *dev_ptr = ctx->halo_out_lo; *nbytes = 3 * nn * 8; break;
+        case MM_SLAB_BUF_HALO_OUT_HI: *dev_ptr = ctx->halo_out_hi; *nbytes = 3 * nn * 8; break;
+        case MM_SLAB_BUF_HALO_IN_LO: *dev_ptr = ctx->halo_in_lo; *nbytes = 3 * nn * 8; break;
+        case MM_SLAB_BUF_HALO_IN_HI: *dev_ptr = ctx->halo_in_hi; *nbytes = 3 * nn * 8; break;
+        default: return mm_fail(ctx, MM_ERR_PARAM, "unknown slab buffer %d", which);
+    }
+    return MM_OK;
+}
+
+int mm_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, double *sums) {
+    if (!ctx) return MM_ERR_PARAM;
+    if (!ctx->slab_mode) return mm_fail(ctx, MM_ERR_CONFIG, "not a slab context");
+    if (!(rho > 0.0) || !isfinite(rho))
+        return mm_fail(ctx, MM_ERR_PARAM, "rho must be positive and finite, got %g", rho);
+    if (!ctx->have_sym) return mm_fail(ctx, MM_ERR_CONFIG, "symbols were never set");
+    if ((step == MM_SLAB_UPDATE || step == MM_SLAB_GRAD) && !u_mean) return MM_ERR_PARAM;
+    if (step == MM_SLAB_UPDATE && !sums) return MM_ERR_PARAM;
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    return mm_run_slab_step(ctx, step, rho, u_mean, sums);
+}
+
 int mm_create_points(int dim, int64_t npts, int device, mm_ctx **out) {
     if (!out) return MM_ERR_PARAM;
     *out = nullptr;
@@ -335,11 +432,14 @@ void mm_destroy(mm_ctx *ctx) {
     for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
     double *ptrs[] = {ctx->F, ctx->G, ctx->Lam, ctx->Ut, ctx->prevF, ctx->modA, ctx->modB,
                       ctx->ang, ctx->chart, ctx->pinc, ctx->n0, ctx->ff, ctx->prevAng,
-                      ctx->prevChart, ctx->prevPinc, ctx->dirbuf, ctx->Ut2, ctx->sym, ctx->partials, ctx->red_out,
+                      ctx->prevChart, ctx->prevPinc, ctx->dirbuf, ctx->Ut2, ctx->halo_in_lo,
+                      ctx->halo_in_hi, ctx->halo_out_lo, ctx->halo_out_hi, ctx->sym, ctx->partials, ctx->red_out,
                       ctx->res, ctx->tstate, ctx->stage};
     for (double *p : ptrs)
         if (p) cudaFree(p);
     if (ctx->spec) cudaFree(ctx->spec);
+    if (ctx->sendbuf) cudaFree(ctx->sendbuf);
+    if (ctx->recvbuf) cudaFree(ctx->recvbuf);
     if (ctx->tw_full) cudaFree(ctx->tw_full);
     if (ctx->tw_half) cudaFree(ctx->tw_half);
     if (ctx->tw_r2c) cudaFree(ctx->tw_r2c);
@@ -554,6 +654,7 @@ int mm_prepare_frozen(mm_ctx *ctx) {
 
 int mm_project(mm_ctx *ctx, double rho, const double *u_mean) {
     if (!ctx || !u_mean) return MM_ERR_PARAM;
+    if (ctx->slab_mode) return mm_fail(ctx, MM_ERR_CONFIG, "slab context: use mm_slab_step");
     if (!(rho > 0.0) || !isfinite(rho))
         return mm_fail(ctx, MM_ERR_PARAM, "rho must be positive and finite, got %g", rho);
     if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
@@ -566,6 +667,7 @@ int mm_project(mm_ctx *ctx, double rho, const double *u_mean) {
 
 int mm_project_residuals(mm_ctx *ctx, double rho, const double *u_mean, mm_update_stats *out) {
     if (!ctx || !u_mean || !out) return MM_ERR_PARAM;
+    if (ctx->slab_mode) return mm_fail(ctx, MM_ERR_CONFIG, "slab context: use mm_slab_step");
     if (!(rho > 0.0) || !isfinite(rho))
         return mm_fail(ctx, MM_ERR_PARAM, "rho must be positive and finite, got %g", rho);
     if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
@@ -599,6 +701,7 @@ int mm_update_and_sweep(mm_ctx *ctx, int material, double rho_next, double tol,
 
 int mm_project_update(mm_ctx *ctx, double rho, const double *u_mean, mm_update_stats *out) {
     if (!ctx || !u_mean || !out) return MM_ERR_PARAM;
+    if (ctx->slab_mode) return mm_fail(ctx, MM_ERR_CONFIG, "slab context: use mm_slab_step");
     if (!(rho > 0.0) || !isfinite(rho))
         return mm_fail(ctx, MM_ERR_PARAM, "rho must be positive and finite, got %g", rho);
     if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");

@@ -82,7 +82,13 @@ struct mm_ctx {
     double ubar[9] = {0};
     double *Ut2 = nullptr;  // second u_tilde buffer (new u during a projection)
     bool F_checked = false;
-    bool points_only = false;    // F verified admissible since the last upload
+    bool points_only = false;
+    // slab decomposition (3D, split along axis 0)
+    bool slab_mode = false;
+    int slab_P = 1, slab_rank = 0, slab_nl = 0;
+    double2 *sendbuf = nullptr, *recvbuf = nullptr;
+    double *halo_in_lo = nullptr, *halo_in_hi = nullptr, *halo_out_lo = nullptr,
+           *halo_out_hi = nullptr;    // F verified admissible since the last upload
     int64_t bytes = 0;
     std::string err;
 };
@@ -280,6 +286,7 @@ int mm_check_det(mm_ctx *ctx, int *bad);
 int mm_run_stencil(mm_ctx *ctx, int op);
 int mm_run_frank_of_ff(mm_ctx *ctx);
 int mm_ilog2(int n);
+int mm_run_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, double *sums);
 GSrc mm_gsrc(mm_ctx *ctx);
 int mm_materialize_G(mm_ctx *ctx);
 int mm_ensure_points(mm_ctx *ctx);

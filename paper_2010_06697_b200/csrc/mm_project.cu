@@ -187,6 +187,10 @@ struct RowGeom {
     int P;          // spectral pitch
     int N;          // complex line length (n/2 packed, or n when odd)
     int packed;     // 1: two reals per complex (even n)
+    // slab mode (3D): nl local planes; T_c0 of the plane below the first /
+    // above the last local plane come from neighbour ranks ([c][i1*n + x]).
+    int nl;
+    const double *hlo, *hhi;
 };
 
 // ---------------------------------------------------------------------------
@@ -200,14 +204,26 @@ __device__ __forceinline__ double tval(const double *__restrict__ F, const doubl
 // start offsets (row * n) of a row and of its neighbour rows along axes 0, 1
 struct RowNbr {
     int64_t self, zp, zm, yp, ym;
+    bool zp_h, zm_h;  // axis-0 neighbour lives in the halo plane (slab mode)
+    int hoff;         // offset of this row inside a halo plane
 };
 
 __device__ __forceinline__ RowNbr row_nbrs(const RowGeom &g, int row) {
     const int n = g.n;
     RowNbr r;
+    r.zp_h = r.zm_h = false;
+    r.hoff = 0;
     if (g.dim == 3) {
         const int i0 = row / n, i1 = row - i0 * n;
-        const int i0p = (i0 + 1 == n) ? 0 : i0 + 1, i0m = (i0 == 0) ? n - 1 : i0 - 1;
+        const int nl = g.nl;
+        int i0p = (i0 + 1 == nl) ? 0 : i0 + 1, i0m = (i0 == 0) ? nl - 1 : i0 - 1;
+        if (g.hhi) {  // slab: neighbours across the slab faces come from halos
+            r.zp_h = (i0 + 1 == nl);
+            r.zm_h = (i0 == 0);
+            if (r.zp_h) i0p = i0;
+            if (r.zm_h) i0m = i0;
+            r.hoff = i1 * n;
+        }
         const int i1p = (i1 + 1 == n) ? 0 : i1 + 1, i1m = (i1 == 0) ? n - 1 : i1 - 1;
         r.zp = (int64_t)(i0p * n + i1) * n;
         r.zm = (int64_t)(i0m * n + i1) * n;
@@ -312,11 +328,22 @@ k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho
                     y1 = (fyp1 - lyp1 * irho) - (fym1 - lym1 * irho);
                 }
                 // T = F - lam/rho (projection.py:154), as F - lam * (1/rho)
+                double tzp0 = fzp0 - lzp0 * irho, tzp1 = fzp1 - lzp1 * irho;
+                double tzm0 = fzm0 - lzm0 * irho, tzm1 = fzm1 - lzm1 * irho;
+                if (DIM == 3 && (nb.zp_h || nb.zm_h)) {
+                    const int64_t hp = (int64_t)c * n * n + nb.hoff;
+                    if (nb.zp_h) {
+                        tzp0 = g.hhi[hp + x0];
+                        tzp1 = g.hhi[hp + x1];
+                    }
+                    if (nb.zm_h) {
+                        tzm0 = g.hlo[hp + x0];
+                        tzm1 = g.hlo[hp + x1];
+                    }
+                }
                 double2 z;
-                z.x = ((fzp0 - lzp0 * irho) - (fzm0 - lzm0 * irho)) + y0 +
-                      ((fx1 - lx1 * irho) - (fxm - lxm * irho));
-                z.y = ((fzp1 - lzp1 * irho) - (fzm1 - lzm1 * irho)) + y1 +
-                      ((fxp - lxp * irho) - (fx0 - lx0 * irho));
+                z.x = (tzp0 - tzm0) + y0 + ((fx1 - lx1 * irho) - (fxm - lxm * irho));
+                z.y = (tzp1 - tzm1) + y1 + ((fxp - lxp * irho) - (fx0 - lx0 * irho));
                 buf[m * LD + c * ROWS + r] = z;
             }
         }
@@ -830,6 +857,9 @@ int run_rows(mm_ctx *ctx, bool fwd, double rho, double *u_out = nullptr) {
     g.P = ctx->P;
     g.packed = (ctx->n % 2 == 0) ? 1 : 0;
     g.N = g.packed ? ctx->n / 2 : ctx->n;
+    g.nl = ctx->slab_mode ? ctx->slab_nl : ctx->n;
+    g.hlo = ctx->slab_mode ? ctx->halo_in_lo : nullptr;
+    g.hhi = ctx->slab_mode ? ctx->halo_in_hi : nullptr;
     const double2 *tw = g.packed ? ctx->tw_half : ctx->tw_full;
     int N1, N2;
     factor(g.N, N1, N2);
@@ -1102,4 +1132,291 @@ int mm_run_stencil(mm_ctx *ctx, int op) {
     }
     MM_LAUNCH_CHECK(ctx);
     return MM_OK;
+}
+
+// ===========================================================================
+// Slab decomposition (one rank's part of a 3D grid split along axis 0).
+// The host moves halos and runs the two all-to-all transposes with NCCL
+// (paper_2010_06697_b200/slab.py); these entry points are the per-rank compute.
+// ===========================================================================
+namespace {
+
+// T_c0 (or u) of the first / last local plane -> halo send buffers [c][i1*n + x]
+__global__ void k_slab_halo(const double *__restrict__ A, const double *__restrict__ B,
+                            double irho, int stride_c, int nc, int n, int nl, int64_t M,
+                            double *__restrict__ lo, double *__restrict__ hi) {
+    const int64_t nn = (int64_t)n * n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc * nn;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i / nn);
+        const int64_t q = i - c * nn;
+        const int64_t comp = (int64_t)c * stride_c * M;
+        const int64_t o0 = comp + q, o1 = comp + (int64_t)(nl - 1) * nn + q;
+        if (B) {  // T = F - lam * (1/rho), the expression the divergence uses
+            lo[i] = A[o0] - B[o0] * irho;
+            hi[i] = A[o1] - B[o1] * irho;
+        } else {
+            lo[i] = A[o0];
+            hi[i] = A[o1];
+        }
+    }
+}
+
+// column transform with two-level line addressing, out of place:
+// element j of a line sits at (j / blk) * sq + (j % blk) * es (+ outer, comp, column)
+struct SlabCol {
+    const double2 *src;
+    double2 *dst;
+    int blk_s, blk_d;
+    int64_t s_sq, s_es, s_os, s_cs;
+    int64_t d_sq, d_es, d_os, d_cs;
+    int outer_off;  // global index of outer line 0 along axis 1 (solve symbols)
+};
+
+template <int N1, int N2, int MODE>
+__global__ void __launch_bounds__(ColCfg<N1, N2>::NT)
+k_col_slab(ColGeom g, SlabCol sc, const double2 *__restrict__ tw) {
+    constexpr int TK = ColCfg<N1, N2>::TK, LD = TK + 1;
+    extern __shared__ double2 smem_c[];
+    double2 *buf = smem_c;
+    double2 *scr = smem_c + (size_t)g.N * LD;
+    const int k0 = blockIdx.x * TK;
+    const int outer = blockIdx.y;
+    const int comp = blockIdx.z;
+    const int N = g.N;
+    const double2 *sb = sc.src + comp * sc.s_cs + outer * sc.s_os + k0;
+    double2 *db = sc.dst + comp * sc.d_cs + outer * sc.d_os + k0;
+    for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
+        const int n = w / TK, c = w - n * TK;
+        double2 v = make_double2(0.0, 0.0);
+        if (k0 + c < g.ncol) v = sb[(n / sc.blk_s) * sc.s_sq + (n % sc.blk_s) * sc.s_es + c];
+        buf[n * LD + c] = v;
+    }
+    __syncthreads();
+    if constexpr (MODE == COL_FWD || MODE == COL_SOLVE)
+        line_transform<N1, N2, TK, false>(buf, scr, N, tw);
+    else
+        line_transform<N1, N2, TK, true>(buf, scr, N, tw);
+    if constexpr (MODE == COL_SOLVE) {
+        const double *s0 = g.sym;
+        const double *slast = g.sym + (int64_t)(g.dim - 1) * g.n;
+        const double s1 = g.sym[g.n + sc.outer_off + outer];
+        for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
+            const int kl = w / TK, c = w - kl * TK;
+            double gsq = s0[kl];
+            gsq = gsq + s1;
+            gsq = gsq + slast[min(k0 + c, g.n - 1)];
+            const double inv = (gsq > g.thresh) ? 1.0 / gsq : 0.0;
+            buf[kl * LD + c] = cscale(buf[kl * LD + c], -inv * g.scale);
+        }
+        __syncthreads();
+        line_transform<N1, N2, TK, true>(buf, scr, N, tw);
+    }
+    for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
+        const int n = w / TK, c = w - n * TK;
+        if (k0 + c < g.ncol) db[(n / sc.blk_d) * sc.d_sq + (n % sc.blk_d) * sc.d_es + c] = buf[n * LD + c];
+    }
+}
+
+// gradient + multiplier ascent on a slab; axis-0 neighbours across the slab
+// faces come from the u halo planes.  Writes G and lam (explicit grad_u).
+// slots: 0 sum dG^2, 1 sum misfit^2, 2.. sum lam
+__global__ void __launch_bounds__(256)
+k_grad_slab(const double *__restrict__ Ut, const double *__restrict__ hlo,
+            const double *__restrict__ hhi, double *__restrict__ G, const double *__restrict__ F,
+            double *__restrict__ Lam, int n, int nl, int64_t M, double inv2h, double rho, Mean9 um,
+            int update, double *partials, double *red_out, unsigned int *count) {
+    constexpr int K = 11;
+    __shared__ double smem[32 * K];
+    double acc[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) acc[q] = 0.0;
+    const int64_t nn = (int64_t)n * n;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int i0 = (int)(p / nn);
+        const int64_t q = p - i0 * nn;
+        const int i1 = (int)(q / n), i2 = (int)(q - (int64_t)i1 * n);
+        const int op1 = (i1 + 1 == n) ? -(n - 1) * n : n, om1 = (i1 == 0) ? (n - 1) * n : -n;
+        const int op2 = (i2 + 1 == n) ? -(n - 1) : 1, om2 = (i2 == 0) ? (n - 1) : -1;
+        double up[9], dn[9];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const double *u = Ut + (int64_t)i * M + p;
+            up[i * 3 + 0] = (i0 + 1 == nl) ? hhi[i * nn + q] : u[nn];
+            dn[i * 3 + 0] = (i0 == 0) ? hlo[i * nn + q] : u[-nn];
+            up[i * 3 + 1] = u[op1];
+            dn[i * 3 + 1] = u[om1];
+            up[i * 3 + 2] = u[op2];
+            dn[i * 3 + 2] = u[om2];
+        }
+        double gold[9], fv[9], lv[9];
+        if (update) {
+#pragma unroll
+            for (int c = 0; c < 9; ++c) {
+                const int64_t o = (int64_t)c * M + p;
+                gold[c] = G[o];
+                fv[c] = F[o];
+                lv[c] = Lam[o];
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 9; ++c) {
+            const double gnew = (up[c] - dn[c]) * inv2h + um.v[c];
+            const int64_t o = (int64_t)c * M + p;
+            if (update) {
+                const double dg = gnew - gold[c];
+                const double mis = gnew - fv[c];
+                const double lnew = lv[c] + rho * mis;
+                Lam[o] = lnew;
+                acc[0] += dg * dg;
+                acc[1] += mis * mis;
+                acc[2 + c] += lnew;
+            }
+            G[o] = gnew;
+        }
+    }
+    if (update) {
+        int ops[K];
+#pragma unroll
+        for (int q = 0; q < K; ++q) ops[q] = RED_SUM;
+        block_reduce<K>(acc, ops, smem);
+        grid_finalize<K>(acc, ops, partials, red_out, count, smem);
+    }
+}
+
+template <int MODE>
+int run_col_slab(mm_ctx *ctx, const ColGeom &g, const SlabCol &sc, int n_outer) {
+    int N1, N2;
+    factor(g.N, N1, N2);
+    auto go = [&](auto kern, int threads, size_t smem) -> int {
+        int rc = launch_smem(ctx, kern, dim3(1), threads, smem);
+        if (rc) return rc;
+        dim3 grid((unsigned)((g.ncol + 7) / 8), (unsigned)n_outer, 3u);
+        kern<<<grid, threads, smem, ctx->stream>>>(g, sc, ctx->tw_full);
+        MM_LAUNCH_CHECK(ctx);
+        return MM_OK;
+    };
+    switch (N1 * 100 + N2) {
+#define CASE(a, b)                                                                          \
+    case a * 100 + b:                                                                       \
+        return go(k_col_slab<a, b, MODE>, ColCfg<a, b>::NT,                                 \
+                  sizeof(double2) * (size_t)g.N * 9);
+        CASE(2, 1) CASE(4, 1) CASE(8, 1) CASE(4, 4) CASE(8, 4) CASE(8, 8) CASE(16, 8)
+        CASE(16, 16) CASE(32, 16) CASE(32, 32)
+#undef CASE
+        default:
+            return go(k_col_slab<0, 0, MODE>, 256, sizeof(double2) * (size_t)g.N * 9 * 2);
+    }
+}
+
+}  // namespace
+
+int mm_run_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, double *sums) {
+    int rc = ensure_constants(ctx);
+    if (rc) return rc;
+    const int n = ctx->n, nl = ctx->slab_nl, P = ctx->slab_P;
+    const int64_t M = ctx->M, nn = (int64_t)n * n;
+    const int Pp = ctx->P;  // spectral pitch
+    const int threads = 256;
+    ColGeom g;
+    g.N = n;
+    g.ncol = ctx->nh;
+    g.n = n;
+    g.dim = 3;
+    g.sym = ctx->sym;
+    g.thresh = ctx->sym_thresh;
+    g.scale = 1.0 / (2.0 * ctx->h) / ((double)n * n * n);
+    g.es = g.os = g.cs = 0;
+    // layouts: spec [c][i0l][i1][k2]; send/recv [q][c][i0l][i1l][k2]
+    const int64_t spec_cs = (int64_t)nl * n * Pp, spec_os = (int64_t)n * Pp;
+    const int64_t blk = 3LL * nl * nl * Pp;  // one destination block
+    switch (step) {
+        case MM_SLAB_HALO_T:
+        case MM_SLAB_HALO_U: {
+            StageScope ss(ctx, MM_STAGE_OTHER);
+            const bool T = step == MM_SLAB_HALO_T;
+            const int blocks = (int)std::min<int64_t>((3 * nn + threads - 1) / threads, 148 * 8);
+            k_slab_halo<<<blocks, threads, 0, ctx->stream>>>(
+                T ? ctx->F : ctx->Ut, T ? ctx->Lam : nullptr, 1.0 / rho, T ? 3 : 1, 3, n, nl, M,
+                ctx->halo_out_lo, ctx->halo_out_hi);
+            MM_LAUNCH_CHECK(ctx);
+            return mm_synchronize(ctx);
+        }
+        case MM_SLAB_FWD: {
+            {
+                StageScope ss(ctx, MM_STAGE_ROW_FWD);
+                if ((rc = run_rows(ctx, true, rho))) return rc;
+            }
+            SlabCol sc;
+            sc.src = ctx->spec;
+            sc.dst = ctx->sendbuf;
+            sc.blk_s = n;
+            sc.s_sq = 0; sc.s_es = Pp; sc.s_os = spec_os; sc.s_cs = spec_cs;
+            sc.blk_d = nl;  // i1 = q * nl + i1l
+            sc.d_sq = blk; sc.d_es = Pp; sc.d_os = (int64_t)nl * Pp; sc.d_cs = (int64_t)nl * nl * Pp;
+            sc.outer_off = 0;
+            StageScope ss(ctx, MM_STAGE_COL_FWD);
+            if ((rc = run_col_slab<COL_FWD>(ctx, g, sc, nl))) return rc;
+            return mm_synchronize(ctx);
+        }
+        case MM_SLAB_SOLVE: {
+            // recv [s][c][i0l][i1l][k2]: line along i0 = s * nl + i0l, outer = i1l
+            SlabCol sc;
+            sc.src = ctx->recvbuf;
+            sc.dst = ctx->recvbuf;
+            sc.blk_s = sc.blk_d = nl;
+            sc.s_sq = sc.d_sq = blk;
+            sc.s_es = sc.d_es = (int64_t)nl * Pp;
+            sc.s_os = sc.d_os = Pp;
+            sc.s_cs = sc.d_cs = (int64_t)nl * nl * Pp;
+            sc.outer_off = ctx->slab_rank * nl;
+            StageScope ss(ctx, MM_STAGE_COL_SOLVE);
+            if ((rc = run_col_slab<COL_SOLVE>(ctx, g, sc, nl))) return rc;
+            return mm_synchronize(ctx);
+        }
+        case MM_SLAB_INV: {
+            SlabCol sc;
+            sc.src = ctx->sendbuf;
+            sc.dst = ctx->spec;
+            sc.blk_s = nl;
+            sc.s_sq = blk; sc.s_es = Pp; sc.s_os = (int64_t)nl * Pp; sc.s_cs = (int64_t)nl * nl * Pp;
+            sc.blk_d = n;
+            sc.d_sq = 0; sc.d_es = Pp; sc.d_os = spec_os; sc.d_cs = spec_cs;
+            sc.outer_off = 0;
+            {
+                StageScope ss(ctx, MM_STAGE_COL_INV);
+                if ((rc = run_col_slab<COL_INV>(ctx, g, sc, nl))) return rc;
+            }
+            StageScope ss(ctx, MM_STAGE_ROW_INV);
+            if ((rc = run_rows(ctx, false, rho, ctx->Ut))) return rc;
+            return mm_synchronize(ctx);
+        }
+        case MM_SLAB_UPDATE:
+        case MM_SLAB_GRAD: {
+            Mean9 um;
+            for (int i = 0; i < 9; ++i) um.v[i] = u_mean[i];
+            const int blocks = (int)std::min<int64_t>((M + threads - 1) / threads, 148 * 8);
+            if ((rc = mm_ensure_partials(ctx, blocks))) return rc;
+            const int upd = step == MM_SLAB_UPDATE;
+            {
+                StageScope ss(ctx, MM_STAGE_GRAD);
+                k_grad_slab<<<blocks, threads, 0, ctx->stream>>>(
+                    ctx->Ut, ctx->halo_in_lo, ctx->halo_in_hi, ctx->G, ctx->F, ctx->Lam, n, nl, M,
+                    1.0 / (2.0 * ctx->h), rho, um, upd, ctx->partials, ctx->red_out,
+                    ctx->red_count);
+            }
+            MM_LAUNCH_CHECK(ctx);
+            ctx->g_implicit = false;
+            ctx->g_buf_valid = true;
+            for (int i = 0; i < 9; ++i) ctx->ubar[i] = um.v[i];
+            if (!upd) return mm_synchronize(ctx);
+            double r[MM_MAX_PARTIALS];
+            if ((rc = mm_fetch_reduction(ctx, 11, r))) return rc;
+            for (int i = 0; i < 11; ++i) sums[i] = r[i];
+            return MM_OK;
+        }
+        default: return mm_fail(ctx, MM_ERR_PARAM, "unknown slab step %d", step);
+    }
+    (void)P;
 }
