@@ -34,6 +34,20 @@ sys.path.insert(0, ROOT)
 
 B_ALG_MR3 = 952.0  # algorithmic bytes per voxel-iteration, 3D MR
 WORD = 8.0
+# FP64 operations (FMA = 2) of one accepted Armijo sweep of the 3D MR descent
+# (trial point, det, objective, cofactor gradient, |g|^2)
+F_SWEEP_MR3 = 170.0
+
+
+def fp64_peak_tflops():
+    """Nominal FP64 (non-tensor) peak: 148 SMs x 64 DFMA/clk x 2 x max SM clock."""
+    mhz = 1965.0
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f).get("sm_max_mhz", mhz))
+    except Exception:
+        pass
+    return 148 * 64 * 2 * mhz * 1e6 / 1e12
 
 
 def laminate(n, dim=3):
@@ -181,6 +195,7 @@ def run_ours(args, rank, world, dist):
     torch.cuda.synchronize()
     w0 = time.perf_counter()
     it0 = st.outer_iter
+    ps0 = eng.point_sweeps
     params = mm.SolverParams(r_p_tol=1e-300, r_d_tol=1e-300, max_outer=args.steps)
     mm.solve(grid, model, bc, params, policy=pol, state=st, raise_on_max=False)
     hist = st.history[-args.steps:]
@@ -198,6 +213,7 @@ def run_ours(args, rank, world, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     sweeps = st.total_sweeps
+    point_sweeps = eng.point_sweeps - ps0
 
     # ---- e2e through the public API with host buffers: solve() on a host
     # state (fresh engine: H2D of F, grad_u, lam, moduli), K iterations, then
@@ -264,6 +280,16 @@ def run_ours(args, rank, world, dist):
     roof_it = {"bound": "hbm", "B_alg_per_voxel": B_ALG_MR3,
                "achieved": round(B_ALG_MR3 * M / (it_ms / 1e3) / 1e9, 1), "peak": peak,
                "unit": "GB/s", "frac": round(B_ALG_MR3 * M / (it_ms / 1e3) / 1e9 / peak, 4)}
+    local_ms = sum(stage_ms.get(k, 0.0) for k in ("local", "fused"))
+    local_fp64 = None
+    if local_ms > 0 and point_sweeps > 0:
+        tf = point_sweeps * F_SWEEP_MR3 / (local_ms / 1e3) / 1e12
+        pk = fp64_peak_tflops()
+        local_fp64 = {"bound": "fp64", "stages": ["local", "fused"],
+                      "point_sweeps_per_voxel_iter": round(point_sweeps / (M * args.steps), 3),
+                      "flop_per_sweep": F_SWEEP_MR3, "achieved": round(tf, 2), "peak": round(pk, 1),
+                      "unit": "TFLOP/s", "frac": round(tf / pk, 4),
+                      "peak_source": "nominal 148 SM x 64 DFMA/clk x 2 x sm_max_mhz"}
     line = {
         "metric": "voxel-ADMM-iterations/sec (fp64)",
         "value": value,
@@ -291,6 +317,7 @@ def run_ours(args, rank, world, dist):
         "stages": per_stage,
         "roofline": roof,
         "roofline_iteration": roof_it,
+        "roofline_local_fp64": local_fp64,
         "gpu_launches": int(sum(stage_launch.values())),
         "clocks": clocks,
         "e2e": {"value": e2e_value, "unit": "voxel-iter/s", "h2d_bytes_per_step": h2d / args.steps,

@@ -81,6 +81,7 @@ typedef struct {
     int64_t n_conv;       /* points counted as converged (converged_frac * npts) */
     double sum_res2;      /* sum of res_pts^2 (solver.py:266 r_l numerator) */
     double sum_F[9];
+    double sum_nsw;       /* sum over points of the sweeps each took (work measure) */
 } mm_local_stats;
 
 /* Solver tail: projection + r_d + multiplier ascent + r_p (solver.py:268-279). */

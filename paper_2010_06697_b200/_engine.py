@@ -39,6 +39,7 @@ class Engine:
         self.model = None          # model whose parameters are on the device
         self.model_version = None
         self.lam_sum = None        # device-side sum of lam (None: recompute)
+        self.point_sweeps = 0.0    # local sweeps summed over points (work counter)
 
     def matches(self, grid: Grid) -> bool:
         return self.grid == grid

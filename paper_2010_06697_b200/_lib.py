@@ -52,7 +52,8 @@ STAGES = ("local", "row_fwd", "col_fwd", "col_solve", "col_inv", "row_inv", "gra
 
 class LocalStatsC(ctypes.Structure):
     _fields_ = [("sweeps", ctypes.c_int64), ("n_conv", ctypes.c_int64),
-                ("sum_res2", ctypes.c_double), ("sum_F", ctypes.c_double * 9)]
+                ("sum_res2", ctypes.c_double), ("sum_F", ctypes.c_double * 9),
+                ("sum_nsw", ctypes.c_double)]
 
 
 class UpdateStatsC(ctypes.Structure):

@@ -140,8 +140,8 @@ k_lce2d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
         const double *__restrict__ Fk, const double *__restrict__ angk, int64_t M, LcePar P,
         double *__restrict__ res_out, int32_t *__restrict__ nsw_out, uint8_t *__restrict__ ok_out,
         double *partials, double *red_out, unsigned int *count) {
-    __shared__ double smem[32 * 7];
-    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    __shared__ double smem[32 * 8];
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const double q = P.q, mur = P.mur, mual = P.mual, rho = P.rho, gam = P.gam;
     const double visF = P.visF, visn = P.visn;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
@@ -318,10 +318,11 @@ k_lce2d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
         acc[2] = fmax(acc[2], (double)nsw);
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[3 + i] += f[i];
+        acc[7] += (double)nsw;
     }
-    const int ops[7] = {RED_SUM, RED_SUM, RED_MAX, RED_SUM, RED_SUM, RED_SUM, RED_SUM};
-    block_reduce<7>(acc, ops, smem);
-    grid_finalize<7>(acc, ops, partials, red_out, count, smem);
+    const int ops[8] = {RED_SUM, RED_SUM, RED_MAX, RED_SUM, RED_SUM, RED_SUM, RED_SUM, RED_SUM};
+    block_reduce<8>(acc, ops, smem);
+    grid_finalize<8>(acc, ops, partials, red_out, count, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -443,12 +444,12 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
         int32_t *__restrict__ nsw_out, uint8_t *__restrict__ ok_out, double *partials,
         double *red_out, unsigned int *count) {
     extern __shared__ double smA[];  // 132 * LCE3_THREADS
-    __shared__ double smem[32 * 12];
+    __shared__ double smem[32 * 13];
     double *S = smA + threadIdx.x;
     constexpr int T = LCE3_THREADS;
-    double acc[12];
+    double acc[13];
 #pragma unroll
-    for (int k = 0; k < 12; ++k) acc[k] = 0.0;
+    for (int k = 0; k < 13; ++k) acc[k] = 0.0;
     const double q = P.q, mur = P.mur, mual = P.mual, rho = P.rho, gam = P.gam;
     const double visF = P.visF, visn = P.visn;
     const double PI = 3.141592653589793;
@@ -786,13 +787,14 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
         acc[2] = fmax(acc[2], (double)nsw);
 #pragma unroll
         for (int i = 0; i < 9; ++i) acc[3 + i] += Fl[i];
+        acc[12] += (double)nsw;
     }
-    int ops[12];
+    int ops[13];
 #pragma unroll
-    for (int k = 0; k < 12; ++k) ops[k] = RED_SUM;
+    for (int k = 0; k < 13; ++k) ops[k] = RED_SUM;
     ops[2] = RED_MAX;
-    block_reduce<12>(acc, ops, smem);
-    grid_finalize<12>(acc, ops, partials, red_out, count, smem);
+    block_reduce<13>(acc, ops, smem);
+    grid_finalize<13>(acc, ops, partials, red_out, count, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -880,7 +882,7 @@ int mm_run_lce(mm_ctx *ctx, double rho, double tol, int64_t max_sweeps, int want
     LcePar P = make_par(ctx->lce, rho, tol, max_sweeps);
     const double *Fk = viscous ? ctx->prevF : nullptr;
     const double *angk = viscous ? ctx->prevAng : nullptr;
-    const int K = 3 + ctx->D;
+    const int K = 4 + ctx->D;  // + sum of per-point sweeps
     if (d == 2) {
         const int threads = 128;
         const int blocks = lce_blocks(M, threads);
@@ -914,6 +916,7 @@ int mm_run_lce(mm_ctx *ctx, double rho, double tol, int64_t max_sweeps, int want
     out->n_conv = (int64_t)r[1];
     out->sweeps = M ? (int64_t)r[2] : 0;
     for (int i = 0; i < ctx->D; ++i) out->sum_F[i] = r[3 + i];
+    out->sum_nsw = r[K - 1];
     return MM_OK;
 }
 

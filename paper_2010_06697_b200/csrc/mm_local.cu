@@ -138,8 +138,8 @@ k_mr2d(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
        const double *__restrict__ mu, const double *__restrict__ kap, int64_t M, double rho,
        double tol, int64_t max_sweeps, double phi_scale, double *__restrict__ res_out,
        int32_t *__restrict__ nsw_out, double *partials, double *red_out, unsigned int *count) {
-    __shared__ double smem[32 * 7];
-    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    __shared__ double smem[32 * 8];
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
          p += (int64_t)gridDim.x * blockDim.x) {
         double a = F[p], b = F[M + p], c = F[2 * M + p], d = F[3 * M + p];
@@ -158,10 +158,11 @@ k_mr2d(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
         acc[1] += (res < tol) ? 1.0 : 0.0;
         acc[2] = fmax(acc[2], (double)nsw);
         acc[3] += a; acc[4] += b; acc[5] += c; acc[6] += d;
+        acc[7] += (double)nsw;
     }
-    const int ops[7] = {RED_SUM, RED_SUM, RED_MAX, RED_SUM, RED_SUM, RED_SUM, RED_SUM};
-    block_reduce<7>(acc, ops, smem);
-    grid_finalize<7>(acc, ops, partials, red_out, count, smem);
+    const int ops[8] = {RED_SUM, RED_SUM, RED_MAX, RED_SUM, RED_SUM, RED_SUM, RED_SUM, RED_SUM};
+    block_reduce<8>(acc, ops, smem);
+    grid_finalize<8>(acc, ops, partials, red_out, count, smem);
 }
 
 // Per-thread batch accumulators kept in shared memory ([slot][thread]) so
@@ -266,9 +267,11 @@ __device__ __forceinline__ void gradient(const double (&X)[D], const double (&B)
         double C[D];
         cof_t<D>(X, C);
         const double iJ = 1.0 / J;
-        const double c2 = k * (J * J - J) - m;  // coefficient of F^{-T}
+        // S + rho X - B with S = m (X - F^{-T}) + k (J^2 - J) F^{-T}, F^{-T} = C / J
+        const double cf = (k * (J * J - J) - m) * iJ;
+        const double mr = m + rho;
 #pragma unroll
-        for (int i = 0; i < D; ++i) g[i] = (m + rho) * X[i] + c2 * (C[i] * iJ) - B[i];
+        for (int i = 0; i < D; ++i) g[i] = fma(mr, X[i], fma(cf, C[i], -B[i]));
     }
 }
 
@@ -283,9 +286,10 @@ __device__ __forceinline__ void gradient_J(const double (&X)[D], double J, const
         double C[D];
         cof_t<D>(X, C);
         const double iJ = 1.0 / J;
-        const double c2 = k * (J * J - J) - m;
+        const double cf = (k * (J * J - J) - m) * iJ;
+        const double mr = m + rho;
 #pragma unroll
-        for (int i = 0; i < D; ++i) g[i] = (m + rho) * X[i] + c2 * (C[i] * iJ) - B[i];
+        for (int i = 0; i < D; ++i) g[i] = fma(mr, X[i], fma(cf, C[i], -B[i]));
     }
 }
 
@@ -414,7 +418,7 @@ k_descent(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
           double rho, double tol, double phi_scale, int s0, int s1, double *__restrict__ tstate,
           uint8_t *__restrict__ freestate, double *__restrict__ res_out,
           int32_t *__restrict__ nsw_io, double *partials, double *red_out, unsigned int *count) {
-    constexpr int K = 4 + D;
+    constexpr int K = 5 + D;  // ..., last slot: sum of per-point sweeps
     __shared__ double smem[32 * K];
     __shared__ double sacc[K * LOCAL_THREADS];
     SmemAcc<K> A;
@@ -440,10 +444,12 @@ k_descent(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
         double t = t0;
         bool freem = false;
         int nsw = 0;
+        int nsw_start = 0;
         if (s0 > 0) {
             t = tstate[p];
             freem = freestate[p] != 0;
             nsw = nsw_io[p];
+            nsw_start = nsw;
         }
         double res = 0.0;
         bool moved = false;
@@ -465,6 +471,7 @@ k_descent(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
         A.add(3, (res > tol) ? res : 0.0);
 #pragma unroll
         for (int i = 0; i < D; ++i) A.add(4 + i, X[i]);
+        A.add(K - 1, (double)(nsw - (s0 > 0 ? nsw_start : 0)));
     }
     double acc[K];
     A.load(acc);
@@ -499,7 +506,7 @@ k_update_local(double *__restrict__ F, double *__restrict__ Lam, double *__restr
                double rho_k, double rho, double tol, double phi_scale, int chunk,
                double *__restrict__ res_out, int32_t *__restrict__ nsw_out, double *partials,
                double *red_out, unsigned int *count) {
-    constexpr int K = 4 + 2 * D;
+    constexpr int K = 5 + 2 * D;  // ..., last slot: sum of per-point sweeps
     __shared__ double smem[32 * K];
     __shared__ double sacc[K * LOCAL_THREADS];
     SmemAcc<K> A;
@@ -564,6 +571,7 @@ k_update_local(double *__restrict__ F, double *__restrict__ Lam, double *__restr
             A.add(3, (res > tol) ? res : 0.0);
 #pragma unroll
             for (int i = 0; i < D; ++i) A.add(4 + i, X[i]);
+            A.add(K - 1, (double)nsw);
         }
     }
     double acc[K];
@@ -727,7 +735,8 @@ int mm_run_local(mm_ctx *ctx, int material, double rho, double tol, int64_t max_
         }
         MM_LAUNCH_CHECK(ctx);
         double r[7];
-        if ((rc = mm_fetch_reduction(ctx, 7, r))) return rc;
+        if ((rc = mm_fetch_reduction(ctx, 8, r))) return rc;
+        out->sum_nsw = r[7];
         out->sum_res2 = r[0];
         out->n_conv = (int64_t)r[1];
         out->sweeps = ctx->M ? (int64_t)r[2] : 0;
@@ -743,7 +752,8 @@ int mm_run_local(mm_ctx *ctx, int material, double rho, double tol, int64_t max_
         if (bad) return mm_fail(ctx, MM_ERR_INADMISSIBLE, "det F <= 0 at %d point(s)", bad);
         ctx->F_checked = true;
     }
-    const int K = 4 + D;
+    const int K = 5 + D;
+    double sum_nsw = 0.0;
     double r[MM_MAX_PARTIALS];
     const bool segmented = max_sweeps > 64;
     if (segmented) {
@@ -760,6 +770,7 @@ int mm_run_local(mm_ctx *ctx, int material, double rho, double tol, int64_t max_
         if (rc) return rc;
         if ((rc = mm_fetch_reduction(ctx, K, r))) return rc;
         sweeps = (int64_t)r[2];
+        sum_nsw = r[K - 1];
     } else {
         double ref = INFINITY;
         while (sweeps < max_sweeps) {
@@ -768,6 +779,7 @@ int mm_run_local(mm_ctx *ctx, int material, double rho, double tol, int64_t max_
                                     want_points);
             if (rc) return rc;
             if ((rc = mm_fetch_reduction(ctx, K, r))) return rc;
+            sum_nsw += r[K - 1];
             const int64_t mx = (int64_t)r[2];
             if (mx < s1) {  // every point stopped before s1
                 sweeps = mx;
@@ -785,6 +797,7 @@ int mm_run_local(mm_ctx *ctx, int material, double rho, double tol, int64_t max_
     out->n_conv = (int64_t)r[1];
     out->sweeps = ctx->M ? sweeps : 0;
     for (int i = 0; i < D; ++i) out->sum_F[i] = r[4 + i];
+    out->sum_nsw = sum_nsw;
     if (want_points) MM_CUDA(ctx, cudaMemsetAsync(ctx->ok, 0, ctx->M, ctx->stream));
     return MM_OK;
 }
@@ -845,7 +858,7 @@ int mm_run_update(mm_ctx *ctx, int material, double rho_next, double tol, int64_
         ctx->g_buf_valid = true;
     }
     double r[MM_MAX_PARTIALS];
-    const int K = 4 + 2 * D;
+    const int K = 5 + 2 * D;
     if ((rc = mm_fetch_reduction(ctx, K, r))) return rc;
     for (int i = 0; i < 9; ++i) us->sum_lam[i] = i < D ? r[4 + D + i] : 0.0;
     if (sweep) {
@@ -853,6 +866,7 @@ int mm_run_update(mm_ctx *ctx, int material, double rho_next, double tol, int64_
         ls->n_conv = (int64_t)r[1];
         ls->sweeps = ctx->M ? (int64_t)r[2] : 0;
         for (int i = 0; i < 9; ++i) ls->sum_F[i] = i < D ? r[4 + i] : 0.0;
+        ls->sum_nsw = r[K - 1];
         if (want_points) MM_CUDA(ctx, cudaMemsetAsync(ctx->ok, 0, ctx->M, ctx->stream));
     }
     return MM_OK;

@@ -42,12 +42,13 @@ class DeviceLocalStats(LocalStats):
     the batch kept per-point residuals (custom policies); the solver needs
     only the reductions (sum res^2 for r_l, the converged count, max sweeps)."""
 
-    def __init__(self, res_pts, sweeps, converged_frac, sum_res2, sum_F):
+    def __init__(self, res_pts, sweeps, converged_frac, sum_res2, sum_F, sum_nsw=0.0):
         self._res = res_pts
         self.sweeps = int(sweeps)
         self.converged_frac = float(converged_frac)
         self.sum_res2 = float(sum_res2)
         self.sum_F = np.asarray(sum_F, dtype=float)
+        self.sum_nsw = float(sum_nsw)  # sweeps summed over points (work done)
 
     @property
     def res_pts(self):

@@ -242,7 +242,7 @@ class LiquidCrystalElastomer(MaterialModel):
         if want_points:
             res, _, _ = ctx.download_points()
         frac = float(st.n_conv) / npts if npts else 1.0
-        return DeviceLocalStats(res, st.sweeps, frac, st.sum_res2, list(st.sum_F))
+        return DeviceLocalStats(res, st.sweeps, frac, st.sum_res2, list(st.sum_F), st.sum_nsw)
 
     def frank_force(self, grid, n_field) -> np.ndarray:
         """2 kappa (D^T D) n (lce.py:213-221) as the radius-2 stencil, on the device."""

@@ -106,7 +106,7 @@ class MooneyRivlin(MaterialModel):
         if want_points:
             res, _, _ = ctx.download_points()
         frac = float(st.n_conv) / npts if npts else 1.0
-        return DeviceLocalStats(res, st.sweeps, frac, st.sum_res2, list(st.sum_F))
+        return DeviceLocalStats(res, st.sweeps, frac, st.sum_res2, list(st.sum_F), st.sum_nsw)
 
     def _run_points(self, F, grad_u, lam, rho, max_sweeps, point_tol, material, abs_tol=None):
         npts = F.shape[0]

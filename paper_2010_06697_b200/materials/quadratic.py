@@ -64,7 +64,7 @@ class QuadraticMaterial(MaterialModel):
         if want_points:
             res, _, _ = ctx.download_points()
         frac = float(st.n_conv) / npts if npts else 1.0
-        return DeviceLocalStats(res, st.sweeps, frac, st.sum_res2, list(st.sum_F))
+        return DeviceLocalStats(res, st.sweeps, frac, st.sum_res2, list(st.sum_F), st.sum_nsw)
 
     def local_sweeps(self, F, internal, grad_u, lam, rho, dt, prev_F, prev_internal, frozen,
                      max_sweeps, point_tol) -> LocalStats:

@@ -370,6 +370,7 @@ def outer_iteration(grid: Grid, model, state: ADMMState, params: SolverParams, b
         chunk = min(policy.chunk, params.max_local - sweeps_total)
         stats = model._device_local(ctx, npts, state.rho, dt, chunk, tol_pt, want_points)
         sweeps_total += stats.sweeps
+        eng.point_sweeps += stats.sum_nsw
         if (policy.is_done(stats, sweeps_total) or stats.sweeps < chunk
                 or sweeps_total >= params.max_local):
             break
@@ -490,6 +491,7 @@ def _solve_fused(grid, model, bc, params, policy, state, r_l_tol):
             else:
                 stats = model._device_local(ctx, npts, state.rho, 0.0, chunk, tol_pt, False)
             sweeps_total += stats.sweeps
+            eng.point_sweeps += stats.sum_nsw
             if (policy.is_done(stats, sweeps_total) or stats.sweeps < chunk
                     or sweeps_total >= params.max_local):
                 break
@@ -526,7 +528,7 @@ def _solve_fused(grid, model, bc, params, policy, state, r_l_tol):
             ls, us = ctx.update_and_sweep(mat, state.rho, tol_next * mu_rep, chunk, phi_scale)
             eng.lam_sum = np.array(us.sum_lam[: d * d])
             pending = DeviceLocalStats(None, ls.sweeps, float(ls.n_conv) / npts if npts else 1.0,
-                                       ls.sum_res2, list(ls.sum_F))
+                                       ls.sum_res2, list(ls.sum_F), ls.sum_nsw)
         wall_ms = (time.perf_counter() - t_start) * 1e3
         resid = Residuals(state.outer_iter, float(r_p), float(r_d), float(r_l), float(state.rho),
                           wall_ms)
