@@ -17,8 +17,8 @@ import sys
 from collections import defaultdict
 
 STAGE_OF = [("k_descent", "local"), ("k_mr2d", "local"), ("k_lce", "local"),
-            ("k_row_fwd", "row_fwd"), ("k_row_inv", "row_inv"), ("k_grad", "grad"),
-            ("k_col<", None)]
+            ("k_update_local", "fused"), ("k_row_fwd", "row_fwd"), ("k_row_inv", "row_inv"),
+            ("k_grad", "grad"), ("k_colp<", None), ("k_col<", None)]
 METRICS = {
     "gpu__time_duration.sum": "duration",
     "dram__bytes_read.sum": "dram_read",
@@ -39,7 +39,8 @@ def stage_of(name, col_idx):
         if key in name:
             if st is None:
                 # k_col<N1, N2, MODE>: MODE 0 fwd, 1 inv, 2 solve
-                mode = name.split("k_col<", 1)[1].split(">")[0].split(",")[-1].strip()
+                key_ = "k_colp<" if "k_colp<" in name else "k_col<"
+                mode = name.split(key_, 1)[1].split(">")[0].split(",")[-1].strip()
                 return {"0": "col_fwd", "1": "col_inv", "2": "col_solve"}.get(mode, "col")
             return st
     return "other"
