@@ -136,6 +136,11 @@ int64_t mm_device_bytes(const mm_ctx *ctx);
 /* Host AoS <-> device SoA.  count = number of doubles in the host array
  * (npts * ncomp of the field); a mismatch is MM_ERR_CONFIG. */
 int mm_upload(mm_ctx *ctx, int field, const double *host, int64_t count);
+/* field += host array (AoS, same count as mm_upload), rounded once per
+ * element like numpy's `state.F = state.F + dF`: the seeded perturbation
+ * of the load-stepping drivers (scenarios.py:801-805) without a round trip
+ * of the field.  field in {F, LAM, PREV_F}. */
+int mm_add_field(mm_ctx *ctx, int field, const double *host, int64_t count);
 int mm_download(mm_ctx *ctx, int field, double *host, int64_t count);
 /* Device-to-device copy of a whole field (e.g. begin_time_step, solver.py:230-233). */
 int mm_copy_field(mm_ctx *ctx, int dst_field, int src_field);
@@ -237,6 +242,15 @@ int mm_set_option(mm_ctx *ctx, int option, int64_t value);
  * op 0: grad_u = D u_tilde (discrete_grad);  op 1: u_tilde = div F
  * (discrete_div).  Both equal the reference's spectral forms to roundoff. */
 int mm_stencil(mm_ctx *ctx, int op);
+
+/* equilibrium_residual (solver.py:346-371): || div P ||_{H^-1} / npts of
+ * the total stress P(F, internal; dt) of `material` on the device state
+ * (MR / quadratic: mooney_rivlin.py:78-85, quadratic.py:34-36; LCE:
+ * lce.py:186-196 incl. reaction and viscous terms; the viscous coefficient
+ * is the vis_F = nu_F / dt of the last mm_set_lce, applied when dt > 0).
+ * MR with det F <= 0 returns MM_ERR_INADMISSIBLE like the reference's
+ * stress(). */
+int mm_equilibrium_residual(mm_ctx *ctx, int material, double dt, double *out);
 
 #ifdef __cplusplus
 }

@@ -39,7 +39,8 @@ EXPORTS = (
     "mm_prepare_frozen", "mm_project", "mm_project_update", "mm_stencil",
     "mm_profile_enable", "mm_profile_read", "mm_frank_stencil", "mm_set_option",
     "mm_project_residuals", "mm_update_multiplier", "mm_update_and_sweep",
-    "mm_create_slab", "mm_slab_buffer", "mm_slab_step",
+    "mm_create_slab", "mm_slab_buffer", "mm_slab_step", "mm_add_field",
+    "mm_equilibrium_residual",
 )
 
 SLAB_HALO_T, SLAB_FWD, SLAB_SOLVE, SLAB_INV, SLAB_HALO_U, SLAB_UPDATE, SLAB_GRAD = range(7)
@@ -121,6 +122,8 @@ def load_library():
             "mm_update_and_sweep": ([P, I, D, D, I64, D, I, ctypes.POINTER(LocalStatsC),
                                      ctypes.POINTER(UpdateStatsC)], I),
             "mm_profile_read": ([P, ctypes.POINTER(ProfileC), I], I),
+            "mm_add_field": ([P, I, P, I64], I),
+            "mm_equilibrium_residual": ([P, I, D, ctypes.POINTER(D)], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -206,6 +209,17 @@ class Context:
     def upload(self, field, arr):
         a = np.ascontiguousarray(arr, dtype=np.float64)
         self.check(self.lib.mm_upload(self.h, field, _ptr(a), a.size))
+
+    def add_field(self, field, arr):
+        """field += arr on the device (one rounding per element)."""
+        a = np.ascontiguousarray(arr, dtype=np.float64)
+        self.check(self.lib.mm_add_field(self.h, field, _ptr(a), a.size))
+
+    def equilibrium_residual(self, material, dt=0.0):
+        out = ctypes.c_double()
+        self.check(self.lib.mm_equilibrium_residual(self.h, int(material), float(dt),
+                                                    ctypes.byref(out)))
+        return out.value
 
     def download(self, field, shape):
         out = np.empty(shape, dtype=np.float64)

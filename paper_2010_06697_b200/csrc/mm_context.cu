@@ -104,6 +104,18 @@ __global__ void k_aos_to_soa(const double *__restrict__ src, double *__restrict_
     }
 }
 
+__global__ void k_aos_add_soa(const double *__restrict__ src, double *__restrict__ dst,
+                              int64_t p0, int64_t np, int ncomp, int64_t M) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t tot = np * ncomp;
+    for (; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t p = i / ncomp;
+        int c = (int)(i - p * ncomp);
+        const int64_t o = (int64_t)c * M + p0 + p;
+        dst[o] = __dadd_rn(dst[o], src[i]);  // numpy's F + dF, one rounding
+    }
+}
+
 __global__ void k_soa_to_aos(const double *__restrict__ src, double *__restrict__ dst,
                              int64_t p0, int64_t np, int ncomp, int64_t M) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -176,7 +188,8 @@ static bool is_pinned(const void *p) {
     return a.type == cudaMemoryTypeHost;
 }
 
-static int transfer(mm_ctx *ctx, double *dev, int ncomp, const double *hsrc, double *hdst) {
+static int transfer(mm_ctx *ctx, double *dev, int ncomp, const double *hsrc, double *hdst,
+                    bool add = false) {
     const int64_t M = ctx->M;
     const int64_t chunk_pts = std::max<int64_t>(1, std::min<int64_t>(M, (int64_t)(1 << 22)));
     int rc = ensure_stage(ctx, chunk_pts * ncomp);
@@ -196,7 +209,10 @@ static int transfer(mm_ctx *ctx, double *dev, int ncomp, const double *hsrc, dou
             }
             MM_CUDA(ctx, cudaMemcpyAsync(ctx->stage, src, bytes, cudaMemcpyHostToDevice,
                                          ctx->stream));
-            k_aos_to_soa<<<blocks, threads, 0, ctx->stream>>>(ctx->stage, dev, p0, np, ncomp, M);
+            if (add)
+                k_aos_add_soa<<<blocks, threads, 0, ctx->stream>>>(ctx->stage, dev, p0, np, ncomp, M);
+            else
+                k_aos_to_soa<<<blocks, threads, 0, ctx->stream>>>(ctx->stage, dev, p0, np, ncomp, M);
             MM_LAUNCH_CHECK(ctx);
             if (!pinned) MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
         } else {
@@ -434,7 +450,7 @@ void mm_destroy(mm_ctx *ctx) {
                       ctx->ang, ctx->chart, ctx->pinc, ctx->n0, ctx->ff, ctx->prevAng,
                       ctx->prevChart, ctx->prevPinc, ctx->dirbuf, ctx->Ut2, ctx->halo_in_lo,
                       ctx->halo_in_hi, ctx->halo_out_lo, ctx->halo_out_hi, ctx->sym, ctx->partials, ctx->red_out,
-                      ctx->res, ctx->tstate, ctx->stage};
+                      ctx->res, ctx->tstate, ctx->stage, ctx->Pbuf};
     for (double *p : ptrs)
         if (p) cudaFree(p);
     if (ctx->spec) cudaFree(ctx->spec);
@@ -513,6 +529,58 @@ int mm_upload(mm_ctx *ctx, int field, const double *host, int64_t count) {
         ctx->g_buf_valid = true;
     }
     return transfer(ctx, *slot, ncomp, host, nullptr);
+}
+
+int mm_add_field(mm_ctx *ctx, int field, const double *host, int64_t count) {
+    if (!ctx || !host) return MM_ERR_PARAM;
+    {
+        int prc = mm_flush_pending(ctx);
+        if (prc) return prc;
+    }
+    if (field != MM_FIELD_F && field != MM_FIELD_LAM && field != MM_FIELD_PREV_F)
+        return mm_fail(ctx, MM_ERR_PARAM, "mm_add_field: field %d is not F, LAM or PREV_F", field);
+    double **slot;
+    int ncomp;
+    int rc = field_info(ctx, field, &slot, &ncomp);
+    if (rc) return rc;
+    if (count != ctx->M * ncomp)
+        return mm_fail(ctx, MM_ERR_CONFIG, "field %d: got %lld doubles, expected %lld", field,
+                       (long long)count, (long long)(ctx->M * ncomp));
+    if (!*slot) return mm_fail(ctx, MM_ERR_CONFIG, "field %d was never set", field);
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    if (field == MM_FIELD_F) ctx->F_checked = false;
+    return transfer(ctx, *slot, ncomp, host, nullptr, true);
+}
+
+int mm_equilibrium_residual(mm_ctx *ctx, int material, double dt, double *out) {
+    if (!ctx || !out) return MM_ERR_PARAM;
+    if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
+    if (ctx->slab_mode)
+        return mm_fail(ctx, MM_ERR_CONFIG, "equilibrium_residual is single-context only");
+    {
+        int prc = mm_flush_pending(ctx);
+        if (prc) return prc;
+    }
+    if (!ctx->F) return mm_fail(ctx, MM_ERR_CONFIG, "F was never set");
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    int rc;
+    if (!ctx->Pbuf && (rc = mm_alloc(ctx, (void **)&ctx->Pbuf, sizeof(double) * ctx->D * ctx->M)))
+        return rc;
+    switch (material) {
+        case MM_MAT_MR:
+        case MM_MAT_MR_DESCENT: {
+            int bad = 0;  // MaterialModel._check_det (base.py:116-121) in stress()
+            if ((rc = mm_check_det(ctx, &bad))) return rc;
+            if (bad) return mm_fail(ctx, MM_ERR_INADMISSIBLE, "det F <= 0 at %d point(s)", bad);
+            rc = mm_run_stress(ctx, material, ctx->Pbuf);
+            break;
+        }
+        case MM_MAT_QUADRATIC: rc = mm_run_stress(ctx, material, ctx->Pbuf); break;
+        case MM_MAT_LCE: rc = mm_run_lce_stress(ctx, dt, ctx->Pbuf); break;
+        default: return mm_fail(ctx, MM_ERR_PARAM, "unknown material %d", material);
+    }
+    if (rc) return rc;
+    return mm_run_eq_residual(ctx, ctx->Pbuf, out);
 }
 
 int mm_download(mm_ctx *ctx, int field, double *host, int64_t count) {

@@ -81,6 +81,7 @@ struct mm_ctx {
     bool g_buf_valid = true;
     double ubar[9] = {0};
     double *Ut2 = nullptr;  // second u_tilde buffer (new u during a projection)
+    double *Pbuf = nullptr; // stress field scratch (equilibrium_residual)
     bool F_checked = false;
     bool points_only = false;
     // slab decomposition (3D, split along axis 0)
@@ -282,6 +283,9 @@ int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
                    mm_update_stats *out);
 int mm_run_frozen(mm_ctx *ctx);
 int mm_run_field_sums(mm_ctx *ctx, const double *field, int ncomp, double *out);
+int mm_run_stress(mm_ctx *ctx, int material, double *P);
+int mm_run_lce_stress(mm_ctx *ctx, double dt, double *P);
+int mm_run_eq_residual(mm_ctx *ctx, const double *P, double *out);
 int mm_check_det(mm_ctx *ctx, int *bad);
 int mm_run_stencil(mm_ctx *ctx, int op);
 int mm_run_frank_of_ff(mm_ctx *ctx);

@@ -856,6 +856,67 @@ __global__ void k_frank(const double *__restrict__ nf, double *__restrict__ ff, 
     }
 }
 
+// total mechanical stress (lce.py:166-174, 186-196) into P (SoA d*d):
+//   mu r1d (F - rr n (F^T n)) + mu alpha (n (F^T n) - c n n0)
+//   + (p_inc + gamma (J - 1)) cof F + (nu_F / dt) (F - F_k)
+template <int DIM>
+__global__ void __launch_bounds__(256)
+k_lce_stress(const double *__restrict__ F, const double *__restrict__ nf,
+             const double *__restrict__ n0, const double *__restrict__ pinc,
+             const double *__restrict__ Fk, double visc, double mu, double r1d, double rr,
+             double alpha, double gamma, double *__restrict__ P, int64_t M) {
+    constexpr int D = DIM * DIM;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        double X[D], n[DIM], m0[DIM], Ftn[DIM], C[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) X[i] = F[i * M + p];
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) {
+            n[i] = nf[i * M + p];
+            m0[i] = n0[i * M + p];
+        }
+        double c = 0.0;
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) {
+            double t = 0.0;
+#pragma unroll
+            for (int i = 0; i < DIM; ++i) t += X[i * DIM + j] * n[i];
+            Ftn[j] = t;
+            c += t * m0[j];
+        }
+        double J;
+        if constexpr (DIM == 2) {
+            J = X[0] * X[3] - X[1] * X[2];
+            C[0] = X[3]; C[1] = -X[2]; C[2] = -X[1]; C[3] = X[0];
+        } else {
+            C[0] = X[4] * X[8] - X[5] * X[7];
+            C[1] = X[5] * X[6] - X[3] * X[8];
+            C[2] = X[3] * X[7] - X[4] * X[6];
+            C[3] = X[2] * X[7] - X[1] * X[8];
+            C[4] = X[0] * X[8] - X[2] * X[6];
+            C[5] = X[1] * X[6] - X[0] * X[7];
+            C[6] = X[1] * X[5] - X[2] * X[4];
+            C[7] = X[2] * X[3] - X[0] * X[5];
+            C[8] = X[0] * X[4] - X[1] * X[3];
+            J = X[0] * C[0] + X[1] * C[1] + X[2] * C[2];
+        }
+        const double react = pinc[p] + gamma * (J - 1.0);
+        const double a = mu * r1d, b = mu * alpha;
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) {
+#pragma unroll
+            for (int j = 0; j < DIM; ++j) {
+                const int q = i * DIM + j;
+                const double nF = n[i] * Ftn[j];
+                double v = a * (X[q] - rr * nF) + b * (nF - c * (n[i] * m0[j])) + react * C[q];
+                if (Fk) v += visc * (X[q] - Fk[q * M + p]);
+                P[q * M + p] = v;
+            }
+        }
+    }
+}
+
 int lce_blocks(int64_t M, int threads) {
     return (int)std::min<int64_t>((M + threads - 1) / threads, 148 * 32);
 }
@@ -964,6 +1025,34 @@ int mm_run_frozen(mm_ctx *ctx) {
         return rc;
     if ((rc = run_director(ctx, ctx->dirbuf))) return rc;
     return run_frank(ctx, ctx->dirbuf);
+}
+
+int mm_run_lce_stress(mm_ctx *ctx, double dt, double *P) {
+    int rc;
+    const int64_t M = ctx->M;
+    const int d = ctx->dim;
+    if (!ctx->ang || !ctx->pinc || !ctx->n0 || (d == 3 && !ctx->chart))
+        return mm_fail(ctx, MM_ERR_CONFIG, "LCE state was never uploaded");
+    const bool visc = dt > 0.0 && ctx->lce.vis_F > 0.0;  // lce.py:194-195
+    if (visc && !ctx->prevF)
+        return mm_fail(ctx, MM_ERR_PARAM, "viscous stress needs prev_F");
+    if (!ctx->dirbuf && (rc = mm_alloc(ctx, (void **)&ctx->dirbuf, sizeof(double) * d * M)))
+        return rc;
+    StageScope ss(ctx, MM_STAGE_OTHER, 2);
+    if ((rc = run_director(ctx, ctx->dirbuf))) return rc;
+    const int threads = 256;
+    const int blocks = lce_blocks(M, threads);
+    const mm_lce_params &L = ctx->lce;
+    const double vis = visc ? ctx->lce.vis_F : 0.0;  // nu_F / dt, set by mm_set_lce
+    const double *Fk = visc ? ctx->prevF : nullptr;
+    if (d == 2)
+        k_lce_stress<2><<<blocks, threads, 0, ctx->stream>>>(ctx->F, ctx->dirbuf, ctx->n0,
+            ctx->pinc, Fk, vis, L.mu, L.r1d, L.rr, L.alpha, L.gamma_inc, P, M);
+    else
+        k_lce_stress<3><<<blocks, threads, 0, ctx->stream>>>(ctx->F, ctx->dirbuf, ctx->n0,
+            ctx->pinc, Fk, vis, L.mu, L.r1d, L.rr, L.alpha, L.gamma_inc, P, M);
+    MM_LAUNCH_CHECK(ctx);
+    return MM_OK;
 }
 
 // Frank force of a director field the caller placed in the FF slot

@@ -626,7 +626,56 @@ k_field_sums(const double *__restrict__ f, int64_t M, double *partials, double *
     grid_finalize<NC>(acc, ops, partials, red_out, count, smem);
 }
 
+// first Piola stress of the hyperelastic models into P (SoA), the input of
+// equilibrium_residual: Mooney-Rivlin mu (F - F^-T) + kappa (J^2 - J) F^-T
+// (mooney_rivlin.py:78-85), quadratic c F (quadratic.py:34-36)
+template <int MAT, int D>
+__global__ void __launch_bounds__(256)
+k_stress(const double *__restrict__ F, const double *__restrict__ modA,
+         const double *__restrict__ modB, double *__restrict__ P, int64_t M) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        double X[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) X[i] = F[i * M + p];
+        const double m = modA[p];
+        if constexpr (MAT == MAT_QUAD) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) P[i * M + p] = m * X[i];
+        } else {
+            const double k = modB[p];
+            const double J = det_t<D>(X);
+            double C[D];
+            cof_t<D>(X, C);
+            const double kj = k * (J * J - J);
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                const double finvt = C[i] / J;
+                P[i * M + p] = m * (X[i] - finvt) + kj * finvt;
+            }
+        }
+    }
+}
+
 }  // namespace
+
+int mm_run_stress(mm_ctx *ctx, int material, double *P) {
+    const int threads = 256;
+    const int blocks = (int)std::min<int64_t>((ctx->M + threads - 1) / threads, 148 * 16);
+    StageScope ss(ctx, MM_STAGE_OTHER);
+    const bool quad = material == MM_MAT_QUADRATIC;
+    const double *kap = quad ? ctx->modA : ctx->modB;
+    if (!ctx->modA || !kap) return mm_fail(ctx, MM_ERR_CONFIG, "material moduli were never set");
+    if (ctx->dim == 2) {
+        if (quad) k_stress<MAT_QUAD, 4><<<blocks, threads, 0, ctx->stream>>>(ctx->F, ctx->modA, kap, P, ctx->M);
+        else k_stress<MAT_MR, 4><<<blocks, threads, 0, ctx->stream>>>(ctx->F, ctx->modA, kap, P, ctx->M);
+    } else {
+        if (quad) k_stress<MAT_QUAD, 9><<<blocks, threads, 0, ctx->stream>>>(ctx->F, ctx->modA, kap, P, ctx->M);
+        else k_stress<MAT_MR, 9><<<blocks, threads, 0, ctx->stream>>>(ctx->F, ctx->modA, kap, P, ctx->M);
+    }
+    MM_LAUNCH_CHECK(ctx);
+    return MM_OK;
+}
 
 static int reduce_blocks(mm_ctx *ctx, int threads) {
     int64_t b = (ctx->M + threads - 1) / threads;

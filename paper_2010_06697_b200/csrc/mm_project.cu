@@ -461,13 +461,20 @@ struct ColGeom {
     int64_t es;        // element stride along the line (complex units)
     int64_t os;        // outer stride
     int64_t cs;        // component stride
-    // solve (MODE 2)
+    // solve (MODE 2) and norm (MODE 3)
     int n, dim;
     const double *sym;
     double thresh, scale;
+    // norm (MODE 3): deterministic block partials
+    double *partials, *red_out;
+    unsigned int *count;
 };
 
-enum { COL_FWD = 0, COL_INV = 1, COL_SOLVE = 2 };
+// COL_NORM: forward FFT along the line, then sum over the tile of
+// m(k2) |X|^2 / |g|^2 on live modes, m = 1 on the k2 = 0 and Nyquist columns
+// of the half spectrum and 2 elsewhere (the full-spectrum sum of a real
+// field's transform; equilibrium_residual, solver.py:364-371)
+enum { COL_FWD = 0, COL_INV = 1, COL_SOLVE = 2, COL_NORM = 3 };
 
 template <int N1, int N2>
 struct ColCfg {
@@ -517,10 +524,34 @@ k_col(double2 *__restrict__ spec, ColGeom g, const double2 *__restrict__ tw) {
         }
     }
     __syncthreads();
-    if constexpr (MODE == COL_FWD || MODE == COL_SOLVE)
+    if constexpr (MODE == COL_FWD || MODE == COL_SOLVE || MODE == COL_NORM)
         line_transform<N1, N2, TK, false>(buf, scr, N, tw);
     else
         line_transform<N1, N2, TK, true>(buf, scr, N, tw);
+    if constexpr (MODE == COL_NORM) {
+        __shared__ double red_sm[32];
+        const double *s0 = g.sym;
+        const double *slast = g.sym + (int64_t)(g.dim - 1) * g.n;
+        const double s1 = (g.dim == 3) ? g.sym[g.n + outer] : 0.0;
+        const int nyq = (g.n % 2 == 0) ? g.n / 2 : -1;
+        double acc[1] = {0.0};
+        for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
+            const int kl = w / TK, c = w - kl * TK;
+            const int k2 = k0 + c;
+            if (k2 >= g.ncol) continue;
+            double gsq = s0[kl];
+            if (g.dim == 3) gsq = gsq + s1;
+            gsq = gsq + slast[k2];
+            if (!(gsq > g.thresh)) continue;
+            const double2 X = buf[kl * LD + c];
+            const double m = (k2 == 0 || k2 == nyq) ? 1.0 : 2.0;
+            acc[0] += m * (X.x * X.x + X.y * X.y) / gsq;
+        }
+        const int ops[1] = {RED_SUM};
+        block_reduce<1>(acc, ops, red_sm);
+        grid_finalize<1>(acc, ops, g.partials, g.red_out, g.count, red_sm);
+        return;
+    }
     if constexpr (MODE == COL_SOLVE) {
         // u_hat = -d_hat / |g|^2 on live modes (projection.py:150-158); the
         // column is the last-axis frequency, `outer` the axis-1 one in 3D
@@ -818,7 +849,7 @@ int launch_smem(mm_ctx *ctx, Kern kern, dim3 grid, int threads, size_t smem) {
 
 template <int N1, int N2, int DIM, int ROWS>
 int run_rows_t(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double2 *tw_line,
-               double *u_out) {
+               double *u_out, const double *fsrc) {
     using C = RowCfg<N1, N2, DIM, ROWS>;
     const int threads = C::NT;
     const size_t smem = sizeof(double2) * (size_t)(g.N + 1) * (C::TK + 1) * (N1 ? 1 : 2);
@@ -827,8 +858,11 @@ int run_rows_t(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double
         auto kern = k_row_fwd<N1, N2, DIM, ROWS>;
         int rc = launch_smem(ctx, kern, grid, threads, smem);
         if (rc) return rc;
-        kern<<<grid, threads, smem, ctx->stream>>>(ctx->F, ctx->Lam, rho, ctx->spec, g, tw_line,
-                                                   ctx->tw_r2c);
+        // fsrc: divergence of that field alone (rho = inf: T = F - L * 0 = F exactly)
+        const double *Fs = fsrc ? fsrc : ctx->F;
+        const double *Ls = fsrc ? fsrc : ctx->Lam;
+        kern<<<grid, threads, smem, ctx->stream>>>(Fs, Ls, fsrc ? INFINITY : rho, ctx->spec, g,
+                                                   tw_line, ctx->tw_r2c);
     } else {
         auto kern = k_row_inv<N1, N2, DIM, ROWS>;
         int rc = launch_smem(ctx, kern, grid, threads, smem);
@@ -841,14 +875,15 @@ int run_rows_t(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double
 
 template <int N1, int N2>
 int run_rows_n(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double2 *tw,
-               double *u_out) {
+               double *u_out, const double *fsrc) {
     // 4 rows per tile (2 for 32-point register FFTs): <= 384 threads, 3-4 tiles per SM
     constexpr bool big = N1 >= 32;
-    if (g.dim == 2) return run_rows_t<N1, N2, 2, big ? 2 : 4>(ctx, fwd, rho, g, tw, u_out);
-    return run_rows_t<N1, N2, 3, big ? 2 : 4>(ctx, fwd, rho, g, tw, u_out);
+    if (g.dim == 2) return run_rows_t<N1, N2, 2, big ? 2 : 4>(ctx, fwd, rho, g, tw, u_out, fsrc);
+    return run_rows_t<N1, N2, 3, big ? 2 : 4>(ctx, fwd, rho, g, tw, u_out, fsrc);
 }
 
-int run_rows(mm_ctx *ctx, bool fwd, double rho, double *u_out = nullptr) {
+int run_rows(mm_ctx *ctx, bool fwd, double rho, double *u_out = nullptr,
+             const double *fsrc = nullptr) {
     RowGeom g;
     g.n = ctx->n;
     g.dim = ctx->dim;
@@ -865,11 +900,11 @@ int run_rows(mm_ctx *ctx, bool fwd, double rho, double *u_out = nullptr) {
     factor(g.N, N1, N2);
     switch (N1 * 100 + N2) {
 #define CASE(a, b) \
-    case a * 100 + b: return run_rows_n<a, b>(ctx, fwd, rho, g, tw, u_out);
+    case a * 100 + b: return run_rows_n<a, b>(ctx, fwd, rho, g, tw, u_out, fsrc);
         CASE(1, 1) CASE(2, 1) CASE(4, 1) CASE(8, 1) CASE(4, 4) CASE(8, 4) CASE(8, 8)
         CASE(16, 8) CASE(16, 16) CASE(32, 16) CASE(32, 32)
 #undef CASE
-        default: return run_rows_n<0, 0>(ctx, fwd, rho, g, tw, u_out);
+        default: return run_rows_n<0, 0>(ctx, fwd, rho, g, tw, u_out, fsrc);
     }
 }
 
@@ -877,7 +912,7 @@ template <int N1, int N2, int MODE>
 int run_col_t(mm_ctx *ctx, const ColGeom &g, int n_outer) {
     constexpr int TK = ColCfg<N1, N2>::TK;
     const int threads = ColCfg<N1, N2>::NT;
-    if constexpr (N1 * N2 >= 16 && MODE != COL_SOLVE) {
+    if constexpr (N1 * N2 >= 16 && (MODE == COL_FWD || MODE == COL_INV)) {
         // persistent pipelined variant
         const size_t smem2 = sizeof(double2) * (size_t)g.N * (TK + 1) * 2;
         auto kern = k_colp<N1, N2, MODE>;
@@ -1064,6 +1099,61 @@ int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
     return MM_OK;
 }
 
+// ||div P||_{H^-1} / npts of a stress field P (SoA, d*d components):
+// stencil divergence + R2C rows, FFT along axis 1 (3D), then the FFT along
+// axis 0 with the weighted |.|^2 sum in the same pass (COL_NORM).  The
+// spectral divergence of the reference (solver.py:364-371) is the DFT of the
+// central-difference divergence, which the row pass computes unscaled
+// (2h times larger): the 1/(4h^2) is applied to the sum.
+int mm_run_eq_residual(mm_ctx *ctx, const double *P, double *out) {
+    int rc = ensure_constants(ctx);
+    if (rc) return rc;
+    const int n = ctx->n, d = ctx->dim;
+    {
+        StageScope ss(ctx, MM_STAGE_OTHER);
+        if ((rc = run_rows(ctx, true, 0.0, nullptr, P))) return rc;
+    }
+    ColGeom g;
+    g.N = n;
+    g.ncol = ctx->nh;
+    g.n = n;
+    g.dim = d;
+    g.sym = ctx->sym;
+    g.thresh = ctx->sym_thresh;
+    g.scale = 1.0;
+    ColGeom gz = g;
+    if (d == 3) {
+        ColGeom gy = g;
+        gy.es = ctx->P;
+        gy.os = (int64_t)n * ctx->P;
+        gy.cs = (int64_t)n * n * ctx->P;
+        gz.es = (int64_t)n * ctx->P;
+        gz.os = ctx->P;
+        gz.cs = gy.cs;
+        StageScope ss(ctx, MM_STAGE_OTHER);
+        if ((rc = run_col<COL_FWD>(ctx, gy, n))) return rc;
+    } else {
+        gz.es = ctx->P;
+        gz.os = 0;
+        gz.cs = (int64_t)n * ctx->P;
+    }
+    const int n_outer = d == 3 ? n : 1;
+    const int64_t nb = (int64_t)((ctx->nh + 7) / 8) * n_outer * d;
+    if ((rc = mm_ensure_partials(ctx, nb))) return rc;
+    gz.partials = ctx->partials;
+    gz.red_out = ctx->red_out;
+    gz.count = ctx->red_count;
+    {
+        StageScope ss(ctx, MM_STAGE_OTHER);
+        if ((rc = run_col<COL_NORM>(ctx, gz, n_outer))) return rc;
+    }
+    double total;
+    if ((rc = mm_fetch_reduction(ctx, 1, &total))) return rc;
+    const double h = ctx->h;
+    *out = sqrt(total / (4.0 * h * h)) / (double)ctx->M;
+    return MM_OK;
+}
+
 int mm_ilog2(int n) { return ilog2_(n); }
 
 GSrc mm_gsrc(mm_ctx *ctx) {
@@ -1193,10 +1283,34 @@ k_col_slab(ColGeom g, SlabCol sc, const double2 *__restrict__ tw) {
         buf[n * LD + c] = v;
     }
     __syncthreads();
-    if constexpr (MODE == COL_FWD || MODE == COL_SOLVE)
+    if constexpr (MODE == COL_FWD || MODE == COL_SOLVE || MODE == COL_NORM)
         line_transform<N1, N2, TK, false>(buf, scr, N, tw);
     else
         line_transform<N1, N2, TK, true>(buf, scr, N, tw);
+    if constexpr (MODE == COL_NORM) {
+        __shared__ double red_sm[32];
+        const double *s0 = g.sym;
+        const double *slast = g.sym + (int64_t)(g.dim - 1) * g.n;
+        const double s1 = (g.dim == 3) ? g.sym[g.n + outer] : 0.0;
+        const int nyq = (g.n % 2 == 0) ? g.n / 2 : -1;
+        double acc[1] = {0.0};
+        for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
+            const int kl = w / TK, c = w - kl * TK;
+            const int k2 = k0 + c;
+            if (k2 >= g.ncol) continue;
+            double gsq = s0[kl];
+            if (g.dim == 3) gsq = gsq + s1;
+            gsq = gsq + slast[k2];
+            if (!(gsq > g.thresh)) continue;
+            const double2 X = buf[kl * LD + c];
+            const double m = (k2 == 0 || k2 == nyq) ? 1.0 : 2.0;
+            acc[0] += m * (X.x * X.x + X.y * X.y) / gsq;
+        }
+        const int ops[1] = {RED_SUM};
+        block_reduce<1>(acc, ops, red_sm);
+        grid_finalize<1>(acc, ops, g.partials, g.red_out, g.count, red_sm);
+        return;
+    }
     if constexpr (MODE == COL_SOLVE) {
         const double *s0 = g.sym;
         const double *slast = g.sym + (int64_t)(g.dim - 1) * g.n;

@@ -108,6 +108,9 @@ class MaterialModel:
         """Upload the per-point parameters of this model to a context."""
         raise NotImplementedError(f"{self.name} has no device local step")
 
+    def _prepare_stress(self, ctx, dt):
+        """Scalars the device stress needs for time step dt (none by default)."""
+
     def _points_context(self, npts):
         """Cached point-set context for direct local_sweeps calls."""
         ctx = getattr(self, "_pts_ctx", None)

@@ -181,6 +181,9 @@ class LiquidCrystalElastomer(MaterialModel):
         return self.frank_kappa * float(np.mean(np.sum(gn * gn, axis=(-2, -1))))
 
     # -- device ------------------------------------------------------------------
+    def _prepare_stress(self, ctx, dt):
+        ctx.set_lce(**self._scalars(dt))  # viscous coefficient nu_F / dt
+
     def _scalars(self, dt):
         d = self.dim
         r1d = self.r ** (1.0 / d)

@@ -26,8 +26,8 @@ import numpy as np
 
 from . import _lib
 from ._engine import STATE_FIELDS, Engine, field_shape
-from .errors import ConvergenceError, DivergenceError, ParameterError
-from .grid import Grid, forward_transform, mean_field, modified_symbols
+from .errors import ConfigurationError, ConvergenceError, DivergenceError, ParameterError
+from .grid import Grid, mean_field
 from .materials.base import DeviceLocalStats
 from .projection import MacroBC, macro_gradient
 
@@ -544,23 +544,23 @@ def _solve_fused(grid, model, bc, params, policy, state, r_l_tol):
 # ---------------------------------------------------------------------------
 
 def equilibrium_residual(grid: Grid, model, state: ADMMState, dt: float = 0.0) -> float:
-    """H^-1-type norm of div P (solver.py:346-371); post-convergence
-    diagnostic evaluated on host views of the state."""
-    d = grid.dim
-    npts = grid.npoints
-    prev = state.prev_F
-    Pf = model.stress_total(state.F.reshape(npts, d, d), state.internal,
-                            prev.reshape(npts, d, d) if prev is not None else None,
-                            state.prev_internal, dt)
-    P = Pf.reshape(grid.shape + (d, d))
-    freqs = modified_symbols(grid)
-    Phat = forward_transform(grid, P)
-    divhat = np.einsum("...ij,...j->...i", Phat, freqs.grad_sym)
-    gsq = freqs.grad_sq
-    live = gsq > 1e-14 * gsq.max()
-    w = np.where(live, 1.0 / np.where(live, gsq, 1.0), 0.0)
-    total = np.sum(np.abs(divhat) ** 2 * w[..., None])
-    return float(np.sqrt(total) / npts)
+    """Negative norm of div P of the total stress (solver.py:346-371), on the
+    device (mm_equilibrium_residual): the material's total stress into a
+    scratch field, its central-difference divergence fused with the R2C row
+    transform (the reference's spectral divergence with g_j = i sin(h xi)/h
+    is exactly the DFT of that stencil), the column FFTs, and the sum of
+    |div P_hat|^2 / |g|^2 over live modes in the last column pass (half
+    spectrum, conjugate columns counted twice)."""
+    mat = getattr(model, "_material_id", None)
+    if mat is None:
+        raise ConfigurationError(f"{getattr(model, 'name', model)} has no device stress")
+    if getattr(model, "dim", grid.dim) != grid.dim:
+        raise ConfigurationError("model and grid dimensions differ")
+    if mat == _lib.MAT_LCE and dt > 0.0 and model.nu_F > 0.0 and state.prev_F is None:
+        raise ParameterError("viscous stress needs prev_F (call begin_time_step)")
+    eng = state._attach(grid, model)
+    model._prepare_stress(eng.ctx, dt)
+    return eng.ctx.equilibrium_residual(mat, dt)
 
 
 def macro_stress(grid: Grid, state: ADMMState) -> np.ndarray:

@@ -266,7 +266,114 @@ def frank(dim, n, seed=4):
     return dict(dim=dim, n=n, L=0.5, n_field=nf, kappa=0.3, ff=ff)
 
 
+def eq_residual_cases():
+    """equilibrium_residual (solver.py:346-371) on seeded non-equilibrium
+    states: MR 2D/3D, quadratic on an odd grid, LCE 2D viscous, LCE 3D."""
+    rng = np.random.default_rng(601)
+    out = {}
+
+    def state_for(g, model, F, internal=None, prev_F=None, prev_internal=None):
+        d = g.dim
+        z = np.zeros(g.shape + (d, d))
+        return mm.ADMMState(u_mean=np.eye(d), u_tilde=np.zeros(g.shape + (d,)), grad_u=z.copy(),
+                            F=F, lam=z.copy(), internal=internal or {}, rho=1.0,
+                            prev_F=prev_F, prev_internal=prev_internal)
+
+    # MR 2D, two-phase
+    g = mm.Grid(2, 16, 0.5)
+    y = g.coords()[..., 1]
+    mu, kap = scenarios.composite_moduli((y + 0.5) < 0.5, 1.0, 20.0, 9.8)
+    F = np.eye(2) + 0.05 * rng.standard_normal(g.shape + (2, 2))
+    m = mm.MooneyRivlin(mu, kap, dim=2, mu_rep=1.0)
+    out["mr2d_F"], out["mr2d_mu"], out["mr2d_kappa"] = F, mu, kap
+    out["mr2d_val"] = mm.equilibrium_residual(g, m, state_for(g, m, F))
+    # MR 3D
+    g = mm.Grid(3, 8, 0.5)
+    x = g.coords()[..., 0]
+    mu, kap = scenarios.composite_moduli((x + 0.5) < 0.5, 1.0, 20.0, 9.8)
+    F = np.eye(3) + 0.05 * rng.standard_normal(g.shape + (3, 3))
+    m = mm.MooneyRivlin(mu, kap, dim=3, mu_rep=1.0)
+    out["mr3d_F"], out["mr3d_mu"], out["mr3d_kappa"] = F, mu, kap
+    out["mr3d_val"] = mm.equilibrium_residual(g, m, state_for(g, m, F))
+    # quadratic, odd n
+    g = mm.Grid(2, 9, 0.5)
+    c = 1.0 + rng.random(g.npoints)
+    F = np.eye(2) + 0.1 * rng.standard_normal(g.shape + (2, 2))
+    m = mm.QuadraticMaterial(c, dim=2)
+    out["quad_F"], out["quad_c"] = F, c
+    out["quad_val"] = mm.equilibrium_residual(g, m, state_for(g, m, F))
+    # LCE 2D, viscous time step
+    g = mm.Grid(2, 16, 0.5)
+    n0 = scenarios.make_stripe_n0(g, [1.0, 0.2], [0.2, 1.0], 4)
+    m = mm.LiquidCrystalElastomer(mu=1.0, r=1.5, alpha=0.2, frank_kappa=1e-4, n0=n0, dim=2,
+                                  nu_F=0.5, nu_n=0.2)
+    internal = m.init_internal(g.npoints)
+    internal["angles"] = internal["angles"] + 0.1 * rng.standard_normal(g.npoints)
+    internal["p_inc"] = 0.05 * rng.standard_normal(g.npoints)
+    F = np.eye(2) + 0.05 * rng.standard_normal(g.shape + (2, 2))
+    Fk = np.eye(2) + 0.05 * rng.standard_normal(g.shape + (2, 2))
+    st = state_for(g, m, F, internal, prev_F=Fk, prev_internal=m.init_internal(g.npoints))
+    out["lce2d_n0"], out["lce2d_F"], out["lce2d_Fk"] = n0, F, Fk
+    out["lce2d_angles"], out["lce2d_p_inc"] = internal["angles"], internal["p_inc"]
+    out["lce2d_val"] = mm.equilibrium_residual(g, m, st, dt=0.1)
+    # LCE 3D
+    g = mm.Grid(3, 8, 0.5)
+    n0 = scenarios.generate_polydomain_n0(g, 0.25, seed=7)
+    m = mm.LiquidCrystalElastomer(mu=1.0, r=2.0, alpha=0.1, frank_kappa=1e-4, n0=n0, dim=3)
+    internal = m.init_internal(g.npoints)
+    internal["angles"] = internal["angles"] + 0.1 * rng.standard_normal((g.npoints, 2))
+    internal["p_inc"] = 0.05 * rng.standard_normal(g.npoints)
+    F = np.eye(3) + 0.05 * rng.standard_normal(g.shape + (3, 3))
+    out["lce3d_n0"], out["lce3d_F"] = n0, F
+    out["lce3d_angles"], out["lce3d_chart"] = internal["angles"], internal["chart"]
+    out["lce3d_p_inc"] = internal["p_inc"]
+    out["lce3d_val"] = mm.equilibrium_residual(g, m, state_for(g, m, F, internal))
+    return out
+
+
+def scenario_fields():
+    """Host microstructure generators and protocol bookkeeping."""
+    g2, g3 = mm.Grid(2, 16, 0.5), mm.Grid(3, 8, 0.5)
+    p = mm.ProtocolSpec("custom", 1.0, 0.9, -0.025,
+                        strain_mask=[[1, 1, 1], [1, 0, 1], [1, 1, 0]])
+    bc = p.macro_bc(0.95, 3, reference=np.diag([1.0, 1.1, 0.9]))
+    pv = mm.ProtocolSpec("monodomain", 1.0, 1.1, 0.05, rate=0.25)
+    n3 = scenarios.generate_polydomain_n0(g3, 0.3, seed=2)
+    return dict(poly2d=scenarios.generate_polydomain_n0(g2, 0.25, seed=3), poly3d=n3,
+                stripe2d=scenarios.make_stripe_n0(g2, [1.0, 0.3], [-0.2, 1.0], 4),
+                stripe3d=scenarios.make_stripe_n0(g3, [1.0, 0.0, 0.3], [0.0, 1.0, 0.0], 2),
+                moduli=np.stack(scenarios.composite_moduli(np.linspace(-0.2, 1.2, 11), 2.0,
+                                                           10.0, 5.0)),
+                S3=scenarios.orientation_tensor(n3),
+                S2=scenarios.orientation_tensor(scenarios.make_stripe_n0(g2, [1, 0], [0, 1], 2)),
+                sched=p.schedule(), bc_mask=bc.strain_mask, bc_value=bc.value,
+                visc_dt=pv.dt, visc_sched=pv.schedule())
+
+
+def lce_protocol_visc():
+    """Viscous load stepping of a 2D stripe LCE (run_lce_protocol with
+    relaxation and rate-derived time step; local-convergent inputs)."""
+    g = mm.Grid(2, 16, 0.5)
+    n0 = scenarios.make_stripe_n0(g, [1.0, 0.2], [0.2, 1.0], 4)
+    m = mm.LiquidCrystalElastomer(mu=1.0, r=1.5, alpha=0.2, frank_kappa=1e-4, n0=n0, dim=2,
+                                  nu_F=0.5, nu_n=0.2)
+    proto = mm.ProtocolSpec("monodomain", 1.0, 1.04, 0.02, rate=0.2)
+    study = mm.run_lce_protocol(g, m, proto, relax=True, seed=3, perturb=1e-4)
+    recs = study.records
+    st = study.state
+    return dict(n=16, L=0.5, n0=n0, lams=study.lams,
+                outer_iters=np.array([r.outer_iters for r in recs]),
+                nominal=study.nominal, S=study.S, Fbar=np.array([r.Fbar for r in recs]),
+                reference=study.reference, F=st.F, lam=st.lam, angles=st.internal["angles"],
+                p_inc=st.internal["p_inc"], total_sweeps=st.total_sweeps)
+
+
 def main():
+    only = sys.argv[1:]
+    if only:  # regenerate the named fixtures only
+        for name in only:
+            save(name, **globals()[name]())
+        return 0
     save("local_mr2d", **local_mr(2, 101, 256, 25, 1e-11, 5.0))
     save("local_mr2d_long", **local_mr(2, 102, 64, 8000, 1e-11, 6.0))
     save("local_mr3d", **local_mr(3, 103, 200, 25, 1e-11, 5.0))
@@ -292,6 +399,9 @@ def main():
     save("lce_poly_2d", **lce_poly_one_iter(2, 16))
     # 3D Newton sweeps amplify roundoff faster: shorter budget
     save("lce_poly_3d", **lce_poly_one_iter(3, 8, max_local=5))
+    save("eq_residual_cases", **eq_residual_cases())
+    save("scenario_fields", **scenario_fields())
+    save("lce_protocol_visc", **lce_protocol_visc())
 
 
 if __name__ == "__main__":
