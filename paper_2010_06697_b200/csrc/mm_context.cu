@@ -1,10 +1,15 @@
 // Context lifetime, host<->device transfers (AoS <-> SoA) and the C-ABI
 // entry points of libmm_admm (declared in include/mm_admm.h).
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <stdarg.h>
 
+#include <mutex>
+#include <sched.h>
+#include <string.h>
+#include <thread>
 #include <vector>
 
 #include "mm_internal.cuh"
@@ -21,19 +26,58 @@ int mm_fail(mm_ctx *ctx, int code, const char *fmt, ...) {
     return code;
 }
 
+// Device memory comes from the device's stream-ordered pool, which keeps up
+// to kPoolKeepBytes of freed memory reserved for the process (like a caching
+// allocator): a context created after another was destroyed -- a solve on
+// host buffers after another -- reuses mapped memory instead of paying
+// cudaMalloc's page mapping again.
+static const uint64_t kPoolKeepBytes = (uint64_t)48 << 30;
+static bool g_pool_ready[64];
+static int g_use_pool = -1;
+
 int mm_alloc(mm_ctx *ctx, void **ptr, size_t bytes) {
     if (bytes == 0) bytes = 8;
-    cudaError_t e = cudaMalloc(ptr, bytes);
+    if (g_use_pool < 0) {
+        const char *e = getenv("MM_DEVICE_POOL");
+        g_use_pool = (e && e[0] == '0') ? 0 : 1;
+    }
+    if (!g_use_pool) {
+        cudaError_t e = cudaMalloc(ptr, bytes);
+        if (e != cudaSuccess)
+            return mm_fail(ctx, MM_ERR_CUDA, "cudaMalloc(%zu) failed: %s", bytes,
+                           cudaGetErrorString(e));
+        ctx->bytes += (int64_t)bytes;
+        return MM_OK;
+    }
+    const int dev = ctx->device;
+    if (dev >= 0 && dev < 64 && !g_pool_ready[dev]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = kPoolKeepBytes;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+        g_pool_ready[dev] = true;
+    }
+    cudaError_t e = cudaMallocAsync(ptr, bytes, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);  // usable from any stream
     if (e != cudaSuccess)
-        return mm_fail(ctx, MM_ERR_CUDA, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+        return mm_fail(ctx, MM_ERR_CUDA, "device allocation of %zu B failed: %s", bytes,
+                       cudaGetErrorString(e));
     ctx->bytes += (int64_t)bytes;
     return MM_OK;
+}
+
+void mm_free(mm_ctx *ctx, void *p) {
+    if (!p) return;
+    if (g_use_pool) cudaFreeAsync(p, ctx->stream);
+    else cudaFree(p);
 }
 
 int mm_ensure_partials(mm_ctx *ctx, int64_t nblocks) {
     if (nblocks <= ctx->partials_cap) return MM_OK;
     if (ctx->partials) {
-        cudaFree(ctx->partials);
+        mm_free(ctx, ctx->partials);
         ctx->bytes -= ctx->partials_cap * MM_MAX_PARTIALS * (int64_t)sizeof(double);
     }
     ctx->partials = nullptr;
@@ -162,20 +206,78 @@ static int ensure_field(mm_ctx *ctx, double **slot, int ncomp) {
     return MM_OK;
 }
 
+// Host staging.  Transfers move CHUNK-byte pieces through a device stage
+// (AoS <-> SoA transpose on the GPU) and, for pageable host memory, through
+// two pinned halves shared by every context of the process: while the DMA of
+// chunk i runs, host threads copy chunk i +- 1 between the caller's array and
+// the other half (multi-threaded: both the memcpy bandwidth and the page
+// faults of freshly allocated destinations scale with threads).  Pinned
+// caller memory is DMA'd directly.
+static const size_t kChunkBytes = (size_t)48 << 20;
+
+struct PinnedPool {
+    std::mutex mu;
+    char *half[2] = {nullptr, nullptr};
+    size_t cap = 0;
+};
+static PinnedPool g_pinned;
+
+static int host_threads() {
+    static int nt = 0;
+    if (!nt) {
+        cpu_set_t set;
+        int c = 0;
+        if (sched_getaffinity(0, sizeof set, &set) == 0) c = CPU_COUNT(&set);
+        nt = std::max(1, std::min(c, 16));
+    }
+    return nt;
+}
+
+static void par_memcpy(void *dst, const void *src, size_t bytes) {
+    const int nt = host_threads();
+    if (nt <= 1 || bytes < ((size_t)4 << 20)) {
+        memcpy(dst, src, bytes);
+        return;
+    }
+    const size_t per = ((bytes + nt - 1) / nt + 4095) & ~(size_t)4095;
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t) {
+        const size_t off = per * t;
+        if (off >= bytes) break;
+        const size_t len = std::min(per, bytes - off);
+        th.emplace_back([=] { memcpy((char *)dst + off, (const char *)src + off, len); });
+    }
+    memcpy(dst, src, std::min(per, bytes));
+    for (auto &x : th) x.join();
+}
+
 static int ensure_stage(mm_ctx *ctx, int64_t ndoubles) {
     if (ndoubles <= ctx->stage_cap) return MM_OK;
     if (ctx->stage) {
-        cudaFree(ctx->stage);
+        mm_free(ctx, ctx->stage);
         ctx->bytes -= ctx->stage_cap * 8;
     }
-    if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
     ctx->stage = nullptr;
-    ctx->host_stage = nullptr;
     int rc = mm_alloc(ctx, (void **)&ctx->stage, sizeof(double) * ndoubles);
     if (rc) return rc;
-    MM_CUDA(ctx, cudaMallocHost((void **)&ctx->host_stage, sizeof(double) * ndoubles));
     ctx->stage_cap = ndoubles;
-    ctx->host_stage_cap = ndoubles;
+    if (!ctx->xfer_ev[0]) {
+        MM_CUDA(ctx, cudaEventCreateWithFlags(&ctx->xfer_ev[0], cudaEventDisableTiming));
+        MM_CUDA(ctx, cudaEventCreateWithFlags(&ctx->xfer_ev[1], cudaEventDisableTiming));
+    }
+    return MM_OK;
+}
+
+static int ensure_pinned(mm_ctx *ctx, size_t bytes) {  // caller holds g_pinned.mu
+    if (bytes <= g_pinned.cap) return MM_OK;
+    for (int h = 0; h < 2; ++h) {
+        if (g_pinned.half[h]) cudaFreeHost(g_pinned.half[h]);
+        g_pinned.half[h] = nullptr;
+    }
+    g_pinned.cap = 0;
+    for (int h = 0; h < 2; ++h)
+        MM_CUDA(ctx, cudaMallocHost((void **)&g_pinned.half[h], bytes));
+    g_pinned.cap = bytes;
     return MM_OK;
 }
 
@@ -188,44 +290,91 @@ static bool is_pinned(const void *p) {
     return a.type == cudaMemoryTypeHost;
 }
 
+static void launch_xpose(mm_ctx *ctx, bool to_soa, bool add, double *dev, int64_t p0, int64_t np,
+                         int ncomp) {
+    const int threads = 256;
+    const int blocks = (int)std::min<int64_t>((np * ncomp + threads - 1) / threads, 148 * 32);
+    if (!to_soa)
+        k_soa_to_aos<<<blocks, threads, 0, ctx->stream>>>(dev, ctx->stage, p0, np, ncomp, ctx->M);
+    else if (add)
+        k_aos_add_soa<<<blocks, threads, 0, ctx->stream>>>(ctx->stage, dev, p0, np, ncomp, ctx->M);
+    else
+        k_aos_to_soa<<<blocks, threads, 0, ctx->stream>>>(ctx->stage, dev, p0, np, ncomp, ctx->M);
+}
+
 static int transfer(mm_ctx *ctx, double *dev, int ncomp, const double *hsrc, double *hdst,
                     bool add = false) {
     const int64_t M = ctx->M;
-    const int64_t chunk_pts = std::max<int64_t>(1, std::min<int64_t>(M, (int64_t)(1 << 22)));
+    const int64_t chunk_pts =
+        std::max<int64_t>(1, std::min<int64_t>(M, (int64_t)(kChunkBytes / (8 * ncomp))));
     int rc = ensure_stage(ctx, chunk_pts * ncomp);
     if (rc) return rc;
-    const bool pinned = is_pinned(hsrc ? (const void *)hsrc : (const void *)hdst);
-    for (int64_t p0 = 0; p0 < M; p0 += chunk_pts) {
-        int64_t np = std::min(chunk_pts, M - p0);
-        size_t bytes = sizeof(double) * np * ncomp;
-        int threads = 256;
-        int blocks = (int)std::min<int64_t>((np * ncomp + threads - 1) / threads, 148 * 32);
-        if (hsrc) {
-            const double *src = hsrc + p0 * ncomp;
-            if (!pinned) {
-                // pageable host memory: bounce through the pinned stage
-                memcpy(ctx->host_stage, src, bytes);
-                src = ctx->host_stage;
+    const bool up = hsrc != nullptr;
+    const bool pinned = is_pinned(up ? (const void *)hsrc : (const void *)hdst);
+    const int64_t nchunk = (M + chunk_pts - 1) / chunk_pts;
+    auto span = [&](int64_t i, int64_t &p0, int64_t &np) {
+        p0 = i * chunk_pts;
+        np = std::min(chunk_pts, M - p0);
+    };
+    if (pinned) {
+        for (int64_t i = 0; i < nchunk; ++i) {
+            int64_t p0, np;
+            span(i, p0, np);
+            const size_t bytes = sizeof(double) * np * ncomp;
+            if (up) {
+                MM_CUDA(ctx, cudaMemcpyAsync(ctx->stage, hsrc + p0 * ncomp, bytes,
+                                             cudaMemcpyHostToDevice, ctx->stream));
+                launch_xpose(ctx, true, add, dev, p0, np, ncomp);
+            } else {
+                launch_xpose(ctx, false, false, dev, p0, np, ncomp);
+                MM_CUDA(ctx, cudaMemcpyAsync(hdst + p0 * ncomp, ctx->stage, bytes,
+                                             cudaMemcpyDeviceToHost, ctx->stream));
             }
-            MM_CUDA(ctx, cudaMemcpyAsync(ctx->stage, src, bytes, cudaMemcpyHostToDevice,
-                                         ctx->stream));
-            if (add)
-                k_aos_add_soa<<<blocks, threads, 0, ctx->stream>>>(ctx->stage, dev, p0, np, ncomp, M);
-            else
-                k_aos_to_soa<<<blocks, threads, 0, ctx->stream>>>(ctx->stage, dev, p0, np, ncomp, M);
             MM_LAUNCH_CHECK(ctx);
-            if (!pinned) MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-        } else {
-            k_soa_to_aos<<<blocks, threads, 0, ctx->stream>>>(dev, ctx->stage, p0, np, ncomp, M);
+        }
+        MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        return MM_OK;
+    }
+    std::lock_guard<std::mutex> lock(g_pinned.mu);
+    if ((rc = ensure_pinned(ctx, kChunkBytes))) return rc;
+    if (up) {
+        for (int64_t i = 0; i < nchunk; ++i) {
+            int64_t p0, np;
+            span(i, p0, np);
+            const size_t bytes = sizeof(double) * np * ncomp;
+            const int h = (int)(i & 1);
+            // the DMA that last read this half (chunk i - 2) must be done
+            if (i >= 2) MM_CUDA(ctx, cudaEventSynchronize(ctx->xfer_ev[h]));
+            par_memcpy(g_pinned.half[h], hsrc + p0 * ncomp, bytes);
+            MM_CUDA(ctx, cudaMemcpyAsync(ctx->stage, g_pinned.half[h], bytes,
+                                         cudaMemcpyHostToDevice, ctx->stream));
+            MM_CUDA(ctx, cudaEventRecord(ctx->xfer_ev[h], ctx->stream));
+            launch_xpose(ctx, true, add, dev, p0, np, ncomp);
             MM_LAUNCH_CHECK(ctx);
-            double *dst = pinned ? hdst + p0 * ncomp : ctx->host_stage;
-            MM_CUDA(ctx, cudaMemcpyAsync(dst, ctx->stage, bytes, cudaMemcpyDeviceToHost,
-                                         ctx->stream));
-            MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-            if (!pinned) memcpy(hdst + p0 * ncomp, ctx->host_stage, bytes);
+        }
+    } else {
+        for (int64_t i = 0; i <= nchunk; ++i) {
+            if (i < nchunk) {
+                int64_t p0, np;
+                span(i, p0, np);
+                const int h = (int)(i & 1);
+                launch_xpose(ctx, false, false, dev, p0, np, ncomp);
+                MM_LAUNCH_CHECK(ctx);
+                MM_CUDA(ctx, cudaMemcpyAsync(g_pinned.half[h], ctx->stage,
+                                             sizeof(double) * np * ncomp,
+                                             cudaMemcpyDeviceToHost, ctx->stream));
+                MM_CUDA(ctx, cudaEventRecord(ctx->xfer_ev[h], ctx->stream));
+            }
+            if (i >= 1) {  // copy out chunk i - 1 while chunk i is in flight
+                int64_t p0, np;
+                span(i - 1, p0, np);
+                const int h = (int)((i - 1) & 1);
+                MM_CUDA(ctx, cudaEventSynchronize(ctx->xfer_ev[h]));
+                par_memcpy(hdst + p0 * ncomp, g_pinned.half[h], sizeof(double) * np * ncomp);
+            }
         }
     }
-    if (hsrc) MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return MM_OK;
 }
 
@@ -451,20 +600,14 @@ void mm_destroy(mm_ctx *ctx) {
                       ctx->prevChart, ctx->prevPinc, ctx->dirbuf, ctx->Ut2, ctx->halo_in_lo,
                       ctx->halo_in_hi, ctx->halo_out_lo, ctx->halo_out_hi, ctx->sym, ctx->partials, ctx->red_out,
                       ctx->res, ctx->tstate, ctx->stage, ctx->Pbuf};
-    for (double *p : ptrs)
-        if (p) cudaFree(p);
-    if (ctx->spec) cudaFree(ctx->spec);
-    if (ctx->sendbuf) cudaFree(ctx->sendbuf);
-    if (ctx->recvbuf) cudaFree(ctx->recvbuf);
-    if (ctx->tw_full) cudaFree(ctx->tw_full);
-    if (ctx->tw_half) cudaFree(ctx->tw_half);
-    if (ctx->tw_r2c) cudaFree(ctx->tw_r2c);
-    if (ctx->red_count) cudaFree(ctx->red_count);
-    if (ctx->nsw) cudaFree(ctx->nsw);
-    if (ctx->ok) cudaFree(ctx->ok);
-    if (ctx->freestate) cudaFree(ctx->freestate);
+    for (double *p : ptrs) mm_free(ctx, p);
+    void *others[] = {ctx->spec, ctx->sendbuf, ctx->recvbuf, ctx->tw_full, ctx->tw_half,
+                      ctx->tw_r2c, ctx->red_count, ctx->nsw, ctx->ok, ctx->freestate};
+    for (void *p : others) mm_free(ctx, p);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->host_out) cudaFreeHost(ctx->host_out);
-    if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
+    if (ctx->xfer_ev[0]) cudaEventDestroy(ctx->xfer_ev[0]);
+    if (ctx->xfer_ev[1]) cudaEventDestroy(ctx->xfer_ev[1]);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

@@ -58,8 +58,7 @@ struct mm_ctx {
     // staging for AoS <-> SoA
     double *stage = nullptr;
     int64_t stage_cap = 0;     // doubles
-    double *host_stage = nullptr;  // pinned
-    int64_t host_stage_cap = 0;
+    cudaEvent_t xfer_ev[2] = {nullptr, nullptr};  // pinned-half reuse (transfers)
     // stage profiling (CUDA events on ctx->stream) and launch counting
     bool prof_on = false;
     double prof_ms[MM_NSTAGE] = {0};
@@ -115,6 +114,7 @@ int mm_fail(mm_ctx *ctx, int code, const char *fmt, ...);
 
 int mm_alloc(mm_ctx *ctx, void **ptr, size_t bytes);
 int mm_ensure_partials(mm_ctx *ctx, int64_t nblocks);
+void mm_free(mm_ctx *ctx, void *p);
 // copy the finalized reduction results (K doubles) back to host
 int mm_fetch_reduction(mm_ctx *ctx, int K, double *out);
 
