@@ -235,7 +235,11 @@ int mm_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, double
  * grad_u implicitly as u_mean + D u_tilde instead of storing the 9-component
  * field (the local step and the next update rebuild it with the same
  * stencil expression; a download materialises it). */
-enum mm_option { MM_OPT_IMPLICIT_GRAD = 0 };
+/* MM_OPT_STENCIL_MARCH (default 1): the 3D residual pass of
+ * mm_project_residuals uses the plane-marching kernel (register/shared-memory
+ * stencil reuse) when n is a multiple of 32; 0 selects the per-voxel kernel
+ * (the two differ only in the order of the residual sums). */
+enum mm_option { MM_OPT_IMPLICIT_GRAD = 0, MM_OPT_STENCIL_MARCH = 1 };
 int mm_set_option(mm_ctx *ctx, int option, int64_t value);
 
 /* Central-difference stencils on the grid fields (grid.py:227-249):

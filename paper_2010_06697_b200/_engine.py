@@ -36,6 +36,7 @@ class Engine:
         self.ctx.set_symbols(tab, thresh)
         # grad_u storage policy (include/mm_admm.h, MM_OPT_IMPLICIT_GRAD)
         self.ctx.set_option(0, int(os.environ.get("MM_IMPLICIT_GRAD", "0")))
+        self.ctx.set_option(1, int(os.environ.get("MM_STENCIL_MARCH", "1")))
         self.model = None          # model whose parameters are on the device
         self.model_version = None
         self.lam_sum = None        # device-side sum of lam (None: recompute)

@@ -936,6 +936,7 @@ int mm_set_option(mm_ctx *ctx, int option, int64_t value) {
             ctx->opt_implicit_g = on;
             return MM_OK;
         }
+        case MM_OPT_STENCIL_MARCH: ctx->opt_march = value != 0; return MM_OK;
         default: return mm_fail(ctx, MM_ERR_PARAM, "unknown option %d", option);
     }
 }

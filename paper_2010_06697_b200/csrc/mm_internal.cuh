@@ -74,6 +74,7 @@ struct mm_ctx {
     // as ubar + D u_tilde (the gradient field is not stored); G is then a
     // cache filled on demand (downloads, LCE local step).
     bool opt_implicit_g = false;  // MM_OPT_IMPLICIT_GRAD
+    bool opt_march = true;        // MM_OPT_STENCIL_MARCH
     bool lam_pending = false;     // multiplier ascent deferred by mm_project_residuals
     double pending_rho = 0.0;
     bool g_implicit = false;
