@@ -256,6 +256,10 @@ int mm_stencil(mm_ctx *ctx, int op);
  * stress(). */
 int mm_equilibrium_residual(mm_ctx *ctx, int material, double dt, double *out);
 
+/* Test hook: y[i] = the device natural logarithm the Mooney-Rivlin objective
+ * uses (table-driven, csrc/mm_local.cu log_pos) for host arrays x, y. */
+int mm_selftest_log(mm_ctx *ctx, const double *x, double *y, int64_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -41,7 +41,7 @@ EXPORTS = (
     "mm_profile_enable", "mm_profile_read", "mm_frank_stencil", "mm_set_option",
     "mm_project_residuals", "mm_update_multiplier", "mm_update_and_sweep",
     "mm_create_slab", "mm_slab_buffer", "mm_slab_step", "mm_add_field",
-    "mm_equilibrium_residual",
+    "mm_equilibrium_residual", "mm_selftest_log",
 )
 
 SLAB_HALO_T, SLAB_FWD, SLAB_SOLVE, SLAB_INV, SLAB_HALO_U, SLAB_UPDATE, SLAB_GRAD = range(7)
@@ -145,6 +145,7 @@ def load_library():
             "mm_profile_read": ([P, ctypes.POINTER(ProfileC), I], I),
             "mm_add_field": ([P, I, P, I64], I),
             "mm_equilibrium_residual": ([P, I, D, ctypes.POINTER(D)], I),
+            "mm_selftest_log": ([P, P, P, I64], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -241,6 +242,12 @@ class Context:
         self.check(self.lib.mm_equilibrium_residual(self.h, int(material), float(dt),
                                                     ctypes.byref(out)))
         return out.value
+
+    def selftest_log(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty_like(x)
+        self.check(self.lib.mm_selftest_log(self.h, _ptr(x), _ptr(y), x.size))
+        return y
 
     def download(self, field, shape):
         out = host_empty(shape)

@@ -18,6 +18,8 @@
 #include <math.h>
 
 #include <algorithm>
+#include <stdint.h>
+#include <string.h>
 
 #include "mm_internal.cuh"
 
@@ -32,6 +34,79 @@ constexpr int LOCAL_THREADS = 128;
 #ifndef LOCAL_MIN_BLOCKS
 #define LOCAL_MIN_BLOCKS 4
 #endif
+
+// ---------------------------------------------------------------------------
+// log(J) of the Mooney-Rivlin objective, table-driven.  x = 2^k z with z in
+// [0.6875, 1.375) split into 128 subintervals (7 leading bits of the
+// biased representation); log x = k ln2 + log(c) + log1p(r), r = z/c - 1,
+// |r| < 0.0039, log1p(r) as its degree-7 Taylor polynomial (truncation
+// < 1e-20), log(c) in double-double from a host long-double table.  Absolute
+// error is ~1e-19 for x near 1 (where the objective evaluates it: J = det F
+// ~ 1) -- far below one ulp of the objective -- at ~25 instructions instead
+// of the ~45 of the libdevice routine, which took 28 % of the local step's
+// instructions (ncu source view).  Non-normal or non-positive x fall back to
+// log().
+// ---------------------------------------------------------------------------
+constexpr int LOGTAB_N = 128;
+__device__ double g_logtab[3 * LOGTAB_N];  // invc | log c (hi) | log c (lo)
+static bool g_logtab_ready[64];
+
+__device__ __forceinline__ double log_pos(double x, const double *__restrict__ T) {
+    const uint64_t ix = (uint64_t)__double_as_longlong(x);
+    if (ix - 0x0010000000000000ULL >= 0x7fe0000000000000ULL) return log(x);
+    const uint64_t tmp = ix - 0x3fe6000000000000ULL;
+    const int i = (int)((tmp >> 45) & (LOGTAB_N - 1));
+    const double kd = (double)((int64_t)tmp >> 52);
+    const double z = __longlong_as_double((long long)(ix - (tmp & 0xfff0000000000000ULL)));
+    const double r = fma(z, T[i], -1.0);
+    const double ln2_hi = 0x1.62e42fefa3800p-1, ln2_lo = 0x1.ef35793c76730p-45;
+    const double w = fma(kd, ln2_hi, T[LOGTAB_N + i]);
+    const double hi = w + r;
+    const double lo = (w - hi) + r;
+    const double r2 = r * r;
+    double p = fma(r, 1.0 / 7.0, -1.0 / 6.0);
+    p = fma(r, p, 0.2);
+    p = fma(r, p, -0.25);
+    p = fma(r, p, 1.0 / 3.0);
+    p = fma(r, p, -0.5);
+    return hi + (fma(kd, ln2_lo, T[2 * LOGTAB_N + i]) + fma(r2, p, lo));
+}
+
+static int ensure_logtab(mm_ctx *ctx) {
+    const int dev = ctx->device;
+    if (dev >= 0 && dev < 64 && g_logtab_ready[dev]) return MM_OK;
+    double h[3 * LOGTAB_N];
+    for (int i = 0; i < LOGTAB_N; ++i) {
+        const uint64_t lo = 0x3fe6000000000000ULL + ((uint64_t)i << 45);
+        const uint64_t hi = 0x3fe6000000000000ULL + ((uint64_t)(i + 1) << 45);
+        double zl, zh;
+        memcpy(&zl, &lo, 8);
+        memcpy(&zh, &hi, 8);
+        const long double c = 0.5L * ((long double)zl + (long double)zh);
+        const double invc = (double)(1.0L / c);
+        const long double lc = -logl((long double)invc);  // log c' with c' = 1/invc exactly
+        h[i] = invc;
+        h[LOGTAB_N + i] = (double)lc;
+        h[2 * LOGTAB_N + i] = (double)(lc - (long double)(double)lc);
+    }
+    MM_CUDA(ctx, cudaMemcpyToSymbol(g_logtab, h, sizeof h));
+    if (dev >= 0 && dev < 64) g_logtab_ready[dev] = true;
+    return MM_OK;
+}
+
+// Largest double T with sqrt_rn(T) <= tol, so that sqrt(gs) > tol <=> gs > T
+// exactly (sqrt is correctly rounded and monotone): the sweep loop tests the
+// squared gradient norm and takes square roots only where the reference's
+// residual value itself is needed.
+static double gs_threshold(double tol) {
+    if (tol != tol) return tol;
+    if (tol < 0.0) return -INFINITY;
+    if (tol == 0.0 || isinf(tol)) return tol;
+    double x = tol * tol;
+    while (x > 0.0 && sqrt(x) > tol) x = nextafter(x, 0.0);
+    while (sqrt(nextafter(x, INFINITY)) <= tol) x = nextafter(x, INFINITY);
+    return x;
+}
 
 inline int local_blocks(int64_t M) {
     int64_t b = (M + LOCAL_THREADS - 1) / LOCAL_THREADS;
@@ -223,7 +298,8 @@ __device__ __forceinline__ void cof_t(const double (&X)[D], double (&C)[D]) {
 // objective (mooney_rivlin.py:132-141 / quadratic.py:52-55); +inf if det <= 0
 template <int MAT, int D>
 __device__ __forceinline__ double objective(const double (&X)[D], const double (&B)[D],
-                                            double cG, double m, double k, double rho) {
+                                            double cG, double m, double k, double rho,
+                                            const double *__restrict__ LT) {
     double bx = 0.0, I1 = 0.0;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
@@ -235,13 +311,14 @@ __device__ __forceinline__ double objective(const double (&X)[D], const double (
     const double J = det_t<D>(X);
     if (J <= 0.0) return INFINITY;
     const double dd = (D == 4) ? 2.0 : 3.0;
-    return 0.5 * m * (I1 - 2.0 * log(J) - dd) + 0.5 * k * (J - 1.0) * (J - 1.0) + coupling;
+    return 0.5 * m * (I1 - 2.0 * log_pos(J, LT) - dd) + 0.5 * k * (J - 1.0) * (J - 1.0) + coupling;
 }
 
 // objective given det X (>0) already computed by the admissibility test
 template <int MAT, int D>
 __device__ __forceinline__ double objective_J(const double (&X)[D], double J, const double (&B)[D],
-                                              double cG, double m, double k, double rho) {
+                                              double cG, double m, double k, double rho,
+                                              const double *__restrict__ LT) {
     double bx = 0.0, I1 = 0.0;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
@@ -251,7 +328,7 @@ __device__ __forceinline__ double objective_J(const double (&X)[D], double J, co
     const double coupling = 0.5 * rho * I1 - bx + cG;
     if constexpr (MAT == MAT_QUAD) return 0.5 * m * I1 + coupling;
     const double dd = (D == 4) ? 2.0 : 3.0;
-    return 0.5 * m * (I1 - 2.0 * log(J) - dd) + 0.5 * k * (J - 1.0) * (J - 1.0) + coupling;
+    return 0.5 * m * (I1 - 2.0 * log_pos(J, LT) - dd) + 0.5 * k * (J - 1.0) * (J - 1.0) + coupling;
 }
 
 // gradient S(X) - lam - rho (G - X) = S(X) + rho X - B
@@ -301,25 +378,27 @@ __device__ __forceinline__ bool admissible(const double (&X)[D]) {
 
 // One point of the vectorised descent (base.py:124-230) for global sweeps
 // [s0, s1): X updated in place; t, freem, nsw persist across segments.
+// tol_gs = gs_threshold(tol): the activity test res > tol is evaluated as
+// |g|^2 > tol_gs (exactly equivalent); res = sqrt(|g|^2) is formed only for
+// the free-mode trend test and on return.
 template <int MAT, int D>
 __device__ __forceinline__ void descent_point(double (&X)[D], const double (&B)[D], double cG,
-                                              double m, double k, double rho, double tol,
+                                              double m, double k, double rho, double tol_gs,
                                               double phi_scale, int s0, int s1, double tmax,
                                               double &t, bool &freem, int &nsw, double &res,
-                                              bool &moved) {
+                                              bool &moved, const double *__restrict__ LT) {
     double g[D], Xt[D];
     gradient<MAT, D>(X, B, m, k, rho, g);
     double gs = 0.0;
 #pragma unroll
     for (int i = 0; i < D; ++i) gs += g[i] * g[i];
-    res = sqrt(gs);
     moved = false;
     bool have_phi = false;
     double phi_cur = 0.0;
     // a point is active at global sweep s iff it was active at every
     // earlier sweep (nsw == s) and res > tol; once inactive it stays so
     for (int s = s0; s < s1; ++s) {
-        if (nsw != s || !(res > tol)) break;
+        if (nsw != s || !(gs > tol_gs)) break;
         nsw += 1;
         moved = true;
         bool in_free = freem, in_arm = false;
@@ -329,7 +408,7 @@ __device__ __forceinline__ void descent_point(double (&X)[D], const double (&B)[
         if (!freem) {
             // phi at the current X is known when the previous sweep ended on
             // an accepted Armijo step or took no step (same X, same bits)
-            phi0 = have_phi ? phi_cur : objective<MAT, D>(X, B, cG, m, k, rho);
+            phi0 = have_phi ? phi_cur : objective<MAT, D>(X, B, cG, m, k, rho, LT);
             phi_cur = phi0;
             have_phi = true;
             gsq = gs;  // same g, same summation order as res (base.py:167 vs :156)
@@ -343,7 +422,7 @@ __device__ __forceinline__ void descent_point(double (&X)[D], const double (&B)[
                 in_arm = true;
             }
         }
-        const double res_before = res;
+        const double gs_before = gs;
         if (in_arm) {
             const double t_in = t;
             bool accepted = false;
@@ -353,10 +432,10 @@ __device__ __forceinline__ void descent_point(double (&X)[D], const double (&B)[
                 double phi_try = INFINITY;
                 double Jt = 0.0;
                 if constexpr (MAT == MAT_QUAD) {
-                    phi_try = objective<MAT, D>(Xt, B, cG, m, k, rho);
+                    phi_try = objective<MAT, D>(Xt, B, cG, m, k, rho, LT);
                 } else {
                     Jt = det_t<D>(Xt);  // admissibility and objective share J
-                    if (Jt > 0.0) phi_try = objective_J<MAT, D>(Xt, Jt, B, cG, m, k, rho);
+                    if (Jt > 0.0) phi_try = objective_J<MAT, D>(Xt, Jt, B, cG, m, k, rho, LT);
                 }
                 if (phi_try <= phi0 - BT_DECREASE * t * gsq) {
 #pragma unroll
@@ -400,13 +479,19 @@ __device__ __forceinline__ void descent_point(double (&X)[D], const double (&B)[
             gs = 0.0;
 #pragma unroll
             for (int i = 0; i < D; ++i) gs += g[i] * g[i];
-            res = sqrt(gs);
         }
-        if (in_free) {
-            if (res > res_before) t *= BT_SHRINK;
+        if (in_free) {  // residual trend (base.py:218-223) on the residual values
+            if (sqrt(gs) > sqrt(gs_before)) t *= BT_SHRINK;
             else t = fmin(t * 1.3, tmax);
         }
     }
+    res = sqrt(gs);
+}
+
+// stage the log table into shared memory (every thread of the block calls)
+__device__ __forceinline__ void load_logtab(double *sh) {
+    for (int i = threadIdx.x; i < 3 * LOGTAB_N; i += blockDim.x) sh[i] = g_logtab[i];
+    __syncthreads();
 }
 
 // slots: 0 sum res^2, 1 n_conv (res < tol), 2 max nsw (cumulative),
@@ -415,12 +500,14 @@ template <int MAT, int D>
 __global__ void __launch_bounds__(LOCAL_THREADS, LOCAL_MIN_BLOCKS)
 k_descent(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
           const double *__restrict__ modA, const double *__restrict__ modB, int64_t M,
-          double rho, double tol, double phi_scale, int s0, int s1, double *__restrict__ tstate,
-          uint8_t *__restrict__ freestate, double *__restrict__ res_out,
+          double rho, double tol, double tol_gs, double phi_scale, int s0, int s1,
+          double *__restrict__ tstate, uint8_t *__restrict__ freestate, double *__restrict__ res_out,
           int32_t *__restrict__ nsw_io, double *partials, double *red_out, unsigned int *count) {
     constexpr int K = 5 + D;  // ..., last slot: sum of per-point sweeps
     __shared__ double smem[32 * K];
     __shared__ double sacc[K * LOCAL_THREADS];
+    __shared__ double ltab[3 * LOGTAB_N];
+    load_logtab(ltab);
     SmemAcc<K> A;
     A.init(sacc);
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
@@ -453,8 +540,8 @@ k_descent(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
         }
         double res = 0.0;
         bool moved = false;
-        descent_point<MAT, D>(X, B, cG, m, k, rho, tol, phi_scale, s0, s1, tmax, t, freem, nsw,
-                              res, moved);
+        descent_point<MAT, D>(X, B, cG, m, k, rho, tol_gs, phi_scale, s0, s1, tmax, t, freem, nsw,
+                              res, moved, ltab);
         if (moved) {
 #pragma unroll
             for (int i = 0; i < D; ++i) F[i * M + p] = X[i];
@@ -503,12 +590,14 @@ __global__ void __launch_bounds__(LOCAL_THREADS, LOCAL_MIN_BLOCKS)
 k_update_local(double *__restrict__ F, double *__restrict__ Lam, double *__restrict__ Gout,
                const GSrc gs,
                const double *__restrict__ modA, const double *__restrict__ modB, int64_t M,
-               double rho_k, double rho, double tol, double phi_scale, int chunk,
+               double rho_k, double rho, double tol, double tol_gs, double phi_scale, int chunk,
                double *__restrict__ res_out, int32_t *__restrict__ nsw_out, double *partials,
                double *red_out, unsigned int *count) {
     constexpr int K = 5 + 2 * D;  // ..., last slot: sum of per-point sweeps
     __shared__ double smem[32 * K];
     __shared__ double sacc[K * LOCAL_THREADS];
+    __shared__ double ltab[(SWEEP && ALGO == 0) ? 3 * LOGTAB_N : 1];
+    if constexpr (SWEEP && ALGO == 0) load_logtab(ltab);
     SmemAcc<K> A;
     A.init(sacc);
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
@@ -554,8 +643,8 @@ k_update_local(double *__restrict__ F, double *__restrict__ Lam, double *__restr
                 const double t0 = (MAT == MAT_MR) ? 1.0 / (rho + m + 4.0 * k) : 1.0 / (rho + m);
                 double t = t0;
                 bool freem = false;
-                descent_point<MAT, D>(X, B, cG, m, k, rho, tol, phi_scale, 0, chunk, t0 * 16.0, t,
-                                      freem, nsw, res, moved);
+                descent_point<MAT, D>(X, B, cG, m, k, rho, tol_gs, phi_scale, 0, chunk, t0 * 16.0,
+                                      t, freem, nsw, res, moved, ltab);
             }
             if (moved) {
 #pragma unroll
@@ -739,9 +828,10 @@ static int launch_descent(mm_ctx *ctx, double rho, double tol, double phi_scale,
     int rc = mm_ensure_partials(ctx, blocks);
     if (rc) return rc;
     StageScope ss(ctx, MM_STAGE_LOCAL);
+    if ((rc = ensure_logtab(ctx))) return rc;
     k_descent<MAT, D><<<blocks, LOCAL_THREADS, 0, ctx->stream>>>(
         ctx->F, mm_gsrc(ctx), ctx->Lam, ctx->modA, MAT == MAT_MR ? ctx->modB : ctx->modA, ctx->M, rho,
-        tol, phi_scale, s0, s1, persist ? ctx->tstate : nullptr,
+        tol, gs_threshold(tol), phi_scale, s0, s1, persist ? ctx->tstate : nullptr,
         persist ? ctx->freestate : nullptr, want_points ? ctx->res : nullptr,
         (persist || want_points) ? ctx->nsw : nullptr, ctx->partials, ctx->red_out,
         ctx->red_count);
@@ -866,9 +956,10 @@ static int launch_update_local(mm_ctx *ctx, double rho_next, double tol, double 
     int rc = mm_ensure_partials(ctx, blocks);
     if (rc) return rc;
     StageScope ss(ctx, SWEEP ? MM_STAGE_FUSED : MM_STAGE_GRAD);
+    if ((rc = ensure_logtab(ctx))) return rc;
     k_update_local<MAT, D, ALGO, SWEEP><<<blocks, LOCAL_THREADS, 0, ctx->stream>>>(
         ctx->F, ctx->Lam, kFusedStoresG ? ctx->G : nullptr, mm_gsrc(ctx), ctx->modA, MAT == MAT_MR ? ctx->modB : ctx->modA, ctx->M,
-        ctx->pending_rho, rho_next, tol, phi_scale, chunk, want_points ? ctx->res : nullptr,
+        ctx->pending_rho, rho_next, tol, gs_threshold(tol), phi_scale, chunk, want_points ? ctx->res : nullptr,
         want_points ? ctx->nsw : nullptr, ctx->partials, ctx->red_out, ctx->red_count);
     MM_LAUNCH_CHECK(ctx);
     return MM_OK;
@@ -925,4 +1016,35 @@ int mm_flush_pending(mm_ctx *ctx) {
     if (!ctx->lam_pending) return MM_OK;
     mm_update_stats us;
     return mm_run_update(ctx, 0, 0.0, 0.0, 0, 0.0, 0, nullptr, &us);
+}
+
+// ---------------------------------------------------------------------------
+// test hook: the device log of the objective on caller-supplied arguments
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void k_selftest_log(const double *__restrict__ x, double *__restrict__ y, int64_t n) {
+    __shared__ double ltab[3 * LOGTAB_N];
+    load_logtab(ltab);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = log_pos(x[i], ltab);
+}
+}  // namespace
+
+extern "C" int mm_selftest_log(mm_ctx *ctx, const double *x, double *y, int64_t n) {
+    if (!ctx || !x || !y || n < 0) return MM_ERR_PARAM;
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    int rc = ensure_logtab(ctx);
+    if (rc) return rc;
+    double *d = nullptr;
+    if ((rc = mm_alloc(ctx, (void **)&d, sizeof(double) * 2 * (n ? n : 1)))) return rc;
+    MM_CUDA(ctx, cudaMemcpyAsync(d, x, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256 + 1, 148 * 8);
+    k_selftest_log<<<blocks, 256, 0, ctx->stream>>>(d, d + n, n);
+    MM_LAUNCH_CHECK(ctx);
+    MM_CUDA(ctx, cudaMemcpyAsync(y, d + n, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    mm_free(ctx, d);
+    ctx->bytes -= (int64_t)(sizeof(double) * 2 * (n ? n : 1));
+    return MM_OK;
 }

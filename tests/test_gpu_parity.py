@@ -326,3 +326,31 @@ def test_large_grid_invariants(n):
     assert np.sqrt(np.mean(div ** 2)) < 1e-9 * max(1.0, np.abs(lam).max())
     np.testing.assert_allclose(mm.mean_field(grid, st.grad_u), Fbar, atol=1e-12)
     assert np.abs(mm.mean_field(grid, st.u_tilde)).max() < 1e-13
+
+
+def test_device_log_accuracy():
+    """The table-driven log of the MR objective (csrc/mm_local.cu log_pos)
+    against an 80-bit reference: absolute error far below one ulp of the
+    objective near J = 1, <= 1 ulp relative elsewhere, libm fallback for
+    non-normal arguments."""
+    rng = np.random.default_rng(3)
+    near = 1.0 + np.concatenate([rng.uniform(-0.3, 0.3, 20000),
+                                 rng.standard_normal(20000) * 1e-3,
+                                 rng.standard_normal(5000) * 1e-8, [0.0, 1e-16, -1e-16]])
+    wide = np.exp(rng.uniform(-700, 700, 20000))
+    edge = np.array([np.finfo(float).tiny, 5e-324, 1e-310, np.finfo(float).max, 0.6875,
+                     1.375, np.nextafter(0.6875, 0), np.nextafter(1.375, 2), 0.5, 2.0])
+    x = np.concatenate([near, wide, edge])
+    ctx = mm._lib.Context(3, npts=8)
+    y = ctx.selftest_log(x)
+    ref = np.log(x.astype(np.longdouble))
+    err = np.abs(y.astype(np.longdouble) - ref)
+    ulp = np.spacing(np.abs(ref.astype(float)))
+    # the objective needs log J to absolute accuracy (it enters as I1 - 2 log J
+    # - d with I1 ~ d, and decisions are only taken on decreases above
+    # 64 eps (|phi| + phi_scale), base.py:168-171)
+    m = np.abs(x - 1.0) < 0.05
+    assert float(np.max(err[m])) < 4e-18
+    far = np.abs(x - 1.0) >= 0.3
+    assert float(np.max(err[far] / ulp[far])) <= 1.0
+    assert np.isneginf(ctx.selftest_log(np.array([0.0])))[0]
