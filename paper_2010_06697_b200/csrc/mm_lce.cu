@@ -388,12 +388,18 @@ __device__ __forceinline__ double phiJ3(const double (&Fl)[9], const double (&n)
 // Gaussian elimination on the 11x11 system held in shared memory: entry
 // (r, c) at S[(r*11 + c) * T], right-hand side r at S[(121 + r) * T]
 // (T = threads per block; each thread owns one column of the buffer).
-__device__ __forceinline__ bool gauss_smem11(double *S, int T, double (&x)[11]) {
+template <int T>
+__device__ __forceinline__ bool gauss_smem11(double *S, double (&x)[11]) {
+    // fully unrolled: every (r, c) offset is an immediate; the pivot row is
+    // held in registers while the rows below it are updated (same
+    // operations in the same order as the loop form, lce.py:315-349)
 #define AS(r, c) S[((r) * 11 + (c)) * T]
 #define BS(r) S[(121 + (r)) * T]
+#pragma unroll
     for (int col = 0; col < 11; ++col) {
         int piv = col;
         double best = fabs(AS(col, col));
+#pragma unroll
         for (int r = col + 1; r < 11; ++r) {
             const double v = fabs(AS(r, col));
             if (v > best) {
@@ -402,22 +408,32 @@ __device__ __forceinline__ bool gauss_smem11(double *S, int T, double (&x)[11]) 
             }
         }
         if (best < 1e-250) return false;
+        double prow[11];
+        double bcol;
         if (piv != col) {
-            for (int c = 0; c < 11; ++c) {
-                const double t = AS(col, c);
-                AS(col, c) = AS(piv, c);
-                AS(piv, c) = t;
+            // columns < col of both rows are never read again: not swapped
+#pragma unroll
+            for (int c = col; c < 11; ++c) {
+                prow[c] = S[(piv * 11 + c) * T];
+                S[(piv * 11 + c) * T] = AS(col, c);
             }
-            const double t = BS(col);
-            BS(col) = BS(piv);
-            BS(piv) = t;
+#pragma unroll
+            for (int c = col; c < 11; ++c) AS(col, c) = prow[c];
+            bcol = S[(121 + piv) * T];
+            S[(121 + piv) * T] = BS(col);
+            BS(col) = bcol;
+        } else {
+#pragma unroll
+            for (int c = col; c < 11; ++c) prow[c] = AS(col, c);
+            bcol = BS(col);
         }
-        const double inv = 1.0 / AS(col, col);
-        const double bcol = BS(col);
+        const double inv = 1.0 / prow[col];
+#pragma unroll
         for (int r = col + 1; r < 11; ++r) {
             const double f = AS(r, col) * inv;
             if (f != 0.0) {
-                for (int c = col; c < 11; ++c) AS(r, c) -= f * AS(col, c);
+#pragma unroll
+                for (int c = col; c < 11; ++c) AS(r, c) -= f * prow[c];
                 BS(r) -= f * bcol;
             }
         }
@@ -484,103 +500,117 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
         int64_t nsw = 0;
         double res = 0.0;
         bool converged = false;
-        for (int64_t it = 0; it < P.max_sweeps + 1; ++it) {
-            double n[3];
-            // keep the chart's azimuth well conditioned (lce.py:709-730)
-            if (sin(ph) < 0.1) {
+        // Sweeps that only ascend the nested det multiplier (the polydomain
+        // stall regime) are cheap; Newton sweeps are ~20x dearer.  Each lane
+        // first runs through its cheap sweeps (inner loop) and the warp then
+        // takes the Newton step for every lane that reached one, so Newton
+        // steps of different lanes execute together instead of one
+        // divergent Newton per sweep in which only the few lanes that need
+        // it are active.  Every lane performs exactly the same sequence of
+        // sweeps as the plain loop.
+        int64_t it = 0;
+        while (it < P.max_sweeps + 1) {
+            double n[3], sp, cp, st, ct, u[3], cc, J, dJ, pr, cof[9], gFl[9], gF2, gn[3];
+            double m1[3], mth[3], g1, g2, gnn, sp2;
+            bool newton = false;
+            for (; it < P.max_sweeps + 1; ++it) {
+                // keep the chart's azimuth well conditioned (lce.py:709-730)
+                if (sin(ph) < 0.1) {
+                    n_from_chart(ph, th, E, n);
+                    int k = 0;
+                    if (fabs(n[1]) < fabs(n[k])) k = 1;
+                    if (fabs(n[2]) < fabs(n[k])) k = 2;
+                    const double dot = (k == 0) ? n[0] : (k == 1 ? n[1] : n[2]);
+                    double e3[3], e3n = 0.0;
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        const double v = (i == k ? 1.0 : 0.0) - dot * n[i];
+                        e3[i] = v;
+                        e3n += v * v;
+                    }
+                    e3n = sqrt(e3n);
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        E[3 * i + 0] = n[i];
+                        E[3 * i + 2] = e3[i] / e3n;
+                    }
+                    E[0 * 3 + 1] = E[1 * 3 + 2] * E[2 * 3 + 0] - E[2 * 3 + 2] * E[1 * 3 + 0];
+                    E[1 * 3 + 1] = E[2 * 3 + 2] * E[0 * 3 + 0] - E[0 * 3 + 2] * E[2 * 3 + 0];
+                    E[2 * 3 + 1] = E[0 * 3 + 2] * E[1 * 3 + 0] - E[1 * 3 + 2] * E[0 * 3 + 0];
+                    ph = 0.5 * PI;
+                    th = 0.0;
+                }
                 n_from_chart(ph, th, E, n);
-                int k = 0;
-                if (fabs(n[1]) < fabs(n[k])) k = 1;
-                if (fabs(n[2]) < fabs(n[k])) k = 2;
-                const double dot = (k == 0) ? n[0] : (k == 1 ? n[1] : n[2]);
-                double e3[3], e3n = 0.0;
+                sincos(ph, &sp, &cp);
+                sincos(th, &st, &ct);
+#pragma unroll
+                for (int j = 0; j < 3; ++j) u[j] = Fl[0 * 3 + j] * n[0] + Fl[1 * 3 + j] * n[1] + Fl[2 * 3 + j] * n[2];
+                cc = u[0] * n0l[0] + u[1] * n0l[1] + u[2] * n0l[2];
+                J = det3(Fl);
+                dJ = J - 1.0;
+                pr = pp + gam * dJ;
+                cof[0] = Fl[4] * Fl[8] - Fl[5] * Fl[7];
+                cof[1] = Fl[5] * Fl[6] - Fl[3] * Fl[8];
+                cof[2] = Fl[3] * Fl[7] - Fl[4] * Fl[6];
+                cof[3] = Fl[2] * Fl[7] - Fl[1] * Fl[8];
+                cof[4] = Fl[0] * Fl[8] - Fl[2] * Fl[6];
+                cof[5] = Fl[1] * Fl[6] - Fl[0] * Fl[7];
+                cof[6] = Fl[1] * Fl[5] - Fl[2] * Fl[4];
+                cof[7] = Fl[2] * Fl[3] - Fl[0] * Fl[5];
+                cof[8] = Fl[0] * Fl[4] - Fl[1] * Fl[3];
+                gF2 = 0.0;
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) {
+                        const int a = 3 * i + j;
+                        const double gg = (mur * Fl[a] + q * n[i] * u[j] - mual * cc * n[i] * n0l[j] +
+                                           pr * cof[a] - D.l(a) - rho * (D.g(a) - Fl[a]) +
+                                           visF * (Fl[a] - D.k(a)));
+                        gFl[a] = gg;
+                        gF2 += gg * gg;
+                    }
+                // dW/dn (lce.py:653-663)
+                {
+                    const double v0 = Fl[0] * n[0] + Fl[3] * n[1] + Fl[6] * n[2];
+                    const double v1 = Fl[1] * n[0] + Fl[4] * n[1] + Fl[7] * n[2];
+                    const double v2 = Fl[2] * n[0] + Fl[5] * n[1] + Fl[8] * n[2];
+                    const double c2 = v0 * n0l[0] + v1 * n0l[1] + v2 * n0l[2];
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        const double h = Fl[3 * i + 0] * v0 + Fl[3 * i + 1] * v1 + Fl[3 * i + 2] * v2;
+                        const double v = Fl[3 * i + 0] * n0l[0] + Fl[3 * i + 1] * n0l[1] + Fl[3 * i + 2] * n0l[2];
+                        gn[i] = q * h - mual * c2 * v + ffl[i] + visn * (n[i] - nkl[i]);
+                    }
+                }
+                g1 = 0.0;
+                g2 = 0.0;
+                gnn = 0.0;
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
-                    const double v = (i == k ? 1.0 : 0.0) - dot * n[i];
-                    e3[i] = v;
-                    e3n += v * v;
+                    m1[i] = cp * ct * E[3 * i + 0] + cp * st * E[3 * i + 1] - sp * E[3 * i + 2];
+                    mth[i] = sp * (-st * E[3 * i + 0] + ct * E[3 * i + 1]);
+                    g1 += gn[i] * m1[i];
+                    g2 += gn[i] * mth[i];
+                    gnn += gn[i] * n[i];
                 }
-                e3n = sqrt(e3n);
-#pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    E[3 * i + 0] = n[i];
-                    E[3 * i + 2] = e3[i] / e3n;
+                sp2 = fmax(sp * sp, 1e-4);
+                res = sqrt(gF2 + g1 * g1 + g2 * g2 / sp2);
+                if (res < P.tol && fabs(dJ) <= P.det_tol) {
+                    converged = true;
+                    break;
                 }
-                E[0 * 3 + 1] = E[1 * 3 + 2] * E[2 * 3 + 0] - E[2 * 3 + 2] * E[1 * 3 + 0];
-                E[1 * 3 + 1] = E[2 * 3 + 2] * E[0 * 3 + 0] - E[0 * 3 + 2] * E[2 * 3 + 0];
-                E[2 * 3 + 1] = E[0 * 3 + 2] * E[1 * 3 + 0] - E[1 * 3 + 2] * E[0 * 3 + 0];
-                ph = 0.5 * PI;
-                th = 0.0;
-            }
-            n_from_chart(ph, th, E, n);
-            double sp, cp, st, ct;
-            sincos(ph, &sp, &cp);
-            sincos(th, &st, &ct);
-            double u[3];
-#pragma unroll
-            for (int j = 0; j < 3; ++j) u[j] = Fl[0 * 3 + j] * n[0] + Fl[1 * 3 + j] * n[1] + Fl[2 * 3 + j] * n[2];
-            const double cc = u[0] * n0l[0] + u[1] * n0l[1] + u[2] * n0l[2];
-            const double J = det3(Fl);
-            const double dJ = J - 1.0;
-            const double pr = pp + gam * dJ;
-            double cof[9];
-            cof[0] = Fl[4] * Fl[8] - Fl[5] * Fl[7];
-            cof[1] = Fl[5] * Fl[6] - Fl[3] * Fl[8];
-            cof[2] = Fl[3] * Fl[7] - Fl[4] * Fl[6];
-            cof[3] = Fl[2] * Fl[7] - Fl[1] * Fl[8];
-            cof[4] = Fl[0] * Fl[8] - Fl[2] * Fl[6];
-            cof[5] = Fl[1] * Fl[6] - Fl[0] * Fl[7];
-            cof[6] = Fl[1] * Fl[5] - Fl[2] * Fl[4];
-            cof[7] = Fl[2] * Fl[3] - Fl[0] * Fl[5];
-            cof[8] = Fl[0] * Fl[4] - Fl[1] * Fl[3];
-            double gFl[9], gF2 = 0.0;
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-#pragma unroll
-                for (int j = 0; j < 3; ++j) {
-                    const int a = 3 * i + j;
-                    const double gg = (mur * Fl[a] + q * n[i] * u[j] - mual * cc * n[i] * n0l[j] +
-                                       pr * cof[a] - D.l(a) - rho * (D.g(a) - Fl[a]) +
-                                       visF * (Fl[a] - D.k(a)));
-                    gFl[a] = gg;
-                    gF2 += gg * gg;
+                if (nsw >= P.max_sweeps) break;
+                nsw += 1;
+                if (fabs(dJ) > P.det_tol && res <= fmax(P.tol, 0.25 * gam * fabs(dJ))) {
+                    pp += gam * dJ;
+                    continue;
                 }
-            // dW/dn (lce.py:653-663)
-            double gn[3];
-            {
-                const double v0 = Fl[0] * n[0] + Fl[3] * n[1] + Fl[6] * n[2];
-                const double v1 = Fl[1] * n[0] + Fl[4] * n[1] + Fl[7] * n[2];
-                const double v2 = Fl[2] * n[0] + Fl[5] * n[1] + Fl[8] * n[2];
-                const double c2 = v0 * n0l[0] + v1 * n0l[1] + v2 * n0l[2];
-#pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    const double h = Fl[3 * i + 0] * v0 + Fl[3 * i + 1] * v1 + Fl[3 * i + 2] * v2;
-                    const double v = Fl[3 * i + 0] * n0l[0] + Fl[3 * i + 1] * n0l[1] + Fl[3 * i + 2] * n0l[2];
-                    gn[i] = q * h - mual * c2 * v + ffl[i] + visn * (n[i] - nkl[i]);
-                }
-            }
-            double m1[3], mth[3];
-            double g1 = 0.0, g2 = 0.0, gnn = 0.0;
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                m1[i] = cp * ct * E[3 * i + 0] + cp * st * E[3 * i + 1] - sp * E[3 * i + 2];
-                mth[i] = sp * (-st * E[3 * i + 0] + ct * E[3 * i + 1]);
-                g1 += gn[i] * m1[i];
-                g2 += gn[i] * mth[i];
-                gnn += gn[i] * n[i];
-            }
-            const double sp2 = fmax(sp * sp, 1e-4);
-            res = sqrt(gF2 + g1 * g1 + g2 * g2 / sp2);
-            if (res < P.tol && fabs(dJ) <= P.det_tol) {
-                converged = true;
+                newton = true;
                 break;
             }
-            if (nsw >= P.max_sweeps) break;
-            nsw += 1;
-            if (fabs(dJ) > P.det_tol && res <= fmax(P.tol, 0.25 * gam * fabs(dJ))) {
-                pp += gam * dJ;
-                continue;
-            }
+            if (!newton) break;
+            ++it;
             const double phi0 = phiJ3(Fl, n, n0l, P, pp, D, ffl, nkl);
             // angle-block and cross-term ingredients (lce.py:807-882)
             double ua[3], ub[3];
@@ -704,7 +734,7 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
 #undef AS
 #pragma unroll
                 for (int a = 0; a < 11; ++a) S[(121 + a) * T] = rhs[a];
-                if (gauss_smem11(S, T, dv)) {
+                if (gauss_smem11<T>(S, dv)) {
                     gd = 0.0;
 #pragma unroll
                     for (int a = 0; a < 11; ++a) gd -= rhs[a] * dv[a];
