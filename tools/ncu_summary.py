@@ -18,7 +18,7 @@ from collections import defaultdict
 
 STAGE_OF = [("k_descent", "local"), ("k_mr2d", "local"), ("k_lce", "local"),
             ("k_update_local", "fused"), ("k_row_fwd", "row_fwd"), ("k_row_inv", "row_inv"),
-            ("k_grad", "grad"), ("k_colp<", None), ("k_col<", None)]
+            ("k_grad", "grad"), ("k_res_march", "grad"), ("k_colp<", None), ("k_col<", None)]
 METRICS = {
     "gpu__time_duration.sum": "duration",
     "dram__bytes_read.sum": "dram_read",
@@ -69,6 +69,7 @@ def load_raw(rep):
 def load_launches(path):
     per = defaultdict(float)
     cnt = defaultdict(int)
+    other = defaultdict(float)
     with open(path) as f:
         txt = f.read()
     start = txt.find('"ID"')
@@ -80,8 +81,12 @@ def load_launches(path):
         if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
             continue
         st = stage_of(r[ki], 0)
-        per[st] += float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1.0)
+        v = float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1.0)
+        per[st] += v
         cnt[st] += 1
+        if st == "other":
+            other[r[ki].split("(")[0].split("<")[0].replace("void ", "").strip()] += v
+    load_launches.other = other
     return per, cnt
 
 
@@ -117,6 +122,13 @@ def main():
                   "|---|---|---|---|"]
         for st, v in sorted(per.items(), key=lambda x: -x[1]):
             lines.append(f"| {st} | {cnt[st]} | {v * 1e6:.1f} | {v / tot:.3f} |")
+        oth = getattr(load_launches, "other", {})
+        if oth:
+            lines += ["", "`other` = kernels outside the iteration (host-transfer AoS/SoA transposes of "
+                      "setup and of the e2e leg, det checks, field sums):", "",
+                      "| kernel | total us |", "|---|---|"]
+            for k, v in sorted(oth.items(), key=lambda x: -x[1])[:8]:
+                lines.append(f"| `{k}` | {v * 1e6:.1f} |")
     with open(prefix + "_ncu_summary.md", "w") as f:
         f.write("\n".join(lines) + "\n")
     tpath = os.path.join(os.path.dirname(prefix), "ncu_traffic.json")
