@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <stdarg.h>
 
+#include <atomic>
+#include <condition_variable>
 #include <mutex>
 #include <sched.h>
 #include <string.h>
@@ -213,7 +215,7 @@ static int ensure_field(mm_ctx *ctx, double **slot, int ncomp) {
 // the other half (multi-threaded: both the memcpy bandwidth and the page
 // faults of freshly allocated destinations scale with threads).  Pinned
 // caller memory is DMA'd directly.
-static const size_t kChunkBytes = (size_t)48 << 20;
+static const size_t kChunkBytes = (size_t)128 << 20;
 
 struct PinnedPool {
     std::mutex mu;
@@ -233,22 +235,76 @@ static int host_threads() {
     return nt;
 }
 
+// Persistent host copy pool (created on first use, never torn down): a copy
+// is cut into one contiguous part per thread, taken from an atomic counter by
+// the workers and the calling thread, so per-chunk thread start-up does not
+// eat into the overlap with the DMA of the next chunk.
+class CopyPool {
+  public:
+    explicit CopyPool(int nworkers) {
+        for (int i = 0; i < nworkers; ++i) std::thread([this] { worker(); }).detach();
+    }
+    void copy(void *dst, const void *src, size_t bytes, int nparts) {
+        // one contiguous part per thread: each thread faults in its own range
+        const size_t part = (((bytes + nparts - 1) / nparts) + 4095) & ~(size_t)4095;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            dst_ = (char *)dst;
+            src_ = (const char *)src;
+            bytes_ = bytes;
+            part_ = part;
+            njobs_ = (int)((bytes + part - 1) / part);
+            next_.store(0);
+            remaining_.store(njobs_);
+            ++gen_;
+        }
+        cv_.notify_all();
+        run();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [this] { return remaining_.load() == 0; });
+    }
+
+  private:
+    void run() {
+        int j;
+        while ((j = next_.fetch_add(1)) < njobs_) {
+            const size_t off = (size_t)j * part_;
+            memcpy(dst_ + off, src_ + off, std::min(part_, bytes_ - off));
+            if (remaining_.fetch_sub(1) == 1) {
+                std::lock_guard<std::mutex> lk(mu_);
+                done_.notify_all();
+            }
+        }
+    }
+    void worker() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+            }
+            run();
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_, done_;
+    char *dst_ = nullptr;
+    const char *src_ = nullptr;
+    size_t bytes_ = 0, part_ = 1;
+    int njobs_ = 0;
+    std::atomic<int> next_{0}, remaining_{0};
+    uint64_t gen_ = 0;
+};
+
 static void par_memcpy(void *dst, const void *src, size_t bytes) {
     const int nt = host_threads();
     if (nt <= 1 || bytes < ((size_t)4 << 20)) {
         memcpy(dst, src, bytes);
         return;
     }
-    const size_t per = ((bytes + nt - 1) / nt + 4095) & ~(size_t)4095;
-    std::vector<std::thread> th;
-    for (int t = 1; t < nt; ++t) {
-        const size_t off = per * t;
-        if (off >= bytes) break;
-        const size_t len = std::min(per, bytes - off);
-        th.emplace_back([=] { memcpy((char *)dst + off, (const char *)src + off, len); });
-    }
-    memcpy(dst, src, std::min(per, bytes));
-    for (auto &x : th) x.join();
+    static CopyPool *pool = new CopyPool(nt - 1);  // intentionally never destroyed
+    pool->copy(dst, src, bytes, nt);
 }
 
 static int ensure_stage(mm_ctx *ctx, int64_t ndoubles) {
