@@ -219,9 +219,21 @@ int mm_update_and_sweep(mm_ctx *ctx, int material, double rho_next, double tol,
  *   HALO_U, [exchange], UPDATE (sums[0..10] = |dG|^2, |misfit|^2, sum lam)
  * Buffers: MM_SLAB_BUF_SEND / RECV  nranks * 3 * (n/nranks)^2 * pitch complex,
  * [peer][c][i0l][i1l][k2]; HALO_*  3 * n^2 doubles [c][i1][i2]. */
+/* Peer-memory variant of the two transposes (no separate all-to-all):
+ * MM_SLAB_FWD_PUSH is MM_SLAB_FWD whose axis-1 FFT stores each output tile
+ * straight into the RECV buffer of the rank that owns it (block `rank` of
+ * that buffer), and MM_SLAB_SOLVE_PUSH is MM_SLAB_SOLVE storing each solved
+ * tile into the SEND buffer of its source rank -- the transfer overlaps the
+ * FFT tile by tile over NVLink/NVSwitch peer stores.  Sequence:
+ *   HALO_T, [exchange], FWD_PUSH, [barrier], SOLVE_PUSH, [barrier], INV, ...
+ * The barriers are host-side (every rank's step has returned, i.e. its
+ * kernels completed); no kernel waits on another rank.  Peer buffers are
+ * registered with mm_slab_set_peers (device pointers usable in this process,
+ * e.g. ranks sharing one process) or mm_slab_open_peers (CUDA IPC handles of
+ * the other processes' buffers, from mm_slab_ipc_handle). */
 enum mm_slab_step {
     MM_SLAB_HALO_T = 0, MM_SLAB_FWD = 1, MM_SLAB_SOLVE = 2, MM_SLAB_INV = 3, MM_SLAB_HALO_U = 4,
-    MM_SLAB_UPDATE = 5, MM_SLAB_GRAD = 6
+    MM_SLAB_UPDATE = 5, MM_SLAB_GRAD = 6, MM_SLAB_FWD_PUSH = 7, MM_SLAB_SOLVE_PUSH = 8
 };
 enum mm_slab_buffer {
     MM_SLAB_BUF_SEND = 0, MM_SLAB_BUF_RECV = 1, MM_SLAB_BUF_HALO_OUT_LO = 2,
@@ -230,6 +242,14 @@ enum mm_slab_buffer {
 int mm_create_slab(int n, double length, int nranks, int rank, int device, mm_ctx **out);
 int mm_slab_buffer(mm_ctx *ctx, int which, void **dev_ptr, int64_t *nbytes);
 int mm_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, double *sums);
+/* which = MM_SLAB_BUF_RECV (targets of FWD_PUSH) or MM_SLAB_BUF_SEND (targets
+ * of SOLVE_PUSH).  ptrs[q] = rank q's buffer, P = nranks. */
+int mm_slab_set_peers(mm_ctx *ctx, int which, void *const *ptrs, int P);
+/* 64-byte CUDA IPC handle of this rank's SEND or RECV buffer. */
+int mm_slab_ipc_handle(mm_ctx *ctx, int which, void *handle_out);
+/* handles = P consecutive 64-byte handles (entry `rank` is ignored: the own
+ * buffer is used); opened with cudaIpcOpenMemHandle, closed by mm_destroy. */
+int mm_slab_open_peers(mm_ctx *ctx, int which, const void *handles, int P);
 
 /* Options.  MM_OPT_IMPLICIT_GRAD (default 0): after a fused projection keep
  * grad_u implicitly as u_mean + D u_tilde instead of storing the 9-component

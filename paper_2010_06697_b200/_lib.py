@@ -41,10 +41,12 @@ EXPORTS = (
     "mm_profile_enable", "mm_profile_read", "mm_frank_stencil", "mm_set_option",
     "mm_project_residuals", "mm_update_multiplier", "mm_update_and_sweep",
     "mm_create_slab", "mm_slab_buffer", "mm_slab_step", "mm_add_field",
-    "mm_equilibrium_residual", "mm_selftest_log",
+    "mm_equilibrium_residual", "mm_selftest_log", "mm_slab_set_peers", "mm_slab_ipc_handle",
+    "mm_slab_open_peers",
 )
 
 SLAB_HALO_T, SLAB_FWD, SLAB_SOLVE, SLAB_INV, SLAB_HALO_U, SLAB_UPDATE, SLAB_GRAD = range(7)
+SLAB_FWD_PUSH, SLAB_SOLVE_PUSH = 7, 8
 SLAB_BUF_SEND, SLAB_BUF_RECV, SLAB_BUF_HALO_OUT_LO, SLAB_BUF_HALO_OUT_HI = range(4)
 SLAB_BUF_HALO_IN_LO, SLAB_BUF_HALO_IN_HI = 4, 5
 
@@ -146,6 +148,9 @@ def load_library():
             "mm_add_field": ([P, I, P, I64], I),
             "mm_equilibrium_residual": ([P, I, D, ctypes.POINTER(D)], I),
             "mm_selftest_log": ([P, P, P, I64], I),
+            "mm_slab_set_peers": ([P, I, P, I], I),
+            "mm_slab_ipc_handle": ([P, I, P], I),
+            "mm_slab_open_peers": ([P, I, P, I], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -352,6 +357,20 @@ class Context:
         self.check(self.lib.mm_slab_buffer(self.h, int(which), ctypes.byref(ptr),
                                            ctypes.byref(nbytes)))
         return ptr.value, nbytes.value
+
+    def slab_set_peers(self, which, ptrs):
+        arr = (ctypes.c_void_p * len(ptrs))(*[int(p) for p in ptrs])
+        self.check(self.lib.mm_slab_set_peers(self.h, int(which), arr, len(ptrs)))
+
+    def slab_ipc_handle(self, which):
+        buf = ctypes.create_string_buffer(64)
+        self.check(self.lib.mm_slab_ipc_handle(self.h, int(which), buf))
+        return buf.raw
+
+    def slab_open_peers(self, which, handles):
+        blob = b"".join(handles)
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        self.check(self.lib.mm_slab_open_peers(self.h, int(which), buf, len(handles)))
 
     def slab_step(self, step, rho, u_mean=None):
         sums = np.zeros(11)

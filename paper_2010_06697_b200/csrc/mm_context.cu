@@ -561,8 +561,10 @@ int mm_create_slab(int n, double length, int nranks, int rank, int device, mm_ct
     TRY(mm_alloc(ctx, (void **)&ctx->Ut, sizeof(double) * 3 * M));
     TRY(mm_alloc(ctx, (void **)&ctx->spec, sizeof(double2) * 3 * ctx->nrows * ctx->P));
     const int64_t bufc = (int64_t)nranks * 3 * nl * nl * ctx->P;
-    TRY(mm_alloc(ctx, (void **)&ctx->sendbuf, sizeof(double2) * bufc));
-    TRY(mm_alloc(ctx, (void **)&ctx->recvbuf, sizeof(double2) * bufc));
+    // exchange buffers by plain cudaMalloc: CUDA IPC exports need it
+    MM_CUDA(ctx, cudaMalloc((void **)&ctx->sendbuf, sizeof(double2) * bufc));
+    MM_CUDA(ctx, cudaMalloc((void **)&ctx->recvbuf, sizeof(double2) * bufc));
+    ctx->bytes += 2 * (int64_t)sizeof(double2) * bufc;
     TRY(mm_alloc(ctx, (void **)&ctx->halo_in_lo, sizeof(double) * 3 * nn));
     TRY(mm_alloc(ctx, (void **)&ctx->halo_in_hi, sizeof(double) * 3 * nn));
     TRY(mm_alloc(ctx, (void **)&ctx->halo_out_lo, sizeof(double) * 3 * nn));
@@ -617,6 +619,63 @@ int mm_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, double
     return mm_run_slab_step(ctx, step, rho, u_mean, sums);
 }
 
+static int peer_table(mm_ctx *ctx, int which, double2 ****slot) {
+    if (!ctx->slab_mode) return mm_fail(ctx, MM_ERR_CONFIG, "not a slab context");
+    if (which == MM_SLAB_BUF_RECV) *slot = &ctx->peer_recv;
+    else if (which == MM_SLAB_BUF_SEND) *slot = &ctx->peer_send;
+    else return mm_fail(ctx, MM_ERR_PARAM, "peer buffers are SEND or RECV, got %d", which);
+    if (!**slot) {
+        int rc = mm_alloc(ctx, (void **)*slot, sizeof(double2 *) * ctx->slab_P);
+        if (rc) return rc;
+    }
+    return MM_OK;
+}
+
+int mm_slab_set_peers(mm_ctx *ctx, int which, void *const *ptrs, int P) {
+    if (!ctx || !ptrs) return MM_ERR_PARAM;
+    if (P != ctx->slab_P) return mm_fail(ctx, MM_ERR_CONFIG, "expected %d peers, got %d", ctx->slab_P, P);
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    double2 ***slot;
+    int rc = peer_table(ctx, which, &slot);
+    if (rc) return rc;
+    MM_CUDA(ctx, cudaMemcpy(*slot, ptrs, sizeof(void *) * P, cudaMemcpyHostToDevice));
+    return MM_OK;
+}
+
+int mm_slab_ipc_handle(mm_ctx *ctx, int which, void *handle_out) {
+    if (!ctx || !handle_out) return MM_ERR_PARAM;
+    if (!ctx->slab_mode) return mm_fail(ctx, MM_ERR_CONFIG, "not a slab context");
+    void *buf = which == MM_SLAB_BUF_RECV ? (void *)ctx->recvbuf
+              : which == MM_SLAB_BUF_SEND ? (void *)ctx->sendbuf : nullptr;
+    if (!buf) return mm_fail(ctx, MM_ERR_PARAM, "peer buffers are SEND or RECV, got %d", which);
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    cudaIpcMemHandle_t h;
+    MM_CUDA(ctx, cudaIpcGetMemHandle(&h, buf));
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    memcpy(handle_out, &h, 64);
+    return MM_OK;
+}
+
+int mm_slab_open_peers(mm_ctx *ctx, int which, const void *handles, int P) {
+    if (!ctx || !handles) return MM_ERR_PARAM;
+    if (P != ctx->slab_P) return mm_fail(ctx, MM_ERR_CONFIG, "expected %d peers, got %d", ctx->slab_P, P);
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    std::vector<void *> ptrs(P);
+    for (int q = 0; q < P; ++q) {
+        if (q == ctx->slab_rank) {
+            ptrs[q] = which == MM_SLAB_BUF_RECV ? (void *)ctx->recvbuf : (void *)ctx->sendbuf;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, (const char *)handles + 64 * q, 64);
+        void *p = nullptr;
+        MM_CUDA(ctx, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        ctx->ipc_opened.push_back(p);
+        ptrs[q] = p;
+    }
+    return mm_slab_set_peers(ctx, which, ptrs.data(), P);
+}
+
 int mm_create_points(int dim, int64_t npts, int device, mm_ctx **out) {
     if (!out) return MM_ERR_PARAM;
     *out = nullptr;
@@ -657,9 +716,12 @@ void mm_destroy(mm_ctx *ctx) {
                       ctx->halo_in_hi, ctx->halo_out_lo, ctx->halo_out_hi, ctx->sym, ctx->partials, ctx->red_out,
                       ctx->res, ctx->tstate, ctx->stage, ctx->Pbuf};
     for (double *p : ptrs) mm_free(ctx, p);
-    void *others[] = {ctx->spec, ctx->sendbuf, ctx->recvbuf, ctx->tw_full, ctx->tw_half,
-                      ctx->tw_r2c, ctx->red_count, ctx->nsw, ctx->ok, ctx->freestate};
+    void *others[] = {ctx->spec, ctx->tw_full, ctx->tw_half, ctx->tw_r2c, ctx->red_count,
+                      ctx->nsw, ctx->ok, ctx->freestate, ctx->peer_recv, ctx->peer_send};
     for (void *p : others) mm_free(ctx, p);
+    for (void *p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
+    if (ctx->sendbuf) cudaFree(ctx->sendbuf);
+    if (ctx->recvbuf) cudaFree(ctx->recvbuf);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->host_out) cudaFreeHost(ctx->host_out);
     if (ctx->xfer_ev[0]) cudaEventDestroy(ctx->xfer_ev[0]);

@@ -87,6 +87,9 @@ struct mm_ctx {
     // slab decomposition (3D, split along axis 0)
     bool slab_mode = false;
     int slab_P = 1, slab_rank = 0, slab_nl = 0;
+    // peer-memory transposes: device tables of every rank's RECV / SEND buffer
+    double2 **peer_recv = nullptr, **peer_send = nullptr;
+    std::vector<void *> ipc_opened;  // closed at destroy
     double2 *sendbuf = nullptr, *recvbuf = nullptr;
     double *halo_in_lo = nullptr, *halo_in_hi = nullptr, *halo_out_lo = nullptr,
            *halo_out_hi = nullptr;    // F verified admissible since the last upload

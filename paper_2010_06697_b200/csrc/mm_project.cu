@@ -1402,6 +1402,10 @@ struct SlabCol {
     int64_t s_sq, s_es, s_os, s_cs;
     int64_t d_sq, d_es, d_os, d_cs;
     int outer_off;  // global index of outer line 0 along axis 1 (solve symbols)
+    // peer stores: block q of the destination lives in peers[q] + peer_off
+    // (d_sq unused); nullptr = local destination
+    double2 *const *peers;
+    int64_t peer_off;
 };
 
 template <int N1, int N2, int MODE>
@@ -1466,6 +1470,17 @@ k_col_slab(ColGeom g, SlabCol sc, const double2 *__restrict__ tw) {
         }
         __syncthreads();
         line_transform<N1, N2, TK, true>(buf, scr, N, tw);
+    }
+    if (sc.peers) {
+        // fused transpose: each element goes straight to the rank that owns
+        // it (NVLink peer store); line element n belongs to block n / blk_d
+        const int64_t loc = comp * sc.d_cs + outer * sc.d_os + k0 + sc.peer_off;
+        for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
+            const int n = w / TK, c = w - n * TK;
+            if (k0 + c < g.ncol)
+                sc.peers[n / sc.blk_d][loc + (n % sc.blk_d) * sc.d_es + c] = buf[n * LD + c];
+        }
+        return;
     }
     for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
         const int n = w / TK, c = w - n * TK;
@@ -1598,12 +1613,18 @@ int mm_run_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, do
             MM_LAUNCH_CHECK(ctx);
             return mm_synchronize(ctx);
         }
-        case MM_SLAB_FWD: {
+        case MM_SLAB_FWD:
+        case MM_SLAB_FWD_PUSH: {
+            const bool push = step == MM_SLAB_FWD_PUSH;
+            if (push && !ctx->peer_recv)
+                return mm_fail(ctx, MM_ERR_CONFIG, "FWD_PUSH: peer RECV buffers were never set");
             {
                 StageScope ss(ctx, MM_STAGE_ROW_FWD);
                 if ((rc = run_rows(ctx, true, rho))) return rc;
             }
             SlabCol sc;
+            sc.peers = push ? ctx->peer_recv : nullptr;
+            sc.peer_off = (int64_t)ctx->slab_rank * blk;
             sc.src = ctx->spec;
             sc.dst = ctx->sendbuf;
             sc.blk_s = n;
@@ -1615,9 +1636,15 @@ int mm_run_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, do
             if ((rc = run_col_slab<COL_FWD>(ctx, g, sc, nl))) return rc;
             return mm_synchronize(ctx);
         }
-        case MM_SLAB_SOLVE: {
+        case MM_SLAB_SOLVE:
+        case MM_SLAB_SOLVE_PUSH: {
             // recv [s][c][i0l][i1l][k2]: line along i0 = s * nl + i0l, outer = i1l
+            const bool push = step == MM_SLAB_SOLVE_PUSH;
+            if (push && !ctx->peer_send)
+                return mm_fail(ctx, MM_ERR_CONFIG, "SOLVE_PUSH: peer SEND buffers were never set");
             SlabCol sc;
+            sc.peers = push ? ctx->peer_send : nullptr;
+            sc.peer_off = (int64_t)ctx->slab_rank * blk;
             sc.src = ctx->recvbuf;
             sc.dst = ctx->recvbuf;
             sc.blk_s = sc.blk_d = nl;
@@ -1632,6 +1659,8 @@ int mm_run_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, do
         }
         case MM_SLAB_INV: {
             SlabCol sc;
+            sc.peers = nullptr;
+            sc.peer_off = 0;
             sc.src = ctx->sendbuf;
             sc.dst = ctx->spec;
             sc.blk_s = nl;

@@ -22,6 +22,16 @@ provide:
 Sums are reduced by all-gathering each rank's fixed-order partials and adding
 them in rank order, so results do not depend on the reduction tree.
 
+``exchange="push"`` replaces T1 and T2 by peer-memory stores fused into the
+FFT kernels (mm_slab_step FWD_PUSH / SOLVE_PUSH): B writes every output tile
+straight into the receive buffer of the rank that owns it, C writes every
+solved tile back into its source rank's send buffer, so the transpose
+traffic overlaps the transforms tile by tile over NVLink / NVSwitch.  The
+peer buffers are mapped once (CUDA IPC handles exchanged through the
+communicator; raw pointers when the ranks share a process) and a host
+barrier after each step is the only synchronisation -- no kernel waits on
+another rank.
+
 ``SlabProjector`` is the orchestration; a *backend* supplies the per-rank
 compute.  ``DeviceSlabBackend`` calls libmm_admm (CUDA); ``NumpySlabBackend``
 restates the same per-rank steps on host arrays with identical buffer
@@ -68,18 +78,35 @@ class SlabLayout:
 
 
 class TorchComm:
-    """Collectives over torch.distributed (NCCL on GPU tensors, gloo on CPU)."""
+    """Collectives over torch.distributed (NCCL on GPU tensors, gloo on CPU).
+
+    With the gloo backend and device buffers (``cpu_stage``), halo planes
+    and partial sums are staged through host memory."""
 
     def __init__(self, dist, device=None):
         self.dist = dist
         self.device = device
         self.P = dist.get_world_size()
         self.rank = dist.get_rank()
+        self.cpu_stage = dist.get_backend() == "gloo"
 
     def _t(self, a):
         import torch
         t = torch.as_tensor(a)
+        if self.cpu_stage:
+            return t.cpu()
         return t.to(self.device) if self.device is not None else t
+
+    def barrier(self):
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+        self.dist.barrier()
+
+    def gather_objects(self, obj):
+        out = [None] * self.P
+        self.dist.all_gather_object(out, obj)
+        return out
 
     def exchange_halos(self, lo_out, hi_out, lo_in=None, hi_in=None):
         """Send my first plane to the lower neighbour and my last plane to the
@@ -95,10 +122,15 @@ class TorchComm:
             lo_in.copy_(hi_out_t)
             hi_in.copy_(lo_out_t)
             return lo_in, hi_in
+        lo_rx = torch.empty_like(lo_out_t) if self.cpu_stage else lo_in
+        hi_rx = torch.empty_like(hi_out_t) if self.cpu_stage else hi_in
         ops = [dist.P2POp(dist.isend, lo_out_t, lo_nb), dist.P2POp(dist.isend, hi_out_t, hi_nb),
-               dist.P2POp(dist.irecv, hi_in, hi_nb), dist.P2POp(dist.irecv, lo_in, lo_nb)]
+               dist.P2POp(dist.irecv, hi_rx, hi_nb), dist.P2POp(dist.irecv, lo_rx, lo_nb)]
         for r in dist.batch_isend_irecv(ops):
             r.wait()
+        if self.cpu_stage:
+            lo_in.copy_(lo_rx)
+            hi_in.copy_(hi_rx)
         return lo_in, hi_in
 
     def all_to_all(self, send, out=None):
@@ -116,7 +148,7 @@ class TorchComm:
         """Sum (or max) per slot over ranks in rank order (deterministic)."""
         import torch
         v = torch.as_tensor(np.asarray(vec, dtype=np.float64))
-        if self.device is not None:
+        if self.device is not None and not self.cpu_stage:
             v = v.to(self.device)
         if self.P == 1:
             return np.asarray(vec, dtype=np.float64)
@@ -154,12 +186,19 @@ class SlabProjector:
         hin = getattr(be, "halo_in", lambda: (None, None))()
         lo, hi = be.boundary_T(rho)                      # A: halos of T_c0
         lo_in, hi_in = comm.exchange_halos(lo, hi, *hin)
-        be.row_fwd(rho, lo_in, hi_in)                    # A
-        send = be.col_fwd_to_send()                      # B
-        recv = comm.all_to_all(send, getattr(be, "recv_buffer", lambda: None)())  # T1
-        back = be.col_solve(recv)                        # C
-        ret = comm.all_to_all(back, getattr(be, "send_buffer", lambda: None)())   # T2
-        be.col_inv_from_send(ret)                        # D
+        if getattr(be, "push", False):
+            be.row_fwd_push(rho, lo_in, hi_in)           # A + B, tiles stored into peers
+            comm.barrier()                               # every rank's tiles have landed
+            be.col_solve_push()                          # C, tiles stored back into sources
+            comm.barrier()
+            be.col_inv_from_send(None)                   # D
+        else:
+            be.row_fwd(rho, lo_in, hi_in)                # A
+            send = be.col_fwd_to_send()                  # B
+            recv = comm.all_to_all(send, getattr(be, "recv_buffer", lambda: None)())  # T1
+            back = be.col_solve(recv)                    # C
+            ret = comm.all_to_all(back, getattr(be, "send_buffer", lambda: None)())   # T2
+            be.col_inv_from_send(ret)                    # D
         be.row_inv()                                     # E
         ulo, uhi = be.boundary_u()                       # F: halos of u
         ulo_in, uhi_in = comm.exchange_halos(ulo, uhi, *hin)
@@ -306,6 +345,17 @@ class ThreadComm:
         self._done()
         return out
 
+    def barrier(self):
+        import torch
+        torch.cuda.synchronize()
+        self.sh["barrier"].wait()
+
+    def gather_objects(self, obj):
+        self._post("obj", obj)
+        out = [self.sh["slots"][("obj", r)] for r in range(self.P)]
+        self._done()
+        return out
+
     def ordered_sum(self, vec, ops=None):
         self._post("sum", np.asarray(vec, dtype=np.float64).copy())
         arr = [self.sh["slots"][("sum", r)] for r in range(self.P)]
@@ -344,6 +394,31 @@ class DeviceSlabBackend:
         self._hil = view(_lib.SLAB_BUF_HALO_IN_LO, None)
         self._hih = view(_lib.SLAB_BUF_HALO_IN_HI, None)
 
+    push = False
+
+    def enable_push(self, comm, same_process):
+        """Map every rank's RECV and SEND buffers into this context: raw
+        device pointers when all ranks live in this process, CUDA IPC
+        handles otherwise."""
+        lib, ctx = self._lib, self.ctx
+        for which in (lib.SLAB_BUF_RECV, lib.SLAB_BUF_SEND):
+            if same_process:
+                ptrs = comm.gather_objects(ctx.slab_buffer(which)[0])
+                ctx.slab_set_peers(which, ptrs)
+            else:
+                handles = comm.gather_objects(ctx.slab_ipc_handle(which))
+                ctx.slab_open_peers(which, handles)
+        comm.barrier()
+        self.push = True
+
+    def row_fwd_push(self, rho, lo_in, hi_in):
+        self._take(self._hil, lo_in)
+        self._take(self._hih, hi_in)
+        self.ctx.slab_step(self._lib.SLAB_FWD_PUSH, rho)
+
+    def col_solve_push(self):
+        self.ctx.slab_step(self._lib.SLAB_SOLVE_PUSH, self._rho)
+
     def halo_in(self):
         return self._hil, self._hih
 
@@ -375,7 +450,8 @@ class DeviceSlabBackend:
         return self._recv
 
     def col_inv_from_send(self, ret):
-        self._take(self._send, ret)
+        if ret is not None:
+            self._take(self._send, ret)
         self.ctx.slab_step(self._lib.SLAB_INV, self._rho)
 
     def row_inv(self):
@@ -405,7 +481,7 @@ class SlabSolver:
     """
 
     def __init__(self, layout: SlabLayout, model, bc, params, policy, comm, F, grad_u, lam,
-                 rho=None, device=None):
+                 rho=None, device=None, exchange="collective"):
         from . import _lib
         from .grid import Grid, axis_symbol_tables
         self.lay, self.model, self.bc, self.params, self.policy, self.comm = (
@@ -426,6 +502,10 @@ class SlabSolver:
         self.ctx.upload(_lib.FIELD_G, grad_u)
         self.ctx.upload(_lib.FIELD_LAM, lam)
         self.backend = DeviceSlabBackend(self.ctx)
+        if exchange == "push":
+            self.backend.enable_push(comm, same_process=isinstance(comm, ThreadComm))
+        elif exchange != "collective":
+            raise ValueError(f"exchange must be 'collective' or 'push', got {exchange!r}")
         self.proj = SlabProjector(layout, self.backend, comm)
         self.rho = float(params.rho_init if params.rho_init is not None else model.mu_rep)
         if rho is not None:

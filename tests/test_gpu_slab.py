@@ -36,8 +36,10 @@ def _problem(n):
     return grid, mu, kap, bc, F, G, lam
 
 
-@pytest.mark.parametrize("n,P,K", [(16, 2, 6), (32, 4, 6), (32, 1, 4)])
-def test_slab_solver_matches_single_gpu(n, P, K):
+@pytest.mark.parametrize("n,P,K,exchange", [(16, 2, 6, "collective"), (32, 4, 6, "collective"),
+                                            (32, 1, 4, "collective"), (16, 2, 6, "push"),
+                                            (32, 4, 6, "push")])
+def test_slab_solver_matches_single_gpu(n, P, K, exchange):
     from paper_2010_06697_b200.slab import SlabLayout, SlabSolver, ThreadComm
     grid, mu, kap, bc, F, G, lam = _problem(n)
     params = mm.SolverParams(r_p_tol=1e-300, r_d_tol=1e-300, max_outer=K)
@@ -60,7 +62,7 @@ def test_slab_solver_matches_single_gpu(n, P, K):
             mloc = mm.MooneyRivlin(mu[pts], kap[pts], dim=3, mu_rep=1.0)
             mloc._phi_cache = ((id(mloc.mu), id(mloc.kappa)), float(mu.max() + kap.max()))
             sv = SlabSolver(lay, mloc, bc, params, pol, ThreadComm(shared, r), F[sl], G[sl],
-                            lam[sl])
+                            lam[sl], exchange=exchange)
             sv.solve()
             out[r] = (sv.fields(), sv.history, sv.total_sweeps)
         except Exception as e:  # pragma: no cover - surfaced below
@@ -81,3 +83,66 @@ def test_slab_solver_matches_single_gpu(n, P, K):
     h_one = np.array([r[:5] for r in st.history])
     np.testing.assert_allclose(h_slab, h_one, rtol=1e-10, atol=1e-14)
     assert out[0][2] == st.total_sweeps
+
+
+def _ipc_rank(rank, P, n, K, port, out_dir):
+    """One process of the multi-process push test (same GPU, CUDA IPC)."""
+    import os
+    import torch
+    import torch.distributed as dist
+    import paper_2010_06697_b200 as mm_
+    from paper_2010_06697_b200.slab import SlabLayout, SlabSolver, TorchComm
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=P)
+    try:
+        torch.cuda.set_device(0)
+        grid, mu, kap, bc, F, G, lam = _problem(n)
+        lay = SlabLayout(n, P, rank, 0.5)
+        sl = lay.plane_slice()
+        pts = slice(rank * lay.npts_local, (rank + 1) * lay.npts_local)
+        mloc = mm_.MooneyRivlin(mu[pts], kap[pts], dim=3, mu_rep=1.0)
+        params = mm_.SolverParams(r_p_tol=1e-300, r_d_tol=1e-300, max_outer=K)
+        sv = SlabSolver(lay, mloc, bc, params, mm_.RatioToDual(0.3), TorchComm(dist, "cuda:0"),
+                        F[sl], G[sl], lam[sl], exchange="push")
+        sv.solve()
+        f = sv.fields()
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), hist=np.array(
+            [r[:5] for r in sv.history]), sweeps=sv.total_sweeps, **f)
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_push_exchange_across_processes_with_ipc(tmp_path):
+    """Two processes on one GPU map each other's exchange buffers with CUDA
+    IPC handles and run the fused (peer-store) transposes; the result equals
+    the single-context solver.  Synchronisation is host-side (gloo barrier),
+    so no kernel waits on the other process."""
+    import socket
+    import torch.multiprocessing as tmp
+    n, P, K = 16, 2, 5
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = tmp.get_context("spawn")
+    procs = [ctx.Process(target=_ipc_rank, args=(r, P, n, K, port, str(tmp_path)))
+             for r in range(P)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    grid, mu, kap, bc, F, G, lam = _problem(n)
+    params = mm.SolverParams(r_p_tol=1e-300, r_d_tol=1e-300, max_outer=K)
+    model = mm.MooneyRivlin(mu, kap, dim=3, mu_rep=1.0)
+    st = mm.ADMMState(u_mean=bc.value.copy(), u_tilde=np.zeros(grid.shape + (3,)), grad_u=G,
+                      F=F, lam=lam, internal={}, rho=1.0)
+    st, _ = mm.solve(grid, model, bc, params, policy=mm.RatioToDual(0.3), state=st,
+                     raise_on_max=False)
+    outs = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(P)]
+    for k in ("F", "lam", "grad_u", "u_tilde"):
+        full = np.concatenate([o[k] for o in outs], axis=0)
+        assert rel_l2(full, getattr(st, k)) < 1e-12, k
+    np.testing.assert_allclose(outs[0]["hist"], np.array([r[:5] for r in st.history]),
+                               rtol=1e-10, atol=1e-14)
+
