@@ -276,6 +276,22 @@ int mm_stencil(mm_ctx *ctx, int op);
  * stress(). */
 int mm_equilibrium_residual(mm_ctx *ctx, int material, double dt, double *out);
 
+/* Bloch-wave stability (stability.py:171-289): smallest eigenvalue of the
+ * shifted acoustic operator at one multiplicity, by the splitting iteration.
+ * Setup (per solve): Minv = (L + rho I)^-1 and L per point (npts x D x D,
+ * D = d^2, row-major blocks), shift = xi + omega per point (npts x d), |b|^2
+ * and the live mask per point (full spectrum, the reference's
+ * bloch_symbols), rho, target = npts^2.  start: p (npts x d complex,
+ * re/im interleaved) -> p_hat = FFT(p) masked and normalised, g = 0.
+ * iterate: up to max_iter iterations; out = {beta, primal, iterations,
+ * converged, diverged}.  mode: p = IFFT(p_hat) as complex AoS. */
+int mm_bloch_setup(mm_ctx *ctx, const double *Minv, const double *Lmat, const double *shift,
+                   const double *bsq, const uint8_t *live, double rho, double target);
+int mm_bloch_start(mm_ctx *ctx, const double *p);
+int mm_bloch_iterate(mm_ctx *ctx, int max_iter, double tol_beta, double tol_primal,
+                     double floor_, double mu_rep, double *out);
+int mm_bloch_mode(mm_ctx *ctx, double *p_out);
+
 /* Test hook: y[i] = the device natural logarithm the Mooney-Rivlin objective
  * uses (table-driven, csrc/mm_local.cu log_pos) for host arrays x, y. */
 int mm_selftest_log(mm_ctx *ctx, const double *x, double *y, int64_t n);

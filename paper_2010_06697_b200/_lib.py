@@ -42,7 +42,8 @@ EXPORTS = (
     "mm_project_residuals", "mm_update_multiplier", "mm_update_and_sweep",
     "mm_create_slab", "mm_slab_buffer", "mm_slab_step", "mm_add_field",
     "mm_equilibrium_residual", "mm_selftest_log", "mm_slab_set_peers", "mm_slab_ipc_handle",
-    "mm_slab_open_peers",
+    "mm_slab_open_peers", "mm_bloch_setup", "mm_bloch_start", "mm_bloch_iterate",
+    "mm_bloch_mode",
 )
 
 SLAB_HALO_T, SLAB_FWD, SLAB_SOLVE, SLAB_INV, SLAB_HALO_U, SLAB_UPDATE, SLAB_GRAD = range(7)
@@ -151,6 +152,10 @@ def load_library():
             "mm_slab_set_peers": ([P, I, P, I], I),
             "mm_slab_ipc_handle": ([P, I, P], I),
             "mm_slab_open_peers": ([P, I, P, I], I),
+            "mm_bloch_setup": ([P, P, P, P, P, P, D, D], I),
+            "mm_bloch_start": ([P, P], I),
+            "mm_bloch_iterate": ([P, I, D, D, D, D, P], I),
+            "mm_bloch_mode": ([P, P], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -357,6 +362,32 @@ class Context:
         self.check(self.lib.mm_slab_buffer(self.h, int(which), ctypes.byref(ptr),
                                            ctypes.byref(nbytes)))
         return ptr.value, nbytes.value
+
+    # -- Bloch stability -----------------------------------------------------------
+    def bloch_setup(self, Minv, Lmat, shift, bsq, live, rho, target):
+        Minv = np.ascontiguousarray(Minv, dtype=np.float64)
+        Lmat = np.ascontiguousarray(Lmat, dtype=np.float64)
+        shift = np.ascontiguousarray(shift, dtype=np.float64)
+        bsq = np.ascontiguousarray(bsq, dtype=np.float64)
+        live = np.ascontiguousarray(live, dtype=np.uint8)
+        self.check(self.lib.mm_bloch_setup(self.h, _ptr(Minv), _ptr(Lmat), _ptr(shift),
+                                           _ptr(bsq), _ptr(live), float(rho), float(target)))
+
+    def bloch_start(self, p):
+        p = np.ascontiguousarray(p, dtype=np.complex128)
+        self.check(self.lib.mm_bloch_start(self.h, _ptr(p)))
+
+    def bloch_iterate(self, max_iter, tol_beta, tol_primal, floor, mu_rep):
+        out = np.zeros(5)
+        self.check(self.lib.mm_bloch_iterate(self.h, int(max_iter), float(tol_beta),
+                                             float(tol_primal), float(floor), float(mu_rep),
+                                             _ptr(out)))
+        return float(out[0]), float(out[1]), int(out[2]), bool(out[3]), bool(out[4])
+
+    def bloch_mode(self, shape):
+        out = np.empty(shape, dtype=np.complex128)
+        self.check(self.lib.mm_bloch_mode(self.h, _ptr(out)))
+        return out
 
     def slab_set_peers(self, which, ptrs):
         arr = (ctypes.c_void_p * len(ptrs))(*[int(p) for p in ptrs])

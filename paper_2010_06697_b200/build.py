@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libmm_admm.so")
-SOURCES = ["mm_context.cu", "mm_local.cu", "mm_project.cu", "mm_lce.cu"]
+SOURCES = ["mm_context.cu", "mm_local.cu", "mm_project.cu", "mm_lce.cu", "mm_bloch.cu"]
 # Files to build without FMA contraction (none: bit-for-bit agreement with the
 # reference's numba kernels is out of reach anyway, because glibc's sin/cos
 # are not correctly rounded and CUDA's differ from them by an ulp).

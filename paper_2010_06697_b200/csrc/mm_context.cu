@@ -710,6 +710,7 @@ void mm_destroy(mm_ctx *ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     mm_drain_timings(ctx);
     for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+    mm_bloch_free(ctx);
     double *ptrs[] = {ctx->F, ctx->G, ctx->Lam, ctx->Ut, ctx->prevF, ctx->modA, ctx->modB,
                       ctx->ang, ctx->chart, ctx->pinc, ctx->n0, ctx->ff, ctx->prevAng,
                       ctx->prevChart, ctx->prevPinc, ctx->dirbuf, ctx->Ut2, ctx->halo_in_lo,

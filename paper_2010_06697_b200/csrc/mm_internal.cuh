@@ -13,6 +13,8 @@
 
 #define MM_MAX_PARTIALS 24  // doubles reduced per block by any kernel
 
+struct mm_bloch_state;
+
 struct mm_ctx {
     int dim = 0, n = 0;
     double L = 0.0, h = 0.0;
@@ -82,6 +84,7 @@ struct mm_ctx {
     double ubar[9] = {0};
     double *Ut2 = nullptr;  // second u_tilde buffer (new u during a projection)
     double *Pbuf = nullptr; // stress field scratch (equilibrium_residual)
+    mm_bloch_state *bloch = nullptr;  // Bloch stability workspace (mm_bloch.cu)
     bool F_checked = false;
     bool points_only = false;
     // slab decomposition (3D, split along axis 0)
@@ -119,6 +122,7 @@ int mm_fail(mm_ctx *ctx, int code, const char *fmt, ...);
 int mm_alloc(mm_ctx *ctx, void **ptr, size_t bytes);
 int mm_ensure_partials(mm_ctx *ctx, int64_t nblocks);
 void mm_free(mm_ctx *ctx, void *p);
+void mm_bloch_free(mm_ctx *ctx);
 // copy the finalized reduction results (K doubles) back to host
 int mm_fetch_reduction(mm_ctx *ctx, int K, double *out);
 

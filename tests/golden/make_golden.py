@@ -368,6 +368,71 @@ def lce_protocol_visc():
                 p_inc=st.internal["p_inc"], total_sweeps=st.total_sweeps)
 
 
+def bloch_cases():
+    """Bloch stability (stability.py:171-289) on the reference's own test
+    inputs: identity moduli (2D, 3D), random major-symmetric PD fields,
+    fields that lose ellipticity, and a converged compressed MR state."""
+    from micromech import stability as stab
+    out = {}
+
+    def rand_tangent(npts, dim, lo, hi, rng):
+        m = dim * dim
+        Q = np.linalg.qr(rng.standard_normal((npts, m, m)))[0]
+        eigs = rng.uniform(lo, hi, size=(npts, m))
+        return np.einsum("pab,pb,pcb->pac", Q, eigs, Q).reshape(npts, dim, dim, dim, dim)
+
+    def ident(npts, dim):
+        eye = np.eye(dim * dim).reshape(dim, dim, dim, dim)
+        return np.broadcast_to(eye, (npts,) + eye.shape).copy()
+
+    cases = []
+    g8 = mm.Grid(2, 8, 0.5)
+    for k in [(2, 2), (3, 2), (4, 3), (1, 1)]:
+        cases.append((f"id8_{k[0]}{k[1]}", g8, ident(g8.npoints, 2), k, 3))
+    cases.append(("id8b", g8, ident(g8.npoints, 2), (2, 3), 1))
+    g4 = mm.Grid(3, 4, 0.5)
+    cases.append(("id3d", g4, ident(g4.npoints, 3), (2, 1, 1), 0))
+    g6 = mm.Grid(2, 6, 0.5)
+    for seed in range(5):
+        rng = np.random.default_rng(100 + seed)
+        Lf = rand_tangent(g6.npoints, 2, 0.5, 3.0, rng)
+        k = [(2, 1), (1, 2), (2, 2), (3, 1), (2, 3)][seed]
+        cases.append((f"pd{seed}", g6, Lf, k, seed))
+    for seed in range(3):
+        rng = np.random.default_rng(200 + seed)
+        a = rng.standard_normal(2)
+        a /= np.linalg.norm(a)
+        v = rng.standard_normal(2)
+        v /= np.linalg.norm(v)
+        x = g6.coords().reshape(-1, 2)
+        env = 1.0 + 0.5 * np.cos(np.pi * x[:, 0] / g6.length)
+        eye = np.eye(4).reshape(2, 2, 2, 2)
+        neg = np.einsum("i,j,k,l->ijkl", a, v, a, v)
+        Lf = eye[None] - 2.5 * env[:, None, None, None, None] * neg[None]
+        k = [(2, 1), (2, 2), (1, 1)][seed]
+        cases.append((f"unst{seed}", g6, Lf, k, seed))
+    names = []
+    for name, g, Lf, k, seed in cases:
+        r = stab.bloch_min_eigen(g, Lf, k, mu_rep=1.0, seed=seed)
+        out[name + "_L"] = Lf
+        out[name + "_meta"] = np.array([g.dim, g.n, seed] + list(k) + [0] * (3 - len(k)), float)
+        out[name + "_beta"] = np.array(r.beta)
+        out[name + "_iters"] = np.array(r.iterations)
+        out[name + "_conv"] = np.array(r.converged)
+        names.append(name)
+    # converged compressed MR state (test_stability.py:217-269)
+    model = mm.MooneyRivlin(mu=1.0, kappa=9.8, dim=2)
+    st, conv = mm.solve(g6, model, mm.MacroBC.strain(0.97 * np.eye(2)),
+                        mm.SolverParams(r_p_tol=1e-9, r_d_tol=1e-9, max_outer=4000))
+    assert conv
+    res = stab.stability_sweep(g6, model, st, k_max=2, seed=0)
+    out["mr_F"] = st.F
+    out["mr_betas"] = np.array([r.beta for r in res])
+    out["mr_ks"] = np.array([r.k for r in res])
+    out["names"] = np.array(names)
+    return out
+
+
 def main():
     only = sys.argv[1:]
     if only:  # regenerate the named fixtures only
@@ -402,6 +467,7 @@ def main():
     save("eq_residual_cases", **eq_residual_cases())
     save("scenario_fields", **scenario_fields())
     save("lce_protocol_visc", **lce_protocol_visc())
+    save("bloch_cases", **bloch_cases())
 
 
 if __name__ == "__main__":
