@@ -259,7 +259,10 @@ int mm_slab_open_peers(mm_ctx *ctx, int which, const void *handles, int P);
  * mm_project_residuals uses the plane-marching kernel (register/shared-memory
  * stencil reuse) when n is a multiple of 32; 0 selects the per-voxel kernel
  * (the two differ only in the order of the residual sums). */
-enum mm_option { MM_OPT_IMPLICIT_GRAD = 0, MM_OPT_STENCIL_MARCH = 1 };
+/* MM_OPT_T_FIELD (default 1): the fused update + local pass also stores
+ * T = F - lam/rho_next, and the next projection differentiates it instead of
+ * re-reading F and lam (even n, single-context grids). */
+enum mm_option { MM_OPT_IMPLICIT_GRAD = 0, MM_OPT_STENCIL_MARCH = 1, MM_OPT_T_FIELD = 2 };
 int mm_set_option(mm_ctx *ctx, int option, int64_t value);
 
 /* Central-difference stencils on the grid fields (grid.py:227-249):

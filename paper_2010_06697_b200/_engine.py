@@ -37,6 +37,7 @@ class Engine:
         # grad_u storage policy (include/mm_admm.h, MM_OPT_IMPLICIT_GRAD)
         self.ctx.set_option(0, int(os.environ.get("MM_IMPLICIT_GRAD", "0")))
         self.ctx.set_option(1, int(os.environ.get("MM_STENCIL_MARCH", "1")))
+        self.ctx.set_option(2, int(os.environ.get("MM_T_FIELD", "1")))
         self.model = None          # model whose parameters are on the device
         self.model_version = None
         self.lam_sum = None        # device-side sum of lam (None: recompute)

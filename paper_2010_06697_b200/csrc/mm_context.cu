@@ -715,7 +715,7 @@ void mm_destroy(mm_ctx *ctx) {
                       ctx->ang, ctx->chart, ctx->pinc, ctx->n0, ctx->ff, ctx->prevAng,
                       ctx->prevChart, ctx->prevPinc, ctx->dirbuf, ctx->Ut2, ctx->halo_in_lo,
                       ctx->halo_in_hi, ctx->halo_out_lo, ctx->halo_out_hi, ctx->sym, ctx->partials, ctx->red_out,
-                      ctx->res, ctx->tstate, ctx->stage, ctx->Pbuf};
+                      ctx->res, ctx->tstate, ctx->stage, ctx->Pbuf, ctx->Tbuf};
     for (double *p : ptrs) mm_free(ctx, p);
     void *others[] = {ctx->spec, ctx->tw_full, ctx->tw_half, ctx->tw_r2c, ctx->red_count,
                       ctx->nsw, ctx->ok, ctx->freestate, ctx->peer_recv, ctx->peer_send};
@@ -779,6 +779,7 @@ int mm_upload(mm_ctx *ctx, int field, const double *host, int64_t count) {
     rc = ensure_field(ctx, slot, ncomp);
     if (rc) return rc;
     if (field == MM_FIELD_F) ctx->F_checked = false;
+    if (field == MM_FIELD_F || field == MM_FIELD_LAM) ctx->T_valid = false;
     if (field == MM_FIELD_PREV_F) ctx->have_prev_F = true;
     if (field == MM_FIELD_PREV_ANG) ctx->have_prev_int = true;
     if (field == MM_FIELD_UT && ctx->g_implicit) {
@@ -811,6 +812,7 @@ int mm_add_field(mm_ctx *ctx, int field, const double *host, int64_t count) {
     if (!*slot) return mm_fail(ctx, MM_ERR_CONFIG, "field %d was never set", field);
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
     if (field == MM_FIELD_F) ctx->F_checked = false;
+    if (field == MM_FIELD_F || field == MM_FIELD_LAM) ctx->T_valid = false;
     return transfer(ctx, *slot, ncomp, host, nullptr, true);
 }
 
@@ -882,6 +884,7 @@ int mm_copy_field(mm_ctx *ctx, int dst_field, int src_field) {
     if ((src_field == MM_FIELD_G || dst_field == MM_FIELD_UT) && (rc = mm_materialize_G(ctx)))
         return rc;
     if (dst_field == MM_FIELD_UT) ctx->g_implicit = false;
+    if (dst_field == MM_FIELD_F || dst_field == MM_FIELD_LAM) ctx->T_valid = false;
     if (dst_field == MM_FIELD_G) {
         ctx->g_implicit = false;
         ctx->g_buf_valid = true;
@@ -1056,6 +1059,10 @@ int mm_set_option(mm_ctx *ctx, int option, int64_t value) {
             return MM_OK;
         }
         case MM_OPT_STENCIL_MARCH: ctx->opt_march = value != 0; return MM_OK;
+        case MM_OPT_T_FIELD:
+            ctx->opt_tfield = value != 0;
+            if (!ctx->opt_tfield) ctx->T_valid = false;
+            return MM_OK;
         default: return mm_fail(ctx, MM_ERR_PARAM, "unknown option %d", option);
     }
 }

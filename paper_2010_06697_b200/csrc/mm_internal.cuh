@@ -77,6 +77,7 @@ struct mm_ctx {
     // cache filled on demand (downloads, LCE local step).
     bool opt_implicit_g = false;  // MM_OPT_IMPLICIT_GRAD
     bool opt_march = true;        // MM_OPT_STENCIL_MARCH
+    bool opt_tfield = true;       // MM_OPT_T_FIELD
     bool lam_pending = false;     // multiplier ascent deferred by mm_project_residuals
     double pending_rho = 0.0;
     bool g_implicit = false;
@@ -84,6 +85,11 @@ struct mm_ctx {
     double ubar[9] = {0};
     double *Ut2 = nullptr;  // second u_tilde buffer (new u during a projection)
     double *Pbuf = nullptr; // stress field scratch (equilibrium_residual)
+    // T = F - lam / T_rho, written by the fused update + local pass so that
+    // the next projection's divergence reads 9 words instead of 18
+    double *Tbuf = nullptr;
+    bool T_valid = false;
+    double T_rho = 0.0;
     mm_bloch_state *bloch = nullptr;  // Bloch stability workspace (mm_bloch.cu)
     bool F_checked = false;
     bool points_only = false;

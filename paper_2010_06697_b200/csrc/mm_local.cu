@@ -502,7 +502,8 @@ k_descent(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
           const double *__restrict__ modA, const double *__restrict__ modB, int64_t M,
           double rho, double tol, double tol_gs, double phi_scale, int s0, int s1,
           double *__restrict__ tstate, uint8_t *__restrict__ freestate, double *__restrict__ res_out,
-          int32_t *__restrict__ nsw_io, double *partials, double *red_out, unsigned int *count) {
+          int32_t *__restrict__ nsw_io, double *__restrict__ Tout, double *partials,
+          double *red_out, unsigned int *count) {
     constexpr int K = 5 + D;  // ..., last slot: sum of per-point sweeps
     __shared__ double smem[32 * K];
     __shared__ double sacc[K * LOCAL_THREADS];
@@ -545,6 +546,11 @@ k_descent(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
         if (moved) {
 #pragma unroll
             for (int i = 0; i < D; ++i) F[i * M + p] = X[i];
+            if (Tout) {  // keep T = F - lam / rho current for the projection
+                const double irho = 1.0 / rho;
+#pragma unroll
+                for (int i = 0; i < D; ++i) Tout[i * M + p] = fma(-Lam[i * M + p], irho, X[i]);
+            }
         }
         if (tstate) {
             tstate[p] = t;
@@ -588,7 +594,7 @@ k_descent(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
 template <int MAT, int D, int ALGO, bool SWEEP>
 __global__ void __launch_bounds__(LOCAL_THREADS, LOCAL_MIN_BLOCKS)
 k_update_local(double *__restrict__ F, double *__restrict__ Lam, double *__restrict__ Gout,
-               const GSrc gs,
+               double *__restrict__ Tout, const GSrc gs,
                const double *__restrict__ modA, const double *__restrict__ modB, int64_t M,
                double rho_k, double rho, double tol, double tol_gs, double phi_scale, int chunk,
                double *__restrict__ res_out, int32_t *__restrict__ nsw_out, double *partials,
@@ -649,6 +655,11 @@ k_update_local(double *__restrict__ F, double *__restrict__ Lam, double *__restr
             if (moved) {
 #pragma unroll
                 for (int i = 0; i < D; ++i) F[i * M + p] = X[i];
+            }
+            if (Tout) {  // T = F - lam / rho for the next projection (row_fwd's expression)
+                const double irho = 1.0 / rho;
+#pragma unroll
+                for (int i = 0; i < D; ++i) Tout[i * M + p] = fma(-L[i], irho, X[i]);
             }
             if (res_out) {
                 res_out[p] = res;
@@ -829,12 +840,15 @@ static int launch_descent(mm_ctx *ctx, double rho, double tol, double phi_scale,
     if (rc) return rc;
     StageScope ss(ctx, MM_STAGE_LOCAL);
     if ((rc = ensure_logtab(ctx))) return rc;
+    // a later chunk keeps the fused pass's T field current for moved points
+    const bool keepT = ctx->T_valid && ctx->Tbuf && ctx->T_rho == rho;
+    if (!keepT) ctx->T_valid = false;
     k_descent<MAT, D><<<blocks, LOCAL_THREADS, 0, ctx->stream>>>(
         ctx->F, mm_gsrc(ctx), ctx->Lam, ctx->modA, MAT == MAT_MR ? ctx->modB : ctx->modA, ctx->M, rho,
         tol, gs_threshold(tol), phi_scale, s0, s1, persist ? ctx->tstate : nullptr,
         persist ? ctx->freestate : nullptr, want_points ? ctx->res : nullptr,
-        (persist || want_points) ? ctx->nsw : nullptr, ctx->partials, ctx->red_out,
-        ctx->red_count);
+        (persist || want_points) ? ctx->nsw : nullptr, keepT ? ctx->Tbuf : nullptr,
+        ctx->partials, ctx->red_out, ctx->red_count);
     MM_LAUNCH_CHECK(ctx);
     return MM_OK;
 }
@@ -860,6 +874,8 @@ int mm_run_local(mm_ctx *ctx, int material, double rho, double tol, int64_t max_
     const int D = ctx->D;
     memset(out, 0, sizeof *out);
     if (want_points && (rc = mm_ensure_points(ctx))) return rc;
+    if (material == MM_MAT_LCE || (material == MM_MAT_MR && ctx->dim == 2))
+        ctx->T_valid = false;  // these kernels do not maintain the T field
     if (material == MM_MAT_LCE) return mm_run_lce(ctx, rho, tol, max_sweeps, want_points, out);
     if (material == MM_MAT_MR && ctx->dim == 2) {
         // compiled 2D kernel (mooney_rivlin.py:169-255)
@@ -957,11 +973,24 @@ static int launch_update_local(mm_ctx *ctx, double rho_next, double tol, double 
     if (rc) return rc;
     StageScope ss(ctx, SWEEP ? MM_STAGE_FUSED : MM_STAGE_GRAD);
     if ((rc = ensure_logtab(ctx))) return rc;
+    // T = F - lam / rho_next for the next projection (single-context grids
+    // with packed even-length rows, where row_fwd uses this expression)
+    double *Tout = nullptr;
+    if (SWEEP && !ctx->slab_mode && !ctx->points_only && ctx->n % 2 == 0 && ctx->opt_tfield) {
+        if (!ctx->Tbuf && (rc = mm_alloc(ctx, (void **)&ctx->Tbuf, sizeof(double) * D * ctx->M)))
+            return rc;
+        Tout = ctx->Tbuf;
+    }
+    ctx->T_valid = false;
     k_update_local<MAT, D, ALGO, SWEEP><<<blocks, LOCAL_THREADS, 0, ctx->stream>>>(
-        ctx->F, ctx->Lam, kFusedStoresG ? ctx->G : nullptr, mm_gsrc(ctx), ctx->modA, MAT == MAT_MR ? ctx->modB : ctx->modA, ctx->M,
+        ctx->F, ctx->Lam, kFusedStoresG ? ctx->G : nullptr, Tout, mm_gsrc(ctx), ctx->modA, MAT == MAT_MR ? ctx->modB : ctx->modA, ctx->M,
         ctx->pending_rho, rho_next, tol, gs_threshold(tol), phi_scale, chunk, want_points ? ctx->res : nullptr,
         want_points ? ctx->nsw : nullptr, ctx->partials, ctx->red_out, ctx->red_count);
     MM_LAUNCH_CHECK(ctx);
+    if (Tout) {
+        ctx->T_valid = true;
+        ctx->T_rho = rho_next;
+    }
     return MM_OK;
 }
 

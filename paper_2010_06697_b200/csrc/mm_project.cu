@@ -198,6 +198,7 @@ struct RowGeom {
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double tval(const double *__restrict__ F, const double *__restrict__ L,
                                        int64_t off, double rho) {
+    if (!L) return __ldg(&F[off]);                  // F holds T already
     return __ldg(&F[off]) - __ldg(&L[off]) / rho;  // projection.py:154 (F - lam / rho)
 }
 
@@ -274,7 +275,9 @@ struct RowCfg {
 };
 
 // A tile holds ROWS consecutive rows x DIM components; line = c * ROWS + r.
-template <int N1, int N2, int DIM, int ROWS>
+// HAS_L = false: F already holds T = F - lam/rho (written by the fused
+// update + local pass) and is differentiated as is; half the loads.
+template <int N1, int N2, int DIM, int ROWS, bool HAS_L = true>
 __global__ void __launch_bounds__(RowCfg<N1, N2, DIM, ROWS>::NT, RowCfg<N1, N2, DIM, ROWS>::MINB)
 k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho,
           double2 *__restrict__ spec, RowGeom g, const double2 *__restrict__ tw_line,
@@ -310,20 +313,20 @@ k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho
                 const int64_t cz = (int64_t)(c * DIM) * M;                  // T_c0 (axis 0)
                 const int64_t cy = (int64_t)(c * DIM + 1) * M;              // T_c1 (axis 1, 3D)
                 const int64_t cx = (int64_t)(c * DIM + DIM - 1) * M + nb.self;  // contiguous
-                const double fxm = __ldg(&F[cx + xm]), lxm = __ldg(&L[cx + xm]);
-                const double fx0 = __ldg(&F[cx + x0]), lx0 = __ldg(&L[cx + x0]);
-                const double fx1 = __ldg(&F[cx + x1]), lx1 = __ldg(&L[cx + x1]);
-                const double fxp = __ldg(&F[cx + xp]), lxp = __ldg(&L[cx + xp]);
-                const double fzp0 = __ldg(&F[cz + nb.zp + x0]), lzp0 = __ldg(&L[cz + nb.zp + x0]);
-                const double fzp1 = __ldg(&F[cz + nb.zp + x1]), lzp1 = __ldg(&L[cz + nb.zp + x1]);
-                const double fzm0 = __ldg(&F[cz + nb.zm + x0]), lzm0 = __ldg(&L[cz + nb.zm + x0]);
-                const double fzm1 = __ldg(&F[cz + nb.zm + x1]), lzm1 = __ldg(&L[cz + nb.zm + x1]);
+                const double fxm = __ldg(&F[cx + xm]), lxm = HAS_L ? __ldg(&L[cx + xm]) : 0.0;
+                const double fx0 = __ldg(&F[cx + x0]), lx0 = HAS_L ? __ldg(&L[cx + x0]) : 0.0;
+                const double fx1 = __ldg(&F[cx + x1]), lx1 = HAS_L ? __ldg(&L[cx + x1]) : 0.0;
+                const double fxp = __ldg(&F[cx + xp]), lxp = HAS_L ? __ldg(&L[cx + xp]) : 0.0;
+                const double fzp0 = __ldg(&F[cz + nb.zp + x0]), lzp0 = HAS_L ? __ldg(&L[cz + nb.zp + x0]) : 0.0;
+                const double fzp1 = __ldg(&F[cz + nb.zp + x1]), lzp1 = HAS_L ? __ldg(&L[cz + nb.zp + x1]) : 0.0;
+                const double fzm0 = __ldg(&F[cz + nb.zm + x0]), lzm0 = HAS_L ? __ldg(&L[cz + nb.zm + x0]) : 0.0;
+                const double fzm1 = __ldg(&F[cz + nb.zm + x1]), lzm1 = HAS_L ? __ldg(&L[cz + nb.zm + x1]) : 0.0;
                 double y0 = 0.0, y1 = 0.0;
                 if (DIM == 3) {
-                    const double fyp0 = __ldg(&F[cy + nb.yp + x0]), lyp0 = __ldg(&L[cy + nb.yp + x0]);
-                    const double fyp1 = __ldg(&F[cy + nb.yp + x1]), lyp1 = __ldg(&L[cy + nb.yp + x1]);
-                    const double fym0 = __ldg(&F[cy + nb.ym + x0]), lym0 = __ldg(&L[cy + nb.ym + x0]);
-                    const double fym1 = __ldg(&F[cy + nb.ym + x1]), lym1 = __ldg(&L[cy + nb.ym + x1]);
+                    const double fyp0 = __ldg(&F[cy + nb.yp + x0]), lyp0 = HAS_L ? __ldg(&L[cy + nb.yp + x0]) : 0.0;
+                    const double fyp1 = __ldg(&F[cy + nb.yp + x1]), lyp1 = HAS_L ? __ldg(&L[cy + nb.yp + x1]) : 0.0;
+                    const double fym0 = __ldg(&F[cy + nb.ym + x0]), lym0 = HAS_L ? __ldg(&L[cy + nb.ym + x0]) : 0.0;
+                    const double fym1 = __ldg(&F[cy + nb.ym + x1]), lym1 = HAS_L ? __ldg(&L[cy + nb.ym + x1]) : 0.0;
                     y0 = (fyp0 - lyp0 * irho) - (fym0 - lym0 * irho);
                     y1 = (fyp1 - lyp1 * irho) - (fym1 - lym1 * irho);
                 }
@@ -353,7 +356,8 @@ k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho
             const int c = line / ROWS, r = line - c * ROWS;
             const int64_t row = row0 + r;
             double2 z = make_double2(0.0, 0.0);
-            if (row < g.nrows) z.x = div_at(F, L, rho, g, c, row_nbrs(g, (int)row), m);
+            if (row < g.nrows)
+                z.x = div_at(F, HAS_L ? L : nullptr, rho, g, c, row_nbrs(g, (int)row), m);
             buf[m * LD + line] = z;
         }
     }
@@ -987,14 +991,20 @@ int run_rows_t(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double
     const size_t smem = sizeof(double2) * (size_t)(g.N + 1) * (C::TK + 1) * (N1 ? 1 : 2);
     dim3 grid((unsigned)((g.nrows + ROWS - 1) / ROWS));
     if (fwd) {
-        auto kern = k_row_fwd<N1, N2, DIM, ROWS>;
-        int rc = launch_smem(ctx, kern, grid, threads, smem);
-        if (rc) return rc;
-        // fsrc: divergence of that field alone (rho = inf: T = F - L * 0 = F exactly)
-        const double *Fs = fsrc ? fsrc : ctx->F;
-        const double *Ls = fsrc ? fsrc : ctx->Lam;
-        kern<<<grid, threads, smem, ctx->stream>>>(Fs, Ls, fsrc ? INFINITY : rho, ctx->spec, g,
-                                                   tw_line, ctx->tw_r2c);
+        if (fsrc) {
+            // divergence of the given field alone (T supplied, or a stress field)
+            auto kern = k_row_fwd<N1, N2, DIM, ROWS, false>;
+            int rc = launch_smem(ctx, kern, grid, threads, smem);
+            if (rc) return rc;
+            kern<<<grid, threads, smem, ctx->stream>>>(fsrc, nullptr, rho, ctx->spec, g, tw_line,
+                                                       ctx->tw_r2c);
+        } else {
+            auto kern = k_row_fwd<N1, N2, DIM, ROWS, true>;
+            int rc = launch_smem(ctx, kern, grid, threads, smem);
+            if (rc) return rc;
+            kern<<<grid, threads, smem, ctx->stream>>>(ctx->F, ctx->Lam, rho, ctx->spec, g,
+                                                       tw_line, ctx->tw_r2c);
+        }
     } else {
         auto kern = k_row_inv<N1, N2, DIM, ROWS>;
         int rc = launch_smem(ctx, kern, grid, threads, smem);
@@ -1106,10 +1116,12 @@ int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
     int rc = ensure_constants(ctx);
     if (rc) return rc;
     const int n = ctx->n, d = ctx->dim;
-    // A: divergence + R2C rows
+    // A: divergence + R2C rows (of the T field the fused pass left, when
+    // it is current for this rho)
     {
         StageScope ss(ctx, MM_STAGE_ROW_FWD);
-        if ((rc = run_rows(ctx, true, rho))) return rc;
+        const bool useT = ctx->T_valid && ctx->Tbuf && ctx->T_rho == rho && !ctx->slab_mode;
+        if ((rc = run_rows(ctx, true, rho, nullptr, useT ? ctx->Tbuf : nullptr))) return rc;
     }
     ColGeom g;
     g.N = n;
@@ -1218,6 +1230,7 @@ int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
         ctx->g_buf_valid = true;
         return MM_OK;
     }
+    if (update == 1) ctx->T_valid = false;  // lam changed
     if (update == 2 || ctx->opt_implicit_g) {
         // new u becomes current; grad_u is now ubar + D u (implicit)
         std::swap(ctx->Ut, ctx->Ut2);
@@ -1252,7 +1265,7 @@ int mm_run_eq_residual(mm_ctx *ctx, const double *P, double *out) {
     const int n = ctx->n, d = ctx->dim;
     {
         StageScope ss(ctx, MM_STAGE_OTHER);
-        if ((rc = run_rows(ctx, true, 0.0, nullptr, P))) return rc;
+        if ((rc = run_rows(ctx, true, 1.0, nullptr, P))) return rc;
     }
     ColGeom g;
     g.N = n;
