@@ -271,6 +271,9 @@ struct RowCfg {
     static constexpr int NT = NT0 < 64 ? 64 : NT0;
     static constexpr int MINB0 = 65536 / (NT * 96);
     static constexpr int MINB = MINB0 < 1 ? 1 : MINB0;  // aim at <= 96 registers
+    // the C2R pass fits 80 registers without spilling: one more resident tile
+    static constexpr int MINB_INV0 = 65536 / (NT * 80);
+    static constexpr int MINB_INV = MINB_INV0 < 1 ? 1 : MINB_INV0;
     static constexpr int NC = N1 * N2;                  // compile-time line length (0: runtime)
 };
 
@@ -390,7 +393,7 @@ k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho
 // E: inverse C2R along rows -> u_tilde (unnormalised; 1/n^d folded into C)
 // ---------------------------------------------------------------------------
 template <int N1, int N2, int DIM, int ROWS>
-__global__ void __launch_bounds__(RowCfg<N1, N2, DIM, ROWS>::NT, RowCfg<N1, N2, DIM, ROWS>::MINB)
+__global__ void __launch_bounds__(RowCfg<N1, N2, DIM, ROWS>::NT, RowCfg<N1, N2, DIM, ROWS>::MINB_INV)
 k_row_inv(const double2 *__restrict__ spec, double *__restrict__ Ut, RowGeom g,
           const double2 *__restrict__ tw_line, const double2 *__restrict__ tw_r2c) {
     using C = RowCfg<N1, N2, DIM, ROWS>;
