@@ -137,15 +137,15 @@ def stage_bytes(n, dim=3):
     return {
         # standalone local chunk, grad_u implicit: read u, F, lam, mu, kappa; write F
         "local": (dim + 2 * D + 2 + D) * w,
-        "row_fwd": 2 * D * w + spec,                     # read F, lam; write spectrum
+        "row_fwd": D * w + spec,                         # read T = F - lam/rho; write spectrum
         "col_fwd": 2 * spec,
         "col_solve": 2 * spec,
         "col_inv": 2 * spec,
         "row_inv": spec + dim * w,                       # read spectrum, write u_tilde
         # residual pass: read u_new, u_old (or G_old), F
         "grad": (2 * dim + D) * w,
-        # fused ascent + first chunk: read u, F, lam, mu, kappa; write lam, F
-        "fused": (dim + 2 * D + 2 + 2 * D) * w,
+        # fused ascent + first chunk: read u, F, lam, mu, kappa; write lam, F, T
+        "fused": (dim + 2 * D + 2 + 3 * D) * w,
     }
 
 

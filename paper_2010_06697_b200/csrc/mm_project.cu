@@ -492,8 +492,13 @@ struct ColCfg {
     static constexpr int MINB = N1 ? (NT <= 128 ? 5 : 2) : 1;
 };
 
+#ifndef COL_SOLVE_MINB
+#define COL_SOLVE_MINB 6
+#endif
 template <int N1, int N2, int MODE>
-__global__ void __launch_bounds__(ColCfg<N1, N2>::NT, ColCfg<N1, N2>::MINB)
+__global__ void __launch_bounds__(ColCfg<N1, N2>::NT,
+                                  (MODE == COL_SOLVE && N1 == 16 && N2 == 16) ? COL_SOLVE_MINB
+                                                                              : ColCfg<N1, N2>::MINB)
 k_col(double2 *__restrict__ spec, ColGeom g, const double2 *__restrict__ tw) {
     constexpr int TK = ColCfg<N1, N2>::TK, LD = TK + 1, NT = ColCfg<N1, N2>::NT;
     extern __shared__ double2 smem_c[];
