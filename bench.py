@@ -141,6 +141,7 @@ def stage_bytes(n, dim=3):
         "col_fwd": 2 * spec,
         "col_solve": 2 * spec,
         "col_inv": 2 * spec,
+        "plane": 2 * spec,                               # B + C + D in one pass (L2-resident planes)
         "row_inv": spec + dim * w,                       # read spectrum, write u_tilde
         # residual pass: read u_new, u_old (or G_old), F
         "grad": (2 * dim + D) * w,

@@ -104,7 +104,8 @@ enum mm_stage {
     MM_STAGE_FROZEN = 7,    /* LCE director + Frank stencil */
     MM_STAGE_OTHER = 8,     /* transfers, sums, checks */
     MM_STAGE_FUSED = 9,     /* multiplier ascent fused with the next first local chunk */
-    MM_NSTAGE = 10
+    MM_STAGE_PLANE = 10,    /* COL_FWD + COL_SOLVE + COL_INV in one cluster pass (3D) */
+    MM_NSTAGE = 11
 };
 
 typedef struct {
@@ -262,7 +263,17 @@ int mm_slab_open_peers(mm_ctx *ctx, int which, const void *handles, int P);
 /* MM_OPT_T_FIELD (default 1): the fused update + local pass also stores
  * T = F - lam/rho_next, and the next projection differentiates it instead of
  * re-reading F and lam (even n, single-context grids). */
-enum mm_option { MM_OPT_IMPLICIT_GRAD = 0, MM_OPT_STENCIL_MARCH = 1, MM_OPT_T_FIELD = 2 };
+/* MM_OPT_PLANE_FFT (default 1): 3D single-GPU grids with power-of-two
+ * n <= 256 keep the half spectrum as (component, k2) planes and run the
+ * axis-1 / axis-0 transforms and the solve in one launch, one thread-block
+ * cluster per plane with the plane resident in L2 (bitwise identical to the
+ * three-launch column sequence). */
+enum mm_option {
+    MM_OPT_IMPLICIT_GRAD = 0,
+    MM_OPT_STENCIL_MARCH = 1,
+    MM_OPT_T_FIELD = 2,
+    MM_OPT_PLANE_FFT = 3
+};
 int mm_set_option(mm_ctx *ctx, int option, int64_t value);
 
 /* Central-difference stencils on the grid fields (grid.py:227-249):

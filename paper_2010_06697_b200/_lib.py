@@ -52,7 +52,7 @@ SLAB_BUF_SEND, SLAB_BUF_RECV, SLAB_BUF_HALO_OUT_LO, SLAB_BUF_HALO_OUT_HI = range
 SLAB_BUF_HALO_IN_LO, SLAB_BUF_HALO_IN_HI = 4, 5
 
 STAGES = ("local", "row_fwd", "col_fwd", "col_solve", "col_inv", "row_inv", "grad", "frozen",
-          "other", "fused")
+          "other", "fused", "plane")
 
 
 class LocalStatsC(ctypes.Structure):
@@ -67,7 +67,7 @@ class UpdateStatsC(ctypes.Structure):
 
 
 class ProfileC(ctypes.Structure):
-    _fields_ = [("ms", ctypes.c_double * 10), ("launches", ctypes.c_int64 * 10)]
+    _fields_ = [("ms", ctypes.c_double * 11), ("launches", ctypes.c_int64 * 11)]
 
 
 class LCEParamsC(ctypes.Structure):

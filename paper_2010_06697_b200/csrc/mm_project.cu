@@ -144,6 +144,158 @@ __device__ __forceinline__ void tile_fft(double2 *buf, const double2 *__restrict
     }
 }
 
+// tile_fft with the direction a runtime argument: the same arithmetic as
+// tile_fft<..., INV> (twiddle imaginary parts and the +-i rotations selected,
+// not recomputed), bit for bit.  One instantiation serves both directions,
+// so a forward and an inverse transform in one loop body share one register
+// allocation (inlined compile-time pairs keep values of the first live into
+// the second and spill).
+template <int R>
+__device__ __forceinline__ void fft_reg_rt(double2 (&v)[R], bool inv) {
+    if constexpr (R > 1) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int j = brev<R>(i);
+            if (j > i) {
+                double2 t = v[i];
+                v[i] = v[j];
+                v[j] = t;
+            }
+        }
+#pragma unroll
+        for (int half = 1; half < R; half <<= 1) {
+#pragma unroll
+            for (int i = 0; i < R; i += 2 * half) {
+#pragma unroll
+                for (int k = 0; k < half; ++k) {
+                    const double2 a = v[i + k];
+                    double2 b = v[i + k + half];
+                    if (k != 0) {
+                        if (2 * k == half) {
+                            b = inv ? make_double2(-b.y, b.x) : make_double2(b.y, -b.x);
+                        } else {
+                            double2 w = c_w32[k * (16 / half)];
+                            if (inv) w.y = -w.y;
+                            b = cmul(b, w);
+                        }
+                    }
+                    v[i + k] = cadd(a, b);
+                    v[i + k + half] = csub(a, b);
+                }
+            }
+        }
+    }
+}
+
+template <int N1, int N2, int TK>
+__device__ __forceinline__ void tile_fft_rt(double2 *buf, const double2 *__restrict__ tw, bool inv) {
+    constexpr int LD = TK + 1;
+    const int tid = threadIdx.x;
+    const int c = tid % TK;
+    static_assert(N2 > 1, "four-step tiles only");
+    double2 v[N1];
+    const int n2 = tid / TK;
+    const bool act1 = tid < TK * N2;
+    if (act1) {
+#pragma unroll
+        for (int n1 = 0; n1 < N1; ++n1) v[n1] = buf[(N2 * n1 + n2) * LD + c];
+        fft_reg_rt<N1>(v, inv);
+#pragma unroll
+        for (int k1 = 1; k1 < N1; ++k1) {
+            if (n2 != 0) {
+                double2 w = __ldg(&tw[n2 * k1]);
+                if (inv) w.y = -w.y;
+                v[k1] = cmul(v[k1], w);
+            }
+        }
+    }
+    __syncthreads();
+    if (act1) {
+#pragma unroll
+        for (int k1 = 0; k1 < N1; ++k1) buf[(k1 * N2 + n2) * LD + c] = v[k1];
+    }
+    __syncthreads();
+    double2 u[N2];
+    const int k1 = tid / TK;
+    const bool act2 = tid < TK * N1;
+    if (act2) {
+#pragma unroll
+        for (int j = 0; j < N2; ++j) u[j] = buf[(k1 * N2 + j) * LD + c];
+        fft_reg_rt<N2>(u, inv);
+    }
+    __syncthreads();
+    if (act2) {
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) buf[(k1 + N1 * k2) * LD + c] = u[k2];
+    }
+    __syncthreads();
+}
+
+// Stockham autosort FFT of TK lines held in shared memory (element n of
+// line c at buf[n*LD + c]) with 8 points per thread: thread t serves line
+// t % TK and butterfly column q = t / TK < N/8.  A pass of radix R (8, 4 or
+// 2) with NS = product of the earlier radices takes butterflies
+// j = q + b*N/8 (b < 8/R): reads x[j + r N/R], multiplies by
+// W_{NS R}^{(j mod NS) r}, transforms in registers and writes
+// y[(j / NS) NS R + (j mod NS) + r NS]; the last pass leaves natural order.
+// Compared with the two-step register four-step (tile_fft, 16 points per
+// thread) it trades one more shared-memory round trip for half the live
+// registers and twice the threads per tile.
+template <int N, int TK, int R, int NS>
+__device__ __forceinline__ void stockham_pass(double2 *buf, const double2 *__restrict__ tw, bool inv) {
+    constexpr int LD = TK + 1, NB = 8 / R, JS = N / 8;
+    const int c = threadIdx.x % TK, q = threadIdx.x / TK;
+    double2 v[NB][R];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[b][r] = buf[(q + b * JS + r * (N / R)) * LD + c];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const int j = q + b * JS;
+        const int jm = j & (NS - 1);
+        if constexpr (NS > 1) {
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                double2 w = __ldg(&tw[jm * r * (N / (NS * R))]);
+                if (inv) w.y = -w.y;
+                v[b][r] = cmul(v[b][r], w);
+            }
+        }
+        fft_reg_rt<R>(v[b], inv);
+        const int base = (j - jm) * R + jm;
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[(base + r * NS) * LD + c] = v[b][r];
+    }
+    __syncthreads();
+}
+
+// radix plan: N = 8 * 8 * 4 (256), 8 * 4 * 4 (128), 8 * 8 (64), 8 * 4 (32), 4 * 4 (16)
+template <int N, int TK>
+__device__ __forceinline__ void tile_fft_s(double2 *buf, const double2 *__restrict__ tw, bool inv) {
+    static_assert(N >= 16 && N <= 256 && (N & (N - 1)) == 0, "N in 16..256, power of two");
+    if constexpr (N == 256) {
+        stockham_pass<N, TK, 8, 1>(buf, tw, inv);
+        stockham_pass<N, TK, 8, 8>(buf, tw, inv);
+        stockham_pass<N, TK, 4, 64>(buf, tw, inv);
+    } else if constexpr (N == 128) {
+        stockham_pass<N, TK, 8, 1>(buf, tw, inv);
+        stockham_pass<N, TK, 4, 8>(buf, tw, inv);
+        stockham_pass<N, TK, 4, 32>(buf, tw, inv);
+    } else if constexpr (N == 64) {
+        stockham_pass<N, TK, 8, 1>(buf, tw, inv);
+        stockham_pass<N, TK, 8, 8>(buf, tw, inv);
+    } else if constexpr (N == 32) {
+        stockham_pass<N, TK, 8, 1>(buf, tw, inv);
+        stockham_pass<N, TK, 4, 8>(buf, tw, inv);
+    } else {
+        stockham_pass<N, TK, 4, 1>(buf, tw, inv);
+        stockham_pass<N, TK, 4, 4>(buf, tw, inv);
+    }
+}
+
 // Exact DFT of TK lines of runtime length N (any N), via a scratch tile.
 template <int TK, bool INV>
 __device__ __forceinline__ void tile_dft(double2 *buf, double2 *scr, int N,
@@ -191,6 +343,9 @@ struct RowGeom {
     // above the last local plane come from neighbour ranks ([c][i1*n + x]).
     int nl;
     const double *hlo, *hhi;
+    // spectrum layout: 0 = rows ((c*nrows + row)*P + k); 1 = planes
+    // ((c*nh + k)*nrows + row), every (c, k) an n x n plane [i0][i1] (k_plane)
+    int plane;
 };
 
 // ---------------------------------------------------------------------------
@@ -369,7 +524,17 @@ k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho
     // split (packed) and store k = 0 .. n/2
     const int nh = packed ? N + 1 : g.n / 2 + 1;
     for (int w = threadIdx.x; w < TK * nh; w += C::NT) {
-        const int line = w / nh, k = w - line * nh;
+        // plane layout: consecutive threads take consecutive rows of one
+        // (c, k) (ROWS x 16 B runs); row layout: consecutive k of one row
+        int line, k;
+        if (g.plane) {
+            const int r0 = w % ROWS, t = w / ROWS;
+            k = t % nh;
+            line = (t / nh) * ROWS + r0;
+        } else {
+            line = w / nh;
+            k = w - line * nh;
+        }
         const int c = line / ROWS, r = line - c * ROWS;
         const int64_t row = row0 + r;
         if (row >= g.nrows) continue;
@@ -385,7 +550,10 @@ k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho
         } else {
             X = buf[k * LD + line];
         }
-        spec[((int64_t)c * g.nrows + row) * g.P + k] = X;
+        if (g.plane)
+            spec[((int64_t)c * nh + k) * g.nrows + row] = X;
+        else
+            spec[((int64_t)c * g.nrows + row) * g.P + k] = X;
     }
 }
 
@@ -406,11 +574,21 @@ k_row_inv(const double2 *__restrict__ spec, double *__restrict__ Ut, RowGeom g,
     const int64_t row0 = (int64_t)blockIdx.x * ROWS;
     const int nh = packed ? N + 1 : g.n / 2 + 1;
     for (int w = threadIdx.x; w < TK * nh; w += C::NT) {
-        const int line = w / nh, k = w - line * nh;
+        int line, k;
+        if (g.plane) {
+            const int r0 = w % ROWS, t = w / ROWS;
+            k = t % nh;
+            line = (t / nh) * ROWS + r0;
+        } else {
+            line = w / nh;
+            k = w - line * nh;
+        }
         const int c = line / ROWS, r = line - c * ROWS;
         const int64_t row = row0 + r;
         double2 X = make_double2(0.0, 0.0);
-        if (row < g.nrows) X = spec[((int64_t)c * g.nrows + row) * g.P + k];
+        if (row < g.nrows)
+            X = g.plane ? spec[((int64_t)c * nh + k) * g.nrows + row]
+                        : spec[((int64_t)c * g.nrows + row) * g.P + k];
         buf[k * LD + line] = X;
     }
     __syncthreads();
@@ -626,7 +804,6 @@ k_colp(double2 *__restrict__ spec, ColGeom g, const double2 *__restrict__ tw, Ti
     constexpr int TK = C::TK, LD = TK + 1, NT = C::NT, N = N1 * N2;
     constexpr int IT = (N * TK + NT - 1) / NT;
     extern __shared__ double2 smem_c[];
-    double2 *bufs[2] = {smem_c, smem_c + (size_t)N * LD};
     auto tile_base = [&](int t, int &k0, int &outer) -> double2 * {
         const int tk = t % tm.ntk;
         const int rest = t / tm.ntk;
@@ -651,11 +828,11 @@ k_colp(double2 *__restrict__ spec, ColGeom g, const double2 *__restrict__ tw, Ti
         cp_async_commit();
     };
     int t = blockIdx.x;
-    if (t < ntiles) issue(t, bufs[0]);
+    if (t < ntiles) issue(t, smem_c);
     for (int iter = 0; t < ntiles; t += gridDim.x, ++iter) {
-        double2 *buf = bufs[iter & 1];
+        double2 *buf = smem_c + (iter & 1) * (N * LD);  // offsets keep LDS/STS (not generic)
         const int tn = t + gridDim.x;
-        if (tn < ntiles) issue(tn, bufs[(iter + 1) & 1]);
+        if (tn < ntiles) issue(tn, smem_c + ((iter + 1) & 1) * (N * LD));
         else cp_async_commit();
         cp_async_wait<1>();
         __syncthreads();
@@ -694,6 +871,158 @@ k_colp(double2 *__restrict__ spec, ColGeom g, const double2 *__restrict__ tw, Ti
         __syncthreads();  // this buffer is refilled two tiles later
     }
     cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
+// B + C + D in one launch on the plane layout (RowGeom::plane): a cluster of
+// CS CTAs owns one (component, k2) plane [i0][i1] of the half spectrum
+// (n x n complex, 1 MB at 256^3) and runs
+//   pass 1  FFT along axis 1 (contiguous lines of the plane)
+//   pass 2  FFT along axis 0, u_hat = -d_hat / |g|^2 on live modes, inverse
+//   pass 3  inverse FFT along axis 1
+// with cluster barriers (release / acquire at cluster scope) between the
+// passes.  CTA r of the cluster takes tiles r*NTILE/CS .. of every pass.  The
+// plane stays in L2 from pass 1 to pass 3, so the spectrum crosses HBM once
+// each way instead of three times (B, C, D of the row layout each read and
+// write it).  The per-line arithmetic (tile_fft, the solve expression and its
+// summation order) is that of k_colp / k_col: results are bitwise identical.
+// ---------------------------------------------------------------------------
+struct PlaneGeom {
+    int n, nh;
+    const double *sym;
+    double thresh, scale;
+};
+
+template <int N1, int N2, int TK>
+struct PlaneCfg {
+    static constexpr int N = N1 * N2;
+    static constexpr int NT = TK * N / 8;  // 8 points per thread (tile_fft_s)
+    static constexpr int IT = (N * TK + NT - 1) / NT;
+    // resident CTAs per SM the two tile buffers allow (<= 227 KB of shared
+    // memory), requested from the register allocator
+    static constexpr int SMEM = 2 * N * (TK + 1) * 16;
+    static constexpr int MINB0 = (227 * 1024) / (SMEM + 1024);
+    static constexpr int MINB1 = MINB0 > 8 ? 8 : (MINB0 < 1 ? 1 : MINB0);
+    // ... but not below 64 registers per thread
+    static constexpr int MINB = MINB1 * NT * 64 > 65536 ? 65536 / (NT * 64) : MINB1;
+};
+
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile(
+        "barrier.cluster.arrive.release.aligned;\n"
+        "barrier.cluster.wait.acquire.aligned;\n" ::
+            : "memory");
+}
+
+// One pass over tiles [t0, t1) of a plane, double-buffered: while tile t is
+// transformed in one shared buffer, the cp.async copies of tile t+1 land in
+// the other (global -> shared without registers; .cg bypasses L1, so data
+// another CTA of the cluster wrote before the barrier is read from L2).
+// KIND 0 / 1: forward / inverse FFT of TK consecutive lines along axis 1
+// (contiguous); KIND 2: forward FFT of TK consecutive columns along axis 0,
+// solve, inverse (k_col<COL_SOLVE>'s arithmetic).
+enum { PL_ROW_FWD = 0, PL_ROW_INV = 1, PL_COL_SOLVE = 2 };
+
+template <int N1, int N2, int TK, int KIND>
+__device__ __forceinline__ void plane_pass(double2 *__restrict__ pl, double2 *smem, int t0, int t1,
+                                           const PlaneGeom &g, int k2,
+                                           const double2 *__restrict__ tw) {
+    using C = PlaneCfg<N1, N2, TK>;
+    constexpr int N = C::N, NT = C::NT, IT = C::IT, LD = TK + 1;
+    // buffer b at smem + b * N * LD (plain offsets from the shared base keep
+    // the accesses LDS/STS; an array of two pointers made them generic)
+    // element w of tile t: global offset and shared slot
+    auto goff = [&](int t, int w) -> int64_t {
+        if constexpr (KIND == PL_COL_SOLVE) return (int64_t)(w / TK) * N + t * TK + w % TK;
+        else return (int64_t)t * TK * N + w;
+    };
+    auto slot = [&](int w) -> int {
+        if constexpr (KIND == PL_COL_SOLVE) return (w / TK) * LD + (w % TK);
+        else return (w % N) * LD + w / N;
+    };
+    auto issue = [&](int t, double2 *dst) {
+        int tx = threadIdx.x;
+        asm volatile("" : "+r"(tx));  // addresses are recomputed per tile, not kept live
+#pragma unroll 4
+        for (int it = 0; it < IT; ++it) {
+            const int w = it * NT + tx;
+            if (w < N * TK) cp_async16(&dst[slot(w)], &pl[goff(t, w)], 16);
+        }
+        cp_async_commit();
+    };
+    if (t0 < t1) issue(t0, smem);
+#pragma unroll 1
+    for (int t = t0, i = 0; t < t1; ++t, ++i) {
+        // keep loop-invariant loads (twiddles, symbols) and addresses inside
+        // the loop instead of hoisted into registers for all tiles
+        int tx = threadIdx.x;
+        const double *sym = g.sym;
+        asm volatile("" : "+l"(tw), "+l"(sym), "+r"(tx));
+        double2 *buf = smem + (i & 1) * (N * LD);
+        if (t + 1 < t1) issue(t + 1, smem + ((i + 1) & 1) * (N * LD));
+        else cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        // COL_SOLVE: the symbols of this thread's elements are loaded before
+        // the forward transform (their latency hides behind it)
+        double s0v[KIND == PL_COL_SOLVE ? IT : 1], s1v = 0.0;
+        if constexpr (KIND == PL_COL_SOLVE) {
+#pragma unroll
+            for (int it = 0; it < IT; ++it) {
+                const int w = it * NT + tx;
+                s0v[it] = w < N * TK ? __ldg(&sym[w / TK]) : 0.0;
+            }
+            s1v = __ldg(&sym[N + t * TK + tx % TK]);  // NT is a multiple of TK
+        }
+        // COL_SOLVE: forward, solve, inverse as two trips of one loop body
+        constexpr int NPH = KIND == PL_COL_SOLVE ? 2 : 1;
+#pragma unroll 1
+        for (int ph = 0; ph < NPH; ++ph) {
+            asm volatile("" : "+l"(tw));
+            tile_fft_s<N, TK>(buf, tw, KIND == PL_ROW_INV || ph == 1);
+            if (KIND == PL_COL_SOLVE && ph == 0) {
+                const double sl = __ldg(&sym[2 * N + k2]);
+#pragma unroll
+                for (int it = 0; it < IT; ++it) {
+                    const int w = it * NT + tx;
+                    if (w < N * TK) {
+                        const int kl = w / TK, c = w % TK;
+                        double gsq = s0v[it];
+                        gsq = gsq + s1v;
+                        gsq = gsq + sl;
+                        const double inv = (gsq > g.thresh) ? 1.0 / gsq : 0.0;
+                        buf[kl * LD + c] = cscale(buf[kl * LD + c], -inv * g.scale);
+                    }
+                }
+                __syncthreads();
+            }
+        }
+#pragma unroll 4
+        for (int it = 0; it < IT; ++it) {
+            const int w = it * NT + tx;
+            if (w < N * TK) pl[goff(t, w)] = buf[slot(w)];
+        }
+        __syncthreads();  // this buffer is refilled by the issue two tiles on
+    }
+    cp_async_wait<0>();
+}
+
+template <int N1, int N2, int TK, int CS>
+__global__ void __cluster_dims__(CS, 1, 1)
+    __launch_bounds__(PlaneCfg<N1, N2, TK>::NT, PlaneCfg<N1, N2, TK>::MINB)
+k_plane(double2 *__restrict__ spec, PlaneGeom g, const double2 *__restrict__ tw) {
+    constexpr int N = N1 * N2;
+    constexpr int PER = N / TK / CS;  // tiles per CTA per pass
+    extern __shared__ double2 smem_c[];
+    const int plane = blockIdx.x / CS;  // c * nh + k2
+    const int r = blockIdx.x % CS;      // rank in the cluster
+    const int k2 = plane % g.nh;
+    double2 *pl = spec + (int64_t)plane * N * N;
+    plane_pass<N1, N2, TK, PL_ROW_FWD>(pl, smem_c, r * PER, (r + 1) * PER, g, k2, tw);
+    cluster_barrier();
+    plane_pass<N1, N2, TK, PL_COL_SOLVE>(pl, smem_c, r * PER, (r + 1) * PER, g, k2, tw);
+    cluster_barrier();
+    plane_pass<N1, N2, TK, PL_ROW_INV>(pl, smem_c, r * PER, (r + 1) * PER, g, k2, tw);
 }
 
 // ---------------------------------------------------------------------------
@@ -1029,12 +1358,21 @@ int run_rows_n(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double
     // 4 rows per tile (2 for 32-point register FFTs): <= 384 threads, 3-4 tiles per SM
     constexpr bool big = N1 >= 32;
     if (g.dim == 2) return run_rows_t<N1, N2, 2, big ? 2 : 4>(ctx, fwd, rho, g, tw, u_out, fsrc);
+    static int rows_env = -1;
+    if (rows_env < 0) {
+        const char *e = getenv("MM_PLANE_ROWS");
+        rows_env = e ? atoi(e) : 4;
+    }
+    // plane layout: ROWS consecutive rows give ROWS x 16 B runs per (c, k2)
+    if constexpr (!big)
+        if (g.plane && rows_env == 8) return run_rows_t<N1, N2, 3, 8>(ctx, fwd, rho, g, tw, u_out, fsrc);
     return run_rows_t<N1, N2, 3, big ? 2 : 4>(ctx, fwd, rho, g, tw, u_out, fsrc);
 }
 
 int run_rows(mm_ctx *ctx, bool fwd, double rho, double *u_out = nullptr,
-             const double *fsrc = nullptr) {
+             const double *fsrc = nullptr, bool plane = false) {
     RowGeom g;
+    g.plane = plane ? 1 : 0;
     g.n = ctx->n;
     g.dim = ctx->dim;
     g.M = ctx->M;
@@ -1102,6 +1440,78 @@ int run_col(mm_ctx *ctx, const ColGeom &g, int n_outer) {
     }
 }
 
+template <int N1, int N2, int TK, int CS>
+int run_plane_t(mm_ctx *ctx, const PlaneGeom &g) {
+    using C = PlaneCfg<N1, N2, TK>;
+    const size_t smem = sizeof(double2) * (size_t)C::N * (TK + 1) * 2;
+    auto kern = k_plane<N1, N2, TK, CS>;
+    int rc = launch_smem(ctx, kern, dim3(1), C::NT, smem);
+    if (rc) return rc;
+    if (CS > 8) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess)
+            return mm_fail(ctx, MM_ERR_CUDA, "cluster size %d: %s", CS, cudaGetErrorString(e));
+    }
+    const int blocks = CS * ctx->dim * g.nh;
+    kern<<<blocks, C::NT, smem, ctx->stream>>>(ctx->spec, g, ctx->tw_full);
+    MM_LAUNCH_CHECK(ctx);
+    return MM_OK;
+}
+
+// cluster size per plane (MM_PLANE_CS overrides; tiles per pass must divide)
+template <int N1, int N2, int TK>
+int run_plane_tk(mm_ctx *ctx, const PlaneGeom &g) {
+    constexpr int NTILE = N1 * N2 / TK;
+    static int cs_env = -1;
+    if (cs_env < 0) {
+        const char *e = getenv("MM_PLANE_CS");
+        cs_env = e ? atoi(e) : 0;
+    }
+    int cs = cs_env > 0 ? cs_env : (N1 * N2 >= 128 ? 4 : N1 * N2 >= 64 ? 2 : 1);
+    while (cs > 1 && (cs > NTILE || NTILE % cs)) cs >>= 1;
+    switch (cs) {
+        case 16: if constexpr (NTILE % 16 == 0) return run_plane_t<N1, N2, TK, 16>(ctx, g); [[fallthrough]];
+        case 8: if constexpr (NTILE % 8 == 0) return run_plane_t<N1, N2, TK, 8>(ctx, g); [[fallthrough]];
+        case 4: if constexpr (NTILE % 4 == 0) return run_plane_t<N1, N2, TK, 4>(ctx, g); [[fallthrough]];
+        case 2: if constexpr (NTILE % 2 == 0) return run_plane_t<N1, N2, TK, 2>(ctx, g); [[fallthrough]];
+        default: return run_plane_t<N1, N2, TK, 1>(ctx, g);
+    }
+}
+
+template <int N1, int N2>
+int run_plane_n(mm_ctx *ctx, const PlaneGeom &g) {
+    static int tk_env = -1;
+    if (tk_env < 0) {
+        const char *e = getenv("MM_PLANE_TK");
+        tk_env = e ? atoi(e) : 8;
+    }
+    if (tk_env == 16 && N1 * N2 >= 64) return run_plane_tk<N1, N2, 16>(ctx, g);
+    if (tk_env == 4) return run_plane_tk<N1, N2, 4>(ctx, g);
+    return run_plane_tk<N1, N2, 8>(ctx, g);
+}
+
+bool plane_eligible(const mm_ctx *ctx) {
+    return ctx->opt_plane && ctx->dim == 3 && !ctx->slab_mode && is_pow2(ctx->n) && ctx->n >= 16 &&
+           ctx->n <= 256;
+}
+
+int run_plane(mm_ctx *ctx, double scale) {
+    PlaneGeom g;
+    g.n = ctx->n;
+    g.nh = ctx->nh;
+    g.sym = ctx->sym;
+    g.thresh = ctx->sym_thresh;
+    g.scale = scale;
+    switch (ctx->n) {
+        case 16: return run_plane_n<4, 4>(ctx, g);
+        case 32: return run_plane_n<8, 4>(ctx, g);
+        case 64: return run_plane_n<8, 8>(ctx, g);
+        case 128: return run_plane_n<16, 8>(ctx, g);
+        case 256: return run_plane_n<16, 16>(ctx, g);
+        default: return mm_fail(ctx, MM_ERR_CONFIG, "plane FFT needs n in 16..256 (pow2)");
+    }
+}
+
 bool g_const_ready[64] = {false};
 
 int ensure_constants(mm_ctx *ctx) {
@@ -1124,12 +1534,13 @@ int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
     int rc = ensure_constants(ctx);
     if (rc) return rc;
     const int n = ctx->n, d = ctx->dim;
+    const bool plane = plane_eligible(ctx);
     // A: divergence + R2C rows (of the T field the fused pass left, when
     // it is current for this rho)
     {
         StageScope ss(ctx, MM_STAGE_ROW_FWD);
         const bool useT = ctx->T_valid && ctx->Tbuf && ctx->T_rho == rho && !ctx->slab_mode;
-        if ((rc = run_rows(ctx, true, rho, nullptr, useT ? ctx->Tbuf : nullptr))) return rc;
+        if ((rc = run_rows(ctx, true, rho, nullptr, useT ? ctx->Tbuf : nullptr, plane))) return rc;
     }
     ColGeom g;
     g.N = n;
@@ -1141,7 +1552,11 @@ int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
     double nd = 1.0;
     for (int i = 0; i < d; ++i) nd *= (double)n;
     g.scale = 1.0 / (2.0 * ctx->h) / nd;
-    if (d == 3) {
+    if (plane) {
+        // B + C + D: one cluster per (component, k2) plane
+        StageScope ss(ctx, MM_STAGE_PLANE);
+        if ((rc = run_plane(ctx, g.scale))) return rc;
+    } else if (d == 3) {
         // spectral index ((c*n + i0)*n + i1)*P + k2
         ColGeom gy = g;
         gy.es = ctx->P;
@@ -1180,7 +1595,7 @@ int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
     }
     {
         StageScope ss(ctx, MM_STAGE_ROW_INV);
-        if ((rc = run_rows(ctx, false, rho, u_new))) return rc;
+        if ((rc = run_rows(ctx, false, rho, u_new, nullptr, plane))) return rc;
     }
     // F: gradient (+ ascent and residual sums)
     Mean9 um, umo;

@@ -354,3 +354,28 @@ def test_device_log_accuracy():
     far = np.abs(x - 1.0) >= 0.3
     assert float(np.max(err[far] / ulp[far])) <= 1.0
     assert np.isneginf(ctx.selftest_log(np.array([0.0])))[0]
+
+
+@pytest.mark.parametrize("n", [16, 32, 64, 128, 256])
+def test_plane_fft_matches_row_layout(n, monkeypatch):
+    """The single-launch cluster pass over (component, k2) planes (k_plane)
+    performs the column sequence's per-line arithmetic; the compiler may
+    contract a complex product's two roundings differently in the two
+    kernels, so whole outer iterations agree with MM_PLANE_FFT=0 (three
+    launches) to roundoff (1e-13 relative L2), the history to 1e-11."""
+    grid, mu, kap = _laminate(3, n, 0)
+    bc = mm.MacroBC.strain(np.diag([0.95, 1.0, 1.0]))
+    m = mm.MooneyRivlin(mu, kap, dim=3, mu_rep=1.0)
+    params = mm.SolverParams(max_outer=3)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("MM_PLANE_FFT", flag)
+        st = mm.solver.init_state(grid, m, bc, params)
+        st.F = st.F + 1e-4 * np.random.default_rng(0).standard_normal(st.F.shape)
+        st, _ = mm.solve(grid, m, bc, params, policy=mm.RatioToDual(0.3), state=st,
+                         raise_on_max=False)
+        out[flag] = (st.F.copy(), st.lam.copy(), st.u_tilde.copy(), st.history[-1][:5])
+    for a, b in zip(out["1"][:3], out["0"][:3]):
+        assert rel_l2(a, b) < 1e-13
+    assert out["1"][3][0] == out["0"][3][0]
+    np.testing.assert_allclose(out["1"][3][1:], out["0"][3][1:], rtol=1e-11)
