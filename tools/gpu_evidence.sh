@@ -1,5 +1,5 @@
-# round evidence: bench line (no profiler), launch list, one full capture per stage kernel,
-# LCE config-3 timing
+# round evidence: bench line (no profiler), reference arm, launch list, one full
+# capture per stage kernel, a 512^3 single-GPU line
 cd /root/repo
 python bench.py > gpurun_out/ev_bench.json 2> gpurun_out/ev_bench.err
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/ev_ref.json 2> gpurun_out/ev_ref.err
@@ -7,7 +7,7 @@ python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ev_plain.log
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ev_launches.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ev_launch.log 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_update_local|k_row_fwd|k_row_inv|k_col|k_res_march" -s 22 -c 8 \
+    -k regex:"k_update_local|k_row_fwd|k_row_inv|k_plane|k_res_march" -s 15 -c 5 \
     -o gpurun_out/ev_full python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ev_full.log 2>&1
-
+timeout 900 python bench.py --n 512 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/ev_bench512.json 2> gpurun_out/ev_bench512.err
 echo done
