@@ -178,6 +178,13 @@ int mm_prepare_frozen(mm_ctx *ctx);
  * the force replaces it in that slot. */
 int mm_frank_stencil(mm_ctx *ctx);
 
+/* Diagnostics: work counters of the 3D LCE Newton kernel, 8 doubles
+ * (multiplier-only sweeps, Newton steps, eliminations, Armijo evaluations,
+ * det-guard trials, fallback passes, fallback evaluations, warp Newton
+ * iterations x 32).  Zeros unless the library was built with
+ * -DMM_LCE_STATS=1 (MM_NVCC_FLAGS); reset != 0 clears them. */
+int mm_debug_lce_counters(double *out, int reset);
+
 /* Helmholtz projection of (F, lam) (projection.py:132-168): writes
  * u_tilde and grad_u = u_mean + D u_tilde on the device.  u_mean (d*d,
  * from macro_gradient, projection.py:125-129) is supplied by the host. */

@@ -43,7 +43,7 @@ EXPORTS = (
     "mm_create_slab", "mm_slab_buffer", "mm_slab_step", "mm_add_field",
     "mm_equilibrium_residual", "mm_selftest_log", "mm_slab_set_peers", "mm_slab_ipc_handle",
     "mm_slab_open_peers", "mm_bloch_setup", "mm_bloch_start", "mm_bloch_iterate",
-    "mm_bloch_mode",
+    "mm_bloch_mode", "mm_debug_lce_counters",
 )
 
 SLAB_HALO_T, SLAB_FWD, SLAB_SOLVE, SLAB_INV, SLAB_HALO_U, SLAB_UPDATE, SLAB_GRAD = range(7)
@@ -156,6 +156,7 @@ def load_library():
             "mm_bloch_start": ([P, P], I),
             "mm_bloch_iterate": ([P, I, D, D, D, D, P], I),
             "mm_bloch_mode": ([P, P], I),
+            "mm_debug_lce_counters": ([P, I], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

@@ -47,7 +47,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         if (not force and os.path.exists(o)
                 and os.path.getmtime(o) >= max(os.path.getmtime(s), newest_hdr)):
             continue
-        flags = list(COMMON)
+        flags = list(COMMON) + os.environ.get("MM_NVCC_FLAGS", "").split()
         if src in NOFMA:
             flags += ["-fmad=false"]
         cmd = [nvcc, *ARCH, *flags, "-c", s, "-o", o]

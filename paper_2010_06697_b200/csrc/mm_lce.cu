@@ -450,6 +450,20 @@ __device__ __forceinline__ bool gauss_smem11(double *S, double (&x)[11]) {
     return true;
 }
 
+// Work counters of the 3D Newton kernel (diagnostics build, -DMM_LCE_STATS=1):
+// 0 multiplier-only sweeps, 1 Newton steps, 2 eliminations (Levenberg tries),
+// 3 Armijo objective evaluations, 4 det-guard trials, 5 gradient-fallback
+// passes, 6 fallback objective evaluations, 7 warp Newton iterations x 32
+#ifndef MM_LCE_STATS
+#define MM_LCE_STATS 0
+#endif
+__device__ unsigned long long g_lce_cnt[8];
+#if MM_LCE_STATS
+#define LCE_CNT(i) (++cnt[i])
+#else
+#define LCE_CNT(i) ((void)0)
+#endif
+
 // slots: 0 sum res^2, 1 n_ok, 2 max nsw, 3..11 sum F
 __global__ void __launch_bounds__(LCE3_THREADS)
 k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ chart,
@@ -469,6 +483,9 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
     const double q = P.q, mur = P.mur, mual = P.mual, rho = P.rho, gam = P.gam;
     const double visF = P.visF, visn = P.visn;
     const double PI = 3.141592653589793;
+#if MM_LCE_STATS
+    unsigned long long cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
          p += (int64_t)gridDim.x * blockDim.x) {
         double Fl[9], E[9];
@@ -604,13 +621,18 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
                 nsw += 1;
                 if (fabs(dJ) > P.det_tol && res <= fmax(P.tol, 0.25 * gam * fabs(dJ))) {
                     pp += gam * dJ;
+                    LCE_CNT(0);
                     continue;
                 }
                 newton = true;
                 break;
             }
+#if MM_LCE_STATS
+            if ((threadIdx.x & 31) == __ffs(__activemask()) - 1) cnt[7] += 32;
+#endif
             if (!newton) break;
             ++it;
+            LCE_CNT(1);
             const double phi0 = phiJ3(Fl, n, n0l, P, pp, D, ffl, nkl);
             // angle-block and cross-term ingredients (lce.py:807-882)
             double ua[3], ub[3];
@@ -734,6 +756,7 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
 #undef AS
 #pragma unroll
                 for (int a = 0; a < 11; ++a) S[(121 + a) * T] = rhs[a];
+                LCE_CNT(2);
                 if (gauss_smem11<T>(S, dv)) {
                     gd = 0.0;
 #pragma unroll
@@ -761,8 +784,10 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
                 }
                 double t = 1.0;
                 double Ft[9];
+                if (pass == 1) LCE_CNT(5);
                 if (decr <= MEAS_EPS * (fabs(phi0) + P.scale)) {
                     for (int bt = 0; bt < 12; ++bt) {
+                        LCE_CNT(4);
 #pragma unroll
                         for (int a = 0; a < 9; ++a) Ft[a] = Fl[a] + t * dv[a];
                         if (det3(Ft) > DET_FLOOR) {
@@ -780,6 +805,7 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
 #pragma unroll
                         for (int a = 0; a < 9; ++a) Ft[a] = Fl[a] + t * dv[a];
                         if (det3(Ft) > DET_FLOOR) {
+                            if (pass == 0) LCE_CNT(3); else LCE_CNT(6);
                             const double ph2 = ph + t * dv[9], th2 = th + t * dv[10];
                             double nt[3];
                             n_from_chart(ph2, th2, E, nt);
@@ -819,6 +845,11 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
         for (int i = 0; i < 9; ++i) acc[3 + i] += Fl[i];
         acc[12] += (double)nsw;
     }
+#if MM_LCE_STATS
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        if (cnt[i]) atomicAdd(&g_lce_cnt[i], cnt[i]);
+#endif
     int ops[13];
 #pragma unroll
     for (int k = 0; k < 13; ++k) ops[k] = RED_SUM;
@@ -952,6 +983,19 @@ int lce_blocks(int64_t M, int threads) {
 }
 
 }  // namespace
+
+// diagnostics: the 3D Newton kernel's work counters (zeros unless built
+// with -DMM_LCE_STATS=1); reset = 1 clears them after the read
+extern "C" int mm_debug_lce_counters(double *out, int reset) {
+    unsigned long long c[8];
+    if (cudaMemcpyFromSymbol(c, g_lce_cnt, sizeof c) != cudaSuccess) return MM_ERR_CUDA;
+    for (int i = 0; i < 8; ++i) out[i] = (double)c[i];
+    if (reset) {
+        const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (cudaMemcpyToSymbol(g_lce_cnt, z, sizeof z) != cudaSuccess) return MM_ERR_CUDA;
+    }
+    return MM_OK;
+}
 
 int mm_run_lce(mm_ctx *ctx, double rho, double tol, int64_t max_sweeps, int want_points,
                mm_local_stats *out) {

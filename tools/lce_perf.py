@@ -34,6 +34,11 @@ def main():
     ctx.synchronize()
     ctx.profile_read(reset=True)
     ctx.profile_enable(True)
+    import ctypes
+    from paper_2010_06697_b200 import _lib
+    cnt = (ctypes.c_double * 8)()
+    lib = _lib.load_library()
+    lib.mm_debug_lce_counters(cnt, 1)
     eng = st._engine
     ps0 = eng.point_sweeps
     t0 = time.perf_counter()
@@ -48,6 +53,13 @@ def main():
     print({k: round(v, 3) for k, v in ms.items() if v}, nl)
     print(f"voxel-iter/s {grid.npoints / wall:.3e}; point sweeps/voxel {psw / grid.npoints:.1f}; "
           f"voxel-sweeps/s {psw / (ms['local'] / 1e3):.3e} (local stage {ms['local']:.1f} ms)")
+    lib.mm_debug_lce_counters(cnt, 1)
+    names = ["multiplier-only sweeps", "Newton steps", "eliminations", "Armijo evaluations",
+             "det-guard trials", "fallback passes", "fallback evaluations",
+             "warp Newton iterations x32"]
+    if any(cnt):
+        for nm, v in zip(names, cnt):
+            print(f"  {nm:28s} {v / grid.npoints:10.2f} per voxel")
 
 
 if __name__ == "__main__":
