@@ -279,7 +279,8 @@ enum mm_option {
     MM_OPT_IMPLICIT_GRAD = 0,
     MM_OPT_STENCIL_MARCH = 1,
     MM_OPT_T_FIELD = 2,
-    MM_OPT_PLANE_FFT = 3
+    MM_OPT_PLANE_FFT = 3,
+    MM_OPT_ROWINV_PIPE = 4  /* default 1: persistent double-buffered C2R rows (plane layout) */
 };
 int mm_set_option(mm_ctx *ctx, int option, int64_t value);
 

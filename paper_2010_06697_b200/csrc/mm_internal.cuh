@@ -79,6 +79,7 @@ struct mm_ctx {
     bool opt_march = true;        // MM_OPT_STENCIL_MARCH
     bool opt_tfield = true;       // MM_OPT_T_FIELD
     bool opt_plane = true;        // MM_OPT_PLANE_FFT
+    bool opt_rowinv_p = true;     // MM_OPT_ROWINV_PIPE
     bool lam_pending = false;     // multiplier ascent deferred by mm_project_residuals
     double pending_rho = 0.0;
     bool g_implicit = false;

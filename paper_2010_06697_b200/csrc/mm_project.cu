@@ -560,38 +560,16 @@ k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho
 // ---------------------------------------------------------------------------
 // E: inverse C2R along rows -> u_tilde (unnormalised; 1/n^d folded into C)
 // ---------------------------------------------------------------------------
+// everything after a tile's spectrum is in buf: Hermitian pair packing,
+// inverse line transform, real rows out (k_row_inv and k_row_inv_p)
 template <int N1, int N2, int DIM, int ROWS>
-__global__ void __launch_bounds__(RowCfg<N1, N2, DIM, ROWS>::NT, RowCfg<N1, N2, DIM, ROWS>::MINB_INV)
-k_row_inv(const double2 *__restrict__ spec, double *__restrict__ Ut, RowGeom g,
-          const double2 *__restrict__ tw_line, const double2 *__restrict__ tw_r2c) {
+__device__ __forceinline__ void row_inv_tile(double2 *buf, double2 *scr, double *__restrict__ Ut,
+                                             const RowGeom &g, int64_t row0, int N, bool packed,
+                                             const double2 *__restrict__ tw_line,
+                                             const double2 *__restrict__ tw_r2c) {
     using C = RowCfg<N1, N2, DIM, ROWS>;
     constexpr int TK = C::TK, LD = TK + 1;
-    extern __shared__ double2 smem_c[];
-    double2 *buf = smem_c;
-    const int N = C::NC ? C::NC : g.N;
-    const bool packed = C::NC ? true : (g.packed != 0);
-    double2 *scr = smem_c + (size_t)(N + 1) * LD;
-    const int64_t row0 = (int64_t)blockIdx.x * ROWS;
     const int nh = packed ? N + 1 : g.n / 2 + 1;
-    for (int w = threadIdx.x; w < TK * nh; w += C::NT) {
-        int line, k;
-        if (g.plane) {
-            const int r0 = w % ROWS, t = w / ROWS;
-            k = t % nh;
-            line = (t / nh) * ROWS + r0;
-        } else {
-            line = w / nh;
-            k = w - line * nh;
-        }
-        const int c = line / ROWS, r = line - c * ROWS;
-        const int64_t row = row0 + r;
-        double2 X = make_double2(0.0, 0.0);
-        if (row < g.nrows)
-            X = g.plane ? spec[((int64_t)c * nh + k) * g.nrows + row]
-                        : spec[((int64_t)c * g.nrows + row) * g.P + k];
-        buf[k * LD + line] = X;
-    }
-    __syncthreads();
     if (packed) {
         // Z[k] = A[k] + i B[k], A = X[k] + conj X[N-k], B = (X[k] - conj X[N-k]) conj(W^k)
         const int npair = N / 2 + 1;
@@ -635,6 +613,41 @@ k_row_inv(const double2 *__restrict__ spec, double *__restrict__ Ut, RowGeom g,
             }
         }
     }
+}
+
+template <int N1, int N2, int DIM, int ROWS>
+__global__ void __launch_bounds__(RowCfg<N1, N2, DIM, ROWS>::NT, RowCfg<N1, N2, DIM, ROWS>::MINB_INV)
+k_row_inv(const double2 *__restrict__ spec, double *__restrict__ Ut, RowGeom g,
+          const double2 *__restrict__ tw_line, const double2 *__restrict__ tw_r2c) {
+    using C = RowCfg<N1, N2, DIM, ROWS>;
+    constexpr int TK = C::TK, LD = TK + 1;
+    extern __shared__ double2 smem_c[];
+    double2 *buf = smem_c;
+    const int N = C::NC ? C::NC : g.N;
+    const bool packed = C::NC ? true : (g.packed != 0);
+    double2 *scr = smem_c + (size_t)(N + 1) * LD;
+    const int64_t row0 = (int64_t)blockIdx.x * ROWS;
+    const int nh = packed ? N + 1 : g.n / 2 + 1;
+    for (int w = threadIdx.x; w < TK * nh; w += C::NT) {
+        int line, k;
+        if (g.plane) {
+            const int r0 = w % ROWS, t = w / ROWS;
+            k = t % nh;
+            line = (t / nh) * ROWS + r0;
+        } else {
+            line = w / nh;
+            k = w - line * nh;
+        }
+        const int c = line / ROWS, r = line - c * ROWS;
+        const int64_t row = row0 + r;
+        double2 X = make_double2(0.0, 0.0);
+        if (row < g.nrows)
+            X = g.plane ? spec[((int64_t)c * nh + k) * g.nrows + row]
+                        : spec[((int64_t)c * g.nrows + row) * g.P + k];
+        buf[k * LD + line] = X;
+    }
+    __syncthreads();
+    row_inv_tile<N1, N2, DIM, ROWS>(buf, scr, Ut, g, row0, N, packed, tw_line, tw_r2c);
 }
 
 // ---------------------------------------------------------------------------
@@ -869,6 +882,48 @@ k_colp(double2 *__restrict__ spec, ColGeom g, const double2 *__restrict__ tw, Ti
             if (w < N * TK && (full || k0 + c < g.ncol)) base[n * g.es + c] = buf[n * LD + c];
         }
         __syncthreads();  // this buffer is refilled two tiles later
+    }
+    cp_async_wait<0>();
+}
+
+// E on the plane layout, persistent and software-pipelined: each block walks
+// tiles t = blockIdx.x, +gridDim.x, ...; the cp.async copies of the next
+// tile's spectrum (ROWS x 16 B runs per (c, k2)) land in the second shared
+// buffer while the current tile is transformed, so loads stay in flight (the
+// one-tile kernel is global-load-latency bound: ncu long_scoreboard).
+template <int N1, int N2, int DIM, int ROWS>
+__global__ void __launch_bounds__(RowCfg<N1, N2, DIM, ROWS>::NT, RowCfg<N1, N2, DIM, ROWS>::MINB_INV)
+k_row_inv_p(const double2 *__restrict__ spec, double *__restrict__ Ut, RowGeom g,
+            const double2 *__restrict__ tw_line, const double2 *__restrict__ tw_r2c, int ntiles) {
+    using C = RowCfg<N1, N2, DIM, ROWS>;
+    constexpr int TK = C::TK, LD = TK + 1, N = N1 * N2, NH = N + 1;
+    extern __shared__ double2 smem_c[];
+    auto issue = [&](int t, double2 *dst) {
+        const int64_t row0 = (int64_t)t * ROWS;
+        for (int w = threadIdx.x; w < TK * NH; w += C::NT) {
+            const int r0 = w % ROWS, tt = w / ROWS;
+            const int k = tt % NH, line = (tt / NH) * ROWS + r0;
+            const int c = line / ROWS;
+            const int64_t row = row0 + r0;
+            const bool ok = row < g.nrows;
+            const double2 *src = spec + ((int64_t)c * NH + k) * g.nrows + (ok ? row : 0);
+            cp_async16(&dst[k * LD + line], src, ok ? 16 : 0);
+        }
+        cp_async_commit();
+    };
+    int t = blockIdx.x;
+    if (t < ntiles) issue(t, smem_c);
+    for (int iter = 0; t < ntiles; t += gridDim.x, ++iter) {
+        double2 *buf = smem_c + (iter & 1) * ((N + 1) * LD);
+        const int tn = t + gridDim.x;
+        if (tn < ntiles) issue(tn, smem_c + ((iter + 1) & 1) * ((N + 1) * LD));
+        else cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        asm volatile("" : "+l"(tw_line), "+l"(tw_r2c));  // twiddle loads stay per tile
+        row_inv_tile<N1, N2, DIM, ROWS>(buf, nullptr, Ut, g, (int64_t)t * ROWS, N, true, tw_line,
+                                        tw_r2c);
+        __syncthreads();  // this buffer is refilled two tiles on
     }
     cp_async_wait<0>();
 }
@@ -1342,6 +1397,20 @@ int run_rows_t(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double
             kern<<<grid, threads, smem, ctx->stream>>>(ctx->F, ctx->Lam, rho, ctx->spec, g,
                                                        tw_line, ctx->tw_r2c);
         }
+    } else if (DIM == 3 && N1 * N2 >= 16 && N1 * N2 <= 128 && g.plane && g.packed &&
+               ctx->opt_rowinv_p) {
+        // persistent, double-buffered (plane layout)
+        auto kern = k_row_inv_p<N1 * N2 >= 16 ? N1 : 4, N1 * N2 >= 16 ? N2 : 4, 3, ROWS>;
+        const size_t smem2 = sizeof(double2) * (size_t)(g.N + 1) * (C::TK + 1) * 2;
+        int rc = launch_smem(ctx, kern, dim3(1), threads, smem2);
+        if (rc) return rc;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem2);
+        if (per_sm < 1) per_sm = 1;
+        const int ntiles = (int)grid.x;
+        const int blocks = std::min(ntiles, per_sm * ctx->num_sms);
+        kern<<<blocks, threads, smem2, ctx->stream>>>(ctx->spec, u_out, g, tw_line, ctx->tw_r2c,
+                                                      ntiles);
     } else {
         auto kern = k_row_inv<N1, N2, DIM, ROWS>;
         int rc = launch_smem(ctx, kern, grid, threads, smem);
