@@ -530,7 +530,14 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
             double n[3], sp, cp, st, ct, u[3], cc, J, dJ, pr, cof[9], gFl[9], gF2, gn[3];
             double m1[3], mth[3], g1, g2, gnn, sp2;
             bool newton = false;
+            // A multiplier-only sweep changes p_inc alone: F, the angles and
+            // the chart stay, so the director, its angle frame, J, cof F and
+            // dW/dn of the next sweep are the values already in registers
+            // (same inputs, same bits).  Only pr and the F-gradient, which
+            // depend on p_inc, are re-evaluated (82 % of polydomain sweeps).
+            bool fresh = true;
             for (; it < P.max_sweeps + 1; ++it) {
+              if (fresh) {
                 // keep the chart's azimuth well conditioned (lce.py:709-730)
                 if (sin(ph) < 0.1) {
                     n_from_chart(ph, th, E, n);
@@ -565,7 +572,6 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
                 cc = u[0] * n0l[0] + u[1] * n0l[1] + u[2] * n0l[2];
                 J = det3(Fl);
                 dJ = J - 1.0;
-                pr = pp + gam * dJ;
                 cof[0] = Fl[4] * Fl[8] - Fl[5] * Fl[7];
                 cof[1] = Fl[5] * Fl[6] - Fl[3] * Fl[8];
                 cof[2] = Fl[3] * Fl[7] - Fl[4] * Fl[6];
@@ -575,18 +581,6 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
                 cof[6] = Fl[1] * Fl[5] - Fl[2] * Fl[4];
                 cof[7] = Fl[2] * Fl[3] - Fl[0] * Fl[5];
                 cof[8] = Fl[0] * Fl[4] - Fl[1] * Fl[3];
-                gF2 = 0.0;
-#pragma unroll
-                for (int i = 0; i < 3; ++i)
-#pragma unroll
-                    for (int j = 0; j < 3; ++j) {
-                        const int a = 3 * i + j;
-                        const double gg = (mur * Fl[a] + q * n[i] * u[j] - mual * cc * n[i] * n0l[j] +
-                                           pr * cof[a] - D.l(a) - rho * (D.g(a) - Fl[a]) +
-                                           visF * (Fl[a] - D.k(a)));
-                        gFl[a] = gg;
-                        gF2 += gg * gg;
-                    }
                 // dW/dn (lce.py:653-663)
                 {
                     const double v0 = Fl[0] * n[0] + Fl[3] * n[1] + Fl[6] * n[2];
@@ -612,6 +606,20 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
                     gnn += gn[i] * n[i];
                 }
                 sp2 = fmax(sp * sp, 1e-4);
+              }
+                pr = pp + gam * dJ;
+                gF2 = 0.0;
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) {
+                        const int a = 3 * i + j;
+                        const double gg = (mur * Fl[a] + q * n[i] * u[j] - mual * cc * n[i] * n0l[j] +
+                                           pr * cof[a] - D.l(a) - rho * (D.g(a) - Fl[a]) +
+                                           visF * (Fl[a] - D.k(a)));
+                        gFl[a] = gg;
+                        gF2 += gg * gg;
+                    }
                 res = sqrt(gF2 + g1 * g1 + g2 * g2 / sp2);
                 if (res < P.tol && fabs(dJ) <= P.det_tol) {
                     converged = true;
@@ -622,6 +630,7 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
                 if (fabs(dJ) > P.det_tol && res <= fmax(P.tol, 0.25 * gam * fabs(dJ))) {
                     pp += gam * dJ;
                     LCE_CNT(0);
+                    fresh = false;
                     continue;
                 }
                 newton = true;
