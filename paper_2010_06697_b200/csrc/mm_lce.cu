@@ -702,17 +702,10 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
             bool found = false;
             for (int lm = 0; lm < 4; ++lm) {
 #define AS(r, c) S[((r) * 11 + (c)) * T]
-                for (int a = 0; a < 11; ++a)
-                    for (int b = 0; b < 11; ++b) AS(a, b) = 0.0;
-                for (int a = 0; a < 9; ++a) AS(a, a) = base;
-#pragma unroll
-                for (int i = 0; i < 3; ++i)
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) {
-                        const double qnn = q * n[i] * n[k];
-#pragma unroll
-                        for (int j = 0; j < 3; ++j) AS(3 * i + j, 3 * k + j) += qnn;
-                    }
+                // F-F block, each entry formed in registers and stored once, with
+                // the terms added in the reference's order: base (diagonal),
+                // q n_i n_k (j = l), gam cof cof - mual w w, pr d^2 J (Levi-Civita,
+                // lce.py:832-845), lam (diagonal)
                 {
                     double wv[9];
 #pragma unroll
@@ -720,29 +713,27 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
 #pragma unroll
                         for (int j = 0; j < 3; ++j) wv[3 * i + j] = n[i] * n0l[j];
 #pragma unroll
-                    for (int a = 0; a < 9; ++a)
-#pragma unroll
-                        for (int b = 0; b < 9; ++b)
-                            AS(a, b) += gam * cof[a] * cof[b] - mual * wv[a] * wv[b];
-                }
-                // pr * d^2 J / dF^2 via the Levi-Civita contraction (lce.py:832-845)
-#pragma unroll
-                for (int i = 0; i < 3; ++i)
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) {
-                        if (k == i) continue;
-                        const int mm_ = 3 - i - k;
-                        const double si = (k == (i + 1) % 3) ? 1.0 : -1.0;
+                    for (int i = 0; i < 3; ++i)
 #pragma unroll
                         for (int j = 0; j < 3; ++j)
 #pragma unroll
-                            for (int l = 0; l < 3; ++l) {
-                                if (l == j) continue;
-                                const int nn = 3 - j - l;
-                                const double sj = (l == (j + 1) % 3) ? 1.0 : -1.0;
-                                AS(3 * i + j, 3 * k + l) += pr * si * sj * Fl[3 * mm_ + nn];
-                            }
-                    }
+                            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                                for (int l = 0; l < 3; ++l) {
+                                    const int a = 3 * i + j, b = 3 * k + l;
+                                    double v = (a == b) ? base : 0.0;
+                                    if (j == l) v += q * n[i] * n[k];
+                                    v += gam * cof[a] * cof[b] - mual * wv[a] * wv[b];
+                                    if (i != k && j != l) {
+                                        const int mm_ = 3 - i - k, nn = 3 - j - l;
+                                        const double si = (k == (i + 1) % 3) ? 1.0 : -1.0;
+                                        const double sj = (l == (j + 1) % 3) ? 1.0 : -1.0;
+                                        v += pr * si * sj * Fl[3 * mm_ + nn];
+                                    }
+                                    if (a == b) v += lam;
+                                    AS(a, b) = v;
+                                }
+                }
 #pragma unroll
                 for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -761,7 +752,8 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
                 AS(9, 10) = h12;
                 AS(10, 9) = h12;
                 AS(10, 10) = h22;
-                for (int a = 0; a < 11; ++a) AS(a, a) += lam;
+                AS(9, 9) += lam;
+                AS(10, 10) += lam;
 #undef AS
 #pragma unroll
                 for (int a = 0; a < 11; ++a) S[(121 + a) * T] = rhs[a];
