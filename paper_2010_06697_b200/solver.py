@@ -31,6 +31,9 @@ from .grid import Grid, mean_field
 from .materials.base import DeviceLocalStats
 from .projection import MacroBC, macro_gradient
 
+# state fields the reference mutates in place during solve()
+INPLACE_FIELDS = ("F", "lam")
+
 __all__ = [
     "SolverParams",
     "Residuals",
@@ -109,6 +112,8 @@ class ADMMState:
         object.__setattr__(self, "_stale", set())   # host copy out of date
         object.__setattr__(self, "_dirty", set())   # host copy must be uploaded
         object.__setattr__(self, "_engine", None)
+        # caller arrays updated in place at the end of solve() (F, lam)
+        object.__setattr__(self, "_inplace", {})
         self.u_mean = np.asarray(u_mean, dtype=float)
         self.F = F
         self.grad_u = grad_u
@@ -143,6 +148,15 @@ class ADMMState:
     def _set(self, name, value):
         if value is not None and name in STATE_FIELDS:
             value = np.asarray(value, dtype=float)
+        # The reference updates F (local_sweeps, base.py:109-111) and lam
+        # (solver.py:279) in place: a writeable contiguous caller array for
+        # either is written back at the end of solve() (_writeback_inplace)
+        if name in INPLACE_FIELDS:
+            if (isinstance(value, np.ndarray) and value.dtype == np.float64
+                    and value.flags.c_contiguous and value.flags.writeable):
+                self._inplace[name] = value
+            else:
+                self._inplace.pop(name, None)
         self._host[name] = value
         self._stale.discard(name)
         self._dev.discard(name)
@@ -150,6 +164,25 @@ class ADMMState:
             self._dirty.add(name)
         else:
             self._dirty.discard(name)
+
+    def _writeback_inplace(self):
+        """Download F and lam into the caller's arrays they were given as
+        (the reference mutates those arrays in place); the arrays become the
+        state's read-only snapshots, as any downloaded field."""
+        eng = self._engine
+        if eng is None:
+            return
+        for nm in INPLACE_FIELDS:
+            target = self._inplace.pop(nm, None)
+            if target is None or nm not in self._stale:
+                continue
+            fid, rank = STATE_FIELDS[nm]
+            if target.shape != field_shape(eng.grid, rank):
+                continue
+            eng.ctx.download_into(fid, target)
+            target.flags.writeable = False
+            self._host[nm] = target
+            self._stale.discard(nm)
 
     def _mark_device(self, *names):
         """Fields just rewritten on the device: host copies are stale."""
@@ -436,6 +469,7 @@ def solve(grid: Grid, model, bc: MacroBC, params: SolverParams,
                     and resid.r_l <= r_l_tol):
                 converged = True
                 break
+    state._writeback_inplace()
     if not converged and raise_on_max:
         raise ConvergenceError(
             f"no convergence in {params.max_outer} outer iterations "

@@ -186,7 +186,7 @@ def test_3d_laminate_matches_oracle(n, K):
     params = mm.SolverParams(max_outer=K)
     st = mm.solver.init_state(grid, m, bc, params)
     F0 = st.F + 1e-4 * np.random.default_rng(0).standard_normal(st.F.shape)
-    st.F = F0
+    st.F = F0.copy()  # solve() writes F back into the array it was given
     st, _ = mm.solve(grid, m, bc, params, policy=mm.RatioToDual(0.3), state=st,
                      raise_on_max=False)
     om = oracle.MR(mu, kap, dim=3, mu_rep=1.0)
@@ -379,3 +379,32 @@ def test_plane_fft_matches_row_layout(n, monkeypatch):
         assert rel_l2(a, b) < 1e-13
     assert out["1"][3][0] == out["0"][3][0]
     np.testing.assert_allclose(out["1"][3][1:], out["0"][3][1:], rtol=1e-11)
+
+
+def test_solve_updates_caller_F_and_lam_in_place():
+    """The reference's local step writes F in place (base.py:109-111) and the
+    ascent does lam += ... (solver.py:279): arrays the caller handed in as F
+    and lam hold the final values after solve(), and are the state's
+    (read-only) F and lam; a read-only caller array is left untouched."""
+    grid, mu, kap = _laminate(3, 8, 0)
+    bc = mm.MacroBC.strain(np.diag([0.95, 1.0, 1.0]))
+    m = mm.MooneyRivlin(mu, kap, dim=3, mu_rep=1.0)
+    params = mm.SolverParams(max_outer=5)
+    runs = []
+    for writeable in (True, False):
+        st = mm.solver.init_state(grid, m, bc, params)
+        F0 = np.ascontiguousarray(st.F + 1e-4 * np.random.default_rng(0).standard_normal(st.F.shape))
+        lam0 = np.zeros_like(F0)
+        keep = (F0.copy(), lam0.copy())
+        F0.flags.writeable = writeable
+        lam0.flags.writeable = writeable
+        st.F, st.lam = F0, lam0
+        st, _ = mm.solve(grid, m, bc, params, policy=mm.RatioToDual(0.3), state=st,
+                         raise_on_max=False)
+        if writeable:
+            assert st.F is F0 and st.lam is lam0
+            assert not F0.flags.writeable
+        else:
+            assert np.array_equal(F0, keep[0]) and np.array_equal(lam0, keep[1])
+        runs.append((np.array(st.F), np.array(st.lam)))
+    assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][1], runs[1][1])

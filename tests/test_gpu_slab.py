@@ -46,8 +46,9 @@ def test_slab_solver_matches_single_gpu(n, P, K, exchange):
     pol = mm.RatioToDual(0.3)
     # single context
     model = mm.MooneyRivlin(mu, kap, dim=3, mu_rep=1.0)
+    # copies: solve() writes F and lam back into the arrays it was given
     st = mm.ADMMState(u_mean=bc.value.copy(), u_tilde=np.zeros(grid.shape + (3,)), grad_u=G,
-                      F=F, lam=lam, internal={}, rho=1.0)
+                      F=F.copy(), lam=lam.copy(), internal={}, rho=1.0)
     st, _ = mm.solve(grid, model, bc, params, policy=pol, state=st, raise_on_max=False)
     # P virtual ranks
     shared = {"P": P, "barrier": threading.Barrier(P), "slots": {}}
