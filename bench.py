@@ -325,8 +325,10 @@ def run_ours(args, rank, world, dist):
                 "d2h_bytes_per_step": d2h / args.steps,
                 "how": "solve(max_outer=K) on a host (pinned) state: engine creation (device "
                        "memory from the process's stream-ordered pool, warm after the timed "
-                       "run), H2D of F, grad_u, lam, u_tilde, moduli, K iterations, D2H of F, "
-                       "grad_u, lam, u_tilde into fresh host arrays; wall clock"},
+                       "run), H2D of F, grad_u, lam, u_tilde, moduli, K iterations, D2H of F "
+                       "and lam back into the caller's (pinned) arrays, as the reference "
+                       "updates both in place, and of grad_u, u_tilde into fresh host arrays; "
+                       "wall clock"},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.cpu_n, args.cpu_steps)
