@@ -1527,7 +1527,10 @@ int run_plane_t(mm_ctx *ctx, const PlaneGeom &g) {
     return MM_OK;
 }
 
-// cluster size per plane (MM_PLANE_CS overrides; tiles per pass must divide)
+// cluster size per plane (MM_PLANE_CS overrides; tiles per pass must divide).
+// 256^3: 8 CTAs per plane keeps ~52 planes (52 MB) in flight, which stay in
+// L2 between the passes (DRAM 1.11x the algorithmic bytes); 4 per plane ran
+// 104 planes and moved 2.2x at the same time (ncu, tools/gpu_ncu_plane.sh)
 template <int N1, int N2, int TK>
 int run_plane_tk(mm_ctx *ctx, const PlaneGeom &g) {
     constexpr int NTILE = N1 * N2 / TK;
@@ -1536,7 +1539,7 @@ int run_plane_tk(mm_ctx *ctx, const PlaneGeom &g) {
         const char *e = getenv("MM_PLANE_CS");
         cs_env = e ? atoi(e) : 0;
     }
-    int cs = cs_env > 0 ? cs_env : (N1 * N2 >= 128 ? 4 : N1 * N2 >= 64 ? 2 : 1);
+    int cs = cs_env > 0 ? cs_env : (N1 * N2 >= 256 ? 8 : N1 * N2 >= 128 ? 4 : N1 * N2 >= 64 ? 2 : 1);
     while (cs > 1 && (cs > NTILE || NTILE % cs)) cs >>= 1;
     switch (cs) {
         case 16: if constexpr (NTILE % 16 == 0) return run_plane_t<N1, N2, TK, 16>(ctx, g); [[fallthrough]];
