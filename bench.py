@@ -168,7 +168,7 @@ def run_ours(args, rank, world, dist):
     import paper_2010_06697_b200 as mm
     from paper_2010_06697_b200 import _lib
 
-    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = bench_device()
     torch.cuda.set_device(dev)
     n = args.n
     M = n ** 3
@@ -336,6 +336,11 @@ def run_ours(args, rank, world, dist):
         print(json.dumps(line), flush=True)
 
 
+def bench_device():
+    """CUDA device of this rank: LOCAL_RANK, or MM_BENCH_DEVICE when set."""
+    return int(os.environ.get("MM_BENCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+
+
 def run_slab(args, rank, world, dist):
     """N > 1: the same n^3 problem split into N slabs along axis 0 (one per
     GPU), projection transposes as NCCL all-to-alls (paper_2010_06697_b200/
@@ -345,7 +350,7 @@ def run_slab(args, rank, world, dist):
     import paper_2010_06697_b200 as mm
     from paper_2010_06697_b200.slab import SlabLayout, SlabSolver, TorchComm
 
-    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = bench_device()
     torch.cuda.set_device(dev)
     n = args.n
     lay = SlabLayout(n, world, rank, 0.5)
@@ -512,8 +517,11 @@ def main():
         import torch.distributed as tdist
 
         backend = "nccl" if args.impl == "ours" else "gloo"
+        # MM_BENCH_BACKEND / MM_BENCH_DEVICE: exercise the N > 1 path with all
+        # ranks on one GPU (gloo; NCCL refuses two ranks per device)
+        backend = os.environ.get("MM_BENCH_BACKEND", backend)
         if args.impl == "ours":
-            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+            torch.cuda.set_device(bench_device())
         tdist.init_process_group(backend=backend)
         dist = tdist
     try:
