@@ -30,7 +30,10 @@ constexpr double BT_SHRINK = 0.5;     // base.py:38
 constexpr int MAX_BT = 60;            // base.py:39
 constexpr double MEAS_EPS = 64.0 * 2.220446049250313e-16;  // base.py:41
 
-constexpr int LOCAL_THREADS = 128;
+#ifndef MM_LOCAL_THREADS
+#define MM_LOCAL_THREADS 128
+#endif
+constexpr int LOCAL_THREADS = MM_LOCAL_THREADS;
 #ifndef LOCAL_MIN_BLOCKS
 #define LOCAL_MIN_BLOCKS 4
 #endif
@@ -110,7 +113,7 @@ static double gs_threshold(double tol) {
 
 inline int local_blocks(int64_t M) {
     int64_t b = (M + LOCAL_THREADS - 1) / LOCAL_THREADS;
-    return (int)std::min<int64_t>(b, 148 * 16);
+    return (int)std::min<int64_t>(b, 148 * 16 * 128 / LOCAL_THREADS);
 }
 
 // One point of the compiled 2D kernel (mooney_rivlin.py:169-255).
