@@ -144,12 +144,11 @@ __device__ __forceinline__ void tile_fft(double2 *buf, const double2 *__restrict
     }
 }
 
-// tile_fft with the direction a runtime argument: the same arithmetic as
-// tile_fft<..., INV> (twiddle imaginary parts and the +-i rotations selected,
-// not recomputed), bit for bit.  One instantiation serves both directions,
-// so a forward and an inverse transform in one loop body share one register
-// allocation (inlined compile-time pairs keep values of the first live into
-// the second and spill).
+// In-register radix-2 FFT with the direction a runtime argument (twiddle
+// imaginary parts and the +-i rotations selected): one instantiation serves
+// both directions, so the forward and inverse transforms of the plane pass's
+// solve step share one register allocation (inlined compile-time pairs kept
+// values of the first live into the second and spilled).
 template <int R>
 __device__ __forceinline__ void fft_reg_rt(double2 (&v)[R], bool inv) {
     if constexpr (R > 1) {
@@ -185,50 +184,6 @@ __device__ __forceinline__ void fft_reg_rt(double2 (&v)[R], bool inv) {
             }
         }
     }
-}
-
-template <int N1, int N2, int TK>
-__device__ __forceinline__ void tile_fft_rt(double2 *buf, const double2 *__restrict__ tw, bool inv) {
-    constexpr int LD = TK + 1;
-    const int tid = threadIdx.x;
-    const int c = tid % TK;
-    static_assert(N2 > 1, "four-step tiles only");
-    double2 v[N1];
-    const int n2 = tid / TK;
-    const bool act1 = tid < TK * N2;
-    if (act1) {
-#pragma unroll
-        for (int n1 = 0; n1 < N1; ++n1) v[n1] = buf[(N2 * n1 + n2) * LD + c];
-        fft_reg_rt<N1>(v, inv);
-#pragma unroll
-        for (int k1 = 1; k1 < N1; ++k1) {
-            if (n2 != 0) {
-                double2 w = __ldg(&tw[n2 * k1]);
-                if (inv) w.y = -w.y;
-                v[k1] = cmul(v[k1], w);
-            }
-        }
-    }
-    __syncthreads();
-    if (act1) {
-#pragma unroll
-        for (int k1 = 0; k1 < N1; ++k1) buf[(k1 * N2 + n2) * LD + c] = v[k1];
-    }
-    __syncthreads();
-    double2 u[N2];
-    const int k1 = tid / TK;
-    const bool act2 = tid < TK * N1;
-    if (act2) {
-#pragma unroll
-        for (int j = 0; j < N2; ++j) u[j] = buf[(k1 * N2 + j) * LD + c];
-        fft_reg_rt<N2>(u, inv);
-    }
-    __syncthreads();
-    if (act2) {
-#pragma unroll
-        for (int k2 = 0; k2 < N2; ++k2) buf[(k1 + N1 * k2) * LD + c] = u[k2];
-    }
-    __syncthreads();
 }
 
 // Stockham autosort FFT of TK lines held in shared memory (element n of
