@@ -96,6 +96,14 @@ class ClockSampler:
         self.th = threading.Thread(target=self._read, daemon=True)
         self.th.start()
 
+    def wait_ready(self, timeout=3.0):
+        """Block until nvidia-smi delivers its first sample (its start-up takes
+        longer than a short timed region), then drop the pre-region samples."""
+        t_end = time.perf_counter() + timeout
+        while self.proc is not None and not self.rows and time.perf_counter() < t_end:
+            time.sleep(0.005)
+        self.rows = []
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
@@ -184,10 +192,11 @@ def run_ours(args, rank, world, dist):
     ctx.profile_read(reset=True)
     ctx.profile_enable(True)
     sampler = ClockSampler(dev)
+    sampler.start()
+    sampler.wait_ready()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler.start()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     # the library runs on its own stream; bracket it from the torch stream with
@@ -384,9 +393,10 @@ def run_slab(args, rank, world, dist):
     sv.ctx.profile_read(reset=True)
     sv.ctx.profile_enable(True)
     sampler = ClockSampler(dev)
+    sampler.start()
+    sampler.wait_ready()
     dist.barrier()
     torch.cuda.synchronize()
-    sampler.start()
     w0 = time.perf_counter()
     sv.solve(max_outer=args.steps)
     sv.ctx.synchronize()
