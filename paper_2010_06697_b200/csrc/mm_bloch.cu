@@ -432,6 +432,7 @@ extern "C" {
 int mm_bloch_setup(mm_ctx *ctx, const double *Minv, const double *Lmat, const double *shift,
                    const double *bsq, const uint8_t *live, double rho, double target) {
     if (!ctx || !Minv || !Lmat || !shift || !bsq || !live) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     if (ctx->points_only || ctx->slab_mode)
         return mm_fail(ctx, MM_ERR_CONFIG, "Bloch analysis needs a full-grid context");
     if (ctx->n > 2048) return mm_fail(ctx, MM_ERR_CONFIG, "Bloch lines limited to n <= 2048");
@@ -489,6 +490,7 @@ int mm_bloch_setup(mm_ctx *ctx, const double *Minv, const double *Lmat, const do
 // modes and scaled to the target norm (stability.py:236-242); g = 0.
 int mm_bloch_start(mm_ctx *ctx, const double *p) {
     if (!ctx || !p) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     mm_bloch_state *b = ctx->bloch;
     if (!b) return mm_fail(ctx, MM_ERR_CONFIG, "mm_bloch_setup was not called");
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
@@ -530,6 +532,7 @@ int mm_bloch_start(mm_ctx *ctx, const double *p) {
 int mm_bloch_iterate(mm_ctx *ctx, int max_iter, double tol_beta, double tol_primal,
                      double floor_, double mu_rep, double *out) {
     if (!ctx || !out) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     mm_bloch_state *b = ctx->bloch;
     if (!b) return mm_fail(ctx, MM_ERR_CONFIG, "mm_bloch_setup was not called");
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
@@ -617,6 +620,7 @@ int mm_bloch_iterate(mm_ctx *ctx, int max_iter, double tol_beta, double tol_prim
 // p = IFFT(phat) (1/npts), complex AoS
 int mm_bloch_mode(mm_ctx *ctx, double *p_out) {
     if (!ctx || !p_out) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     mm_bloch_state *b = ctx->bloch;
     if (!b) return mm_fail(ctx, MM_ERR_CONFIG, "mm_bloch_setup was not called");
     MM_CUDA(ctx, cudaSetDevice(ctx->device));

@@ -609,6 +609,7 @@ int mm_slab_buffer(mm_ctx *ctx, int which, void **dev_ptr, int64_t *nbytes) {
 
 int mm_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, double *sums) {
     if (!ctx) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     if (!ctx->slab_mode) return mm_fail(ctx, MM_ERR_CONFIG, "not a slab context");
     if (!(rho > 0.0) || !isfinite(rho))
         return mm_fail(ctx, MM_ERR_PARAM, "rho must be positive and finite, got %g", rho);
@@ -633,6 +634,7 @@ static int peer_table(mm_ctx *ctx, int which, double2 ****slot) {
 
 int mm_slab_set_peers(mm_ctx *ctx, int which, void *const *ptrs, int P) {
     if (!ctx || !ptrs) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     if (P != ctx->slab_P) return mm_fail(ctx, MM_ERR_CONFIG, "expected %d peers, got %d", ctx->slab_P, P);
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
     double2 ***slot;
@@ -658,6 +660,7 @@ int mm_slab_ipc_handle(mm_ctx *ctx, int which, void *handle_out) {
 
 int mm_slab_open_peers(mm_ctx *ctx, int which, const void *handles, int P) {
     if (!ctx || !handles) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     if (P != ctx->slab_P) return mm_fail(ctx, MM_ERR_CONFIG, "expected %d peers, got %d", ctx->slab_P, P);
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
     std::vector<void *> ptrs(P);
@@ -725,6 +728,7 @@ void mm_destroy(mm_ctx *ctx) {
     if (ctx->recvbuf) cudaFree(ctx->recvbuf);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->host_out) cudaFreeHost(ctx->host_out);
+    if (ctx->ev_red) cudaEventDestroy(ctx->ev_red);
     if (ctx->xfer_ev[0]) cudaEventDestroy(ctx->xfer_ev[0]);
     if (ctx->xfer_ev[1]) cudaEventDestroy(ctx->xfer_ev[1]);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -764,6 +768,7 @@ int mm_profile_read(mm_ctx *ctx, mm_profile *out, int reset) {
 
 int mm_upload(mm_ctx *ctx, int field, const double *host, int64_t count) {
     if (!ctx || !host) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     {
         int prc = mm_flush_pending(ctx);
         if (prc) return prc;
@@ -796,6 +801,7 @@ int mm_upload(mm_ctx *ctx, int field, const double *host, int64_t count) {
 
 int mm_add_field(mm_ctx *ctx, int field, const double *host, int64_t count) {
     if (!ctx || !host) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     {
         int prc = mm_flush_pending(ctx);
         if (prc) return prc;
@@ -818,6 +824,7 @@ int mm_add_field(mm_ctx *ctx, int field, const double *host, int64_t count) {
 
 int mm_equilibrium_residual(mm_ctx *ctx, int material, double dt, double *out) {
     if (!ctx || !out) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
     if (ctx->slab_mode)
         return mm_fail(ctx, MM_ERR_CONFIG, "equilibrium_residual is single-context only");
@@ -849,6 +856,7 @@ int mm_equilibrium_residual(mm_ctx *ctx, int material, double dt, double *out) {
 
 int mm_download(mm_ctx *ctx, int field, double *host, int64_t count) {
     if (!ctx || !host) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     {
         int prc = mm_flush_pending(ctx);
         if (prc) return prc;
@@ -868,6 +876,7 @@ int mm_download(mm_ctx *ctx, int field, double *host, int64_t count) {
 
 int mm_copy_field(mm_ctx *ctx, int dst_field, int src_field) {
     if (!ctx) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     {
         int prc = mm_flush_pending(ctx);
         if (prc) return prc;
@@ -916,6 +925,7 @@ int mm_field_sums(mm_ctx *ctx, int field, double *out) {
 
 int mm_set_symbols(mm_ctx *ctx, const double *axis_tab, double threshold) {
     if (!ctx || !axis_tab) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
     MM_CUDA(ctx, cudaMemcpy(ctx->sym, axis_tab, sizeof(double) * ctx->dim * ctx->n,
@@ -927,6 +937,7 @@ int mm_set_symbols(mm_ctx *ctx, const double *axis_tab, double threshold) {
 
 int mm_set_lce(mm_ctx *ctx, const mm_lce_params *p) {
     if (!ctx || !p) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     ctx->lce = *p;
     ctx->have_lce = true;
     return MM_OK;
@@ -935,6 +946,7 @@ int mm_set_lce(mm_ctx *ctx, const mm_lce_params *p) {
 int mm_local_sweeps(mm_ctx *ctx, int material, double rho, double tol, int64_t max_sweeps,
                     double phi_scale, int want_points, mm_local_stats *out) {
     if (!ctx || !out) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     if (!(rho > 0.0) || !isfinite(rho))
         return mm_fail(ctx, MM_ERR_PARAM, "rho must be positive and finite, got %g", rho);
     if (max_sweeps < 0) return mm_fail(ctx, MM_ERR_PARAM, "max_sweeps must be >= 0");
@@ -977,6 +989,7 @@ int mm_download_points(mm_ctx *ctx, double *res, int64_t *nsw, uint8_t *ok, int6
 
 int mm_prepare_frozen(mm_ctx *ctx) {
     if (!ctx) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     if (!ctx->have_lce) return mm_fail(ctx, MM_ERR_CONFIG, "LCE parameters were never set");
     if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
@@ -987,6 +1000,7 @@ int mm_prepare_frozen(mm_ctx *ctx) {
 
 int mm_project(mm_ctx *ctx, double rho, const double *u_mean) {
     if (!ctx || !u_mean) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     if (ctx->slab_mode) return mm_fail(ctx, MM_ERR_CONFIG, "slab context: use mm_slab_step");
     if (!(rho > 0.0) || !isfinite(rho))
         return mm_fail(ctx, MM_ERR_PARAM, "rho must be positive and finite, got %g", rho);
@@ -1013,6 +1027,7 @@ int mm_project_residuals(mm_ctx *ctx, double rho, const double *u_mean, mm_updat
 
 int mm_update_multiplier(mm_ctx *ctx, mm_update_stats *out) {
     if (!ctx || !out) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
     return mm_run_update(ctx, 0, 0.0, 0.0, 0, 0.0, 0, nullptr, out);
 }
@@ -1021,6 +1036,7 @@ int mm_update_and_sweep(mm_ctx *ctx, int material, double rho_next, double tol,
                         int64_t max_sweeps, double phi_scale, int want_points,
                         mm_local_stats *ls, mm_update_stats *us) {
     if (!ctx || !ls || !us) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     if (!(rho_next > 0.0) || !isfinite(rho_next))
         return mm_fail(ctx, MM_ERR_PARAM, "rho must be positive and finite, got %g", rho_next);
     if (max_sweeps < 0) return mm_fail(ctx, MM_ERR_PARAM, "max_sweeps must be >= 0");
@@ -1034,6 +1050,7 @@ int mm_update_and_sweep(mm_ctx *ctx, int material, double rho_next, double tol,
 
 int mm_project_update(mm_ctx *ctx, double rho, const double *u_mean, mm_update_stats *out) {
     if (!ctx || !u_mean || !out) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     if (ctx->slab_mode) return mm_fail(ctx, MM_ERR_CONFIG, "slab context: use mm_slab_step");
     if (!(rho > 0.0) || !isfinite(rho))
         return mm_fail(ctx, MM_ERR_PARAM, "rho must be positive and finite, got %g", rho);
@@ -1047,6 +1064,7 @@ int mm_project_update(mm_ctx *ctx, double rho, const double *u_mean, mm_update_s
 
 int mm_set_option(mm_ctx *ctx, int option, int64_t value) {
     if (!ctx) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     switch (option) {
         case MM_OPT_IMPLICIT_GRAD: {
             const bool on = value != 0;
@@ -1065,12 +1083,14 @@ int mm_set_option(mm_ctx *ctx, int option, int64_t value) {
             return MM_OK;
         case MM_OPT_PLANE_FFT: ctx->opt_plane = value != 0; return MM_OK;
         case MM_OPT_ROWINV_PIPE: ctx->opt_rowinv_p = value != 0; return MM_OK;
+        case MM_OPT_SPECULATE: ctx->opt_speculate = value != 0; return MM_OK;
         default: return mm_fail(ctx, MM_ERR_PARAM, "unknown option %d", option);
     }
 }
 
 int mm_frank_stencil(mm_ctx *ctx) {
     if (!ctx) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
     if (!ctx->have_lce) return mm_fail(ctx, MM_ERR_CONFIG, "LCE parameters were never set");
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
@@ -1079,6 +1099,7 @@ int mm_frank_stencil(mm_ctx *ctx) {
 
 int mm_stencil(mm_ctx *ctx, int op) {
     if (!ctx) return MM_ERR_PARAM;
+    ctx->gen++;  // invalidates a speculative projection front
     if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
     if (op != 0 && op != 1) return mm_fail(ctx, MM_ERR_PARAM, "unknown stencil op %d", op);
     MM_CUDA(ctx, cudaSetDevice(ctx->device));

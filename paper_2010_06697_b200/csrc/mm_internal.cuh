@@ -80,6 +80,15 @@ struct mm_ctx {
     bool opt_tfield = true;       // MM_OPT_T_FIELD
     bool opt_plane = true;        // MM_OPT_PLANE_FFT
     bool opt_rowinv_p = true;     // MM_OPT_ROWINV_PIPE
+    bool opt_speculate = true;    // MM_OPT_SPECULATE
+    // speculative projection front (A, column passes, E of the next
+    // iteration launched by mm_update_and_sweep behind the fused pass): valid
+    // for front_rho while no other entry point ran since (gen unchanged)
+    uint64_t gen = 0;
+    bool front_valid = false;
+    double front_rho = 0.0;
+    uint64_t front_gen = 0;
+    cudaEvent_t ev_red = nullptr;
     bool lam_pending = false;     // multiplier ascent deferred by mm_project_residuals
     double pending_rho = 0.0;
     bool g_implicit = false;
@@ -297,6 +306,7 @@ int mm_run_local(mm_ctx *ctx, int material, double rho, double tol, int64_t max_
                  double phi_scale, int want_points, mm_local_stats *out);
 int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
                    mm_update_stats *out);
+int mm_run_project_front(mm_ctx *ctx, double rho, int update, double **u_new_out);
 int mm_run_frozen(mm_ctx *ctx);
 int mm_run_field_sums(mm_ctx *ctx, const double *field, int ncomp, double *out);
 int mm_run_stress(mm_ctx *ctx, int material, double *P);

@@ -1031,7 +1031,29 @@ int mm_run_update(mm_ctx *ctx, int material, double rho_next, double tol, int64_
     }
     double r[MM_MAX_PARTIALS];
     const int K = 5 + 2 * D;
-    if ((rc = mm_fetch_reduction(ctx, K, r))) return rc;
+    // Speculative front: the next projection's A / column passes / E depend
+    // only on the T field this pass writes (for rho_next), so they are queued
+    // right behind it and run while the host waits for this pass's sums and
+    // takes its decisions; mm_project_residuals uses them when nothing else
+    // ran in between (generation count) and rho is rho_next, else recomputes.
+    const bool spec = sweep && ctx->opt_speculate && !ctx->slab_mode && !ctx->points_only &&
+                      ctx->have_sym && ctx->T_valid && ctx->T_rho == rho_next;
+    ctx->front_valid = false;
+    if (spec) {
+        if (!ctx->ev_red) MM_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_red, cudaEventDisableTiming));
+        MM_CUDA(ctx, cudaMemcpyAsync(ctx->host_out, ctx->red_out, sizeof(double) * K,
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+        MM_CUDA(ctx, cudaEventRecord(ctx->ev_red, ctx->stream));
+        double *u_new = nullptr;
+        if ((rc = mm_run_project_front(ctx, rho_next, 2, &u_new))) return rc;
+        ctx->front_valid = true;
+        ctx->front_rho = rho_next;
+        ctx->front_gen = ctx->gen;
+        MM_CUDA(ctx, cudaEventSynchronize(ctx->ev_red));
+        memcpy(r, ctx->host_out, sizeof(double) * K);
+    } else if ((rc = mm_fetch_reduction(ctx, K, r))) {
+        return rc;
+    }
     for (int i = 0; i < 9; ++i) us->sum_lam[i] = i < D ? r[4 + D + i] : 0.0;
     if (sweep) {
         ls->sum_res2 = r[0];
@@ -1064,6 +1086,7 @@ __global__ void k_selftest_log(const double *__restrict__ x, double *__restrict_
 }  // namespace
 
 extern "C" int mm_selftest_log(mm_ctx *ctx, const double *x, double *y, int64_t n) {
+    if (ctx) ctx->gen++;
     if (!ctx || !x || !y || n < 0) return MM_ERR_PARAM;
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
     int rc = ensure_logtab(ctx);

@@ -1556,8 +1556,9 @@ int ensure_constants(mm_ctx *ctx) {
 
 }  // namespace
 
-int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
-                   mm_update_stats *out) {
+// A (divergence + R2C rows), the column passes with the solve, E (C2R rows
+// -> u_new): the part of the projection that does not need u_mean
+int mm_run_project_front(mm_ctx *ctx, double rho, int update, double **u_new_out) {
     int rc = ensure_constants(ctx);
     if (rc) return rc;
     const int n = ctx->n, d = ctx->dim;
@@ -1624,6 +1625,23 @@ int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
         StageScope ss(ctx, MM_STAGE_ROW_INV);
         if ((rc = run_rows(ctx, false, rho, u_new, nullptr, plane))) return rc;
     }
+    *u_new_out = u_new;
+    return MM_OK;
+}
+
+int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
+                   mm_update_stats *out) {
+    int rc;
+    const int n = ctx->n, d = ctx->dim;
+    double *u_new = nullptr;
+    if (update == 2 && ctx->front_valid && ctx->front_rho == rho && ctx->front_gen == ctx->gen &&
+        ctx->Ut2) {
+        u_new = ctx->Ut2;  // launched by mm_update_and_sweep behind the fused pass
+    } else if ((rc = mm_run_project_front(ctx, rho, update, &u_new))) {
+        ctx->front_valid = false;
+        return rc;
+    }
+    ctx->front_valid = false;
     // F: gradient (+ ascent and residual sums)
     Mean9 um, umo;
     for (int i = 0; i < 9; ++i) {

@@ -408,3 +408,30 @@ def test_solve_updates_caller_F_and_lam_in_place():
             assert np.array_equal(F0, keep[0]) and np.array_equal(lam0, keep[1])
         runs.append((np.array(st.F), np.array(st.lam)))
     assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][1], runs[1][1])
+
+
+@pytest.mark.parametrize("n,K", [(16, 12), (64, 6)])
+def test_speculative_projection_front_is_exact(n, K, monkeypatch):
+    """mm_update_and_sweep queues the next projection's rows / column passes /
+    C2R behind the fused pass (MM_OPT_SPECULATE); whether they are used or
+    recomputed (an extra local chunk, a host access in between), every field
+    and the history equal the non-speculative run bit for bit."""
+    grid, mu, kap = _laminate(3, n, 0)
+    bc = mm.MacroBC.strain(np.diag([0.95, 1.0, 1.0]))
+    m = mm.MooneyRivlin(mu, kap, dim=3, mu_rep=1.0)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("MM_SPECULATE", flag)
+        params = mm.SolverParams(max_outer=K // 2)
+        st = mm.solver.init_state(grid, m, bc, params)
+        st.F = st.F + 1e-3 * np.random.default_rng(0).standard_normal(st.F.shape)
+        st, _ = mm.solve(grid, m, bc, params, policy=mm.RatioToDual(0.3), state=st,
+                         raise_on_max=False)
+        _ = st.grad_u  # host access between two solves
+        st, _ = mm.solve(grid, m, bc, params, policy=mm.RatioToDual(0.3), state=st,
+                         raise_on_max=False)
+        out[flag] = ([np.array(getattr(st, k)) for k in ("F", "lam", "grad_u", "u_tilde")],
+                     [r[:5] for r in st.history], st.total_sweeps)
+    for a, b in zip(out["1"][0], out["0"][0]):
+        assert np.array_equal(a, b)
+    assert out["1"][1] == out["0"][1] and out["1"][2] == out["0"][2]
