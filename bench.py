@@ -40,14 +40,22 @@ F_SWEEP_MR3 = 170.0
 
 
 def fp64_peak_tflops():
-    """Nominal FP64 (non-tensor) peak: 148 SMs x 64 DFMA/clk x 2 x max SM clock."""
+    """FP64 (non-tensor) peak: the DFMA microbenchmark measured on this pool's
+    B200s (profiles/fp64_peak.json, tools/microbench/fp64_peak.cu), else the
+    nominal 148 SMs x 64 DFMA/clk x 2 x max SM clock.  Returns (TF/s, source)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            return float(json.load(f)["fp64_dfma_tflops"]), \
+                "measured DFMA microbenchmark (profiles/fp64_peak.json)"
+    except Exception:
+        pass
     mhz = 1965.0
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             mhz = float(json.load(f).get("sm_max_mhz", mhz))
     except Exception:
         pass
-    return 148 * 64 * 2 * mhz * 1e6 / 1e12
+    return 148 * 64 * 2 * mhz * 1e6 / 1e12, "nominal 148 SM x 64 DFMA/clk x 2 x sm_max_mhz"
 
 
 def laminate(n, dim=3):
@@ -294,12 +302,12 @@ def run_ours(args, rank, world, dist):
     local_fp64 = None
     if local_ms > 0 and point_sweeps > 0:
         tf = point_sweeps * F_SWEEP_MR3 / (local_ms / 1e3) / 1e12
-        pk = fp64_peak_tflops()
+        pk, pk_src = fp64_peak_tflops()
         local_fp64 = {"bound": "fp64", "stages": ["local", "fused"],
                       "point_sweeps_per_voxel_iter": round(point_sweeps / (M * args.steps), 3),
                       "flop_per_sweep": F_SWEEP_MR3, "achieved": round(tf, 2), "peak": round(pk, 1),
                       "unit": "TFLOP/s", "frac": round(tf / pk, 4),
-                      "peak_source": "nominal 148 SM x 64 DFMA/clk x 2 x sm_max_mhz"}
+                      "peak_source": pk_src}
     line = {
         "metric": "voxel-ADMM-iterations/sec (fp64)",
         "value": value,
