@@ -6,8 +6,6 @@ python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/ev_ref.json 2
 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ev_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ev_launches.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ev_launch.log 2>&1
-ncu --set full --clock-control none --import-source on \
-    -k regex:"k_update_local|k_row_fwd|k_row_inv|k_plane|k_res_march" -s 15 -c 5 \
-    -o gpurun_out/ev_full python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ev_full.log 2>&1
+bash tools/gpu_ncu_full.sh  # one full capture per stage kernel, steady state
 timeout 900 python bench.py --n 512 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/ev_bench512.json 2> gpurun_out/ev_bench512.err
 echo done
