@@ -132,3 +132,30 @@ def test_state_host_views_round_trip():
     assert st.F[1, 1, 0, 0] == 1.8
     assert st.internal == {}
     assert st.r_d_prev == np.inf
+
+
+def test_inplace_targets_are_only_writeable_contiguous_float64():
+    """F and lam handed in as writeable C-contiguous float64 arrays are the
+    arrays solve() writes back into (the reference mutates them in place);
+    anything else is copied and left alone."""
+    z = np.zeros((4, 4, 2, 2))
+    ok = np.ones((4, 4, 2, 2))
+    ro = np.ones((4, 4, 2, 2))
+    ro.flags.writeable = False
+    st = mm.ADMMState(u_mean=np.eye(2), u_tilde=np.zeros((4, 4, 2)), grad_u=z.copy(), F=ok,
+                      lam=ro, internal={}, rho=1.0)
+    assert st._inplace.get("F") is ok and "lam" not in st._inplace
+    st.F = np.asfortranarray(np.ones((4, 4, 2, 2)))   # not C-contiguous: a copy is kept
+    assert "F" not in st._inplace
+    st.lam = np.ones((4, 4, 2, 2), dtype=np.float32)  # converted: not the caller's array
+    assert "lam" not in st._inplace
+    assert "grad_u" not in st._inplace and "u_tilde" not in st._inplace
+
+
+def test_bench_fp64_peak_is_the_measured_one():
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    pk, src = bench.fp64_peak_tflops()
+    assert 30.0 < pk < 45.0
+    assert "measured" in src
