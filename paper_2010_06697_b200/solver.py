@@ -146,13 +146,14 @@ class ADMMState:
         return self._host.get(name)
 
     def _set(self, name, value):
+        given = value
         if value is not None and name in STATE_FIELDS:
             value = np.asarray(value, dtype=float)
         # The reference updates F (local_sweeps, base.py:109-111) and lam
         # (solver.py:279) in place: a writeable contiguous caller array for
         # either is written back at the end of solve() (_writeback_inplace)
         if name in INPLACE_FIELDS:
-            if (isinstance(value, np.ndarray) and value.dtype == np.float64
+            if (value is given and isinstance(value, np.ndarray) and value.dtype == np.float64
                     and value.flags.c_contiguous and value.flags.writeable):
                 self._inplace[name] = value
             else:
