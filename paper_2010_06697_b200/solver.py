@@ -166,6 +166,17 @@ class ADMMState:
         else:
             self._dirty.discard(name)
 
+    def _prefault_downloads(self, grid):
+        """Fields the caller holds on the host (other than the in-place F and
+        lam) are re-read after the solve as fresh arrays: prepare those host
+        arrays while the device iterates (_lib.prefault_async)."""
+        shapes = []
+        for nm in ("grad_u", "u_tilde"):
+            if self._host.get(nm) is not None:
+                shapes.append(field_shape(grid, STATE_FIELDS[nm][1]))
+        if shapes:
+            _lib.prefault_async(shapes)
+
     def _writeback_inplace(self):
         """Download F and lam into the caller's arrays they were given as
         (the reference mutates those arrays in place); the arrays become the
@@ -458,6 +469,7 @@ def solve(grid: Grid, model, bc: MacroBC, params: SolverParams,
                                                                    params.r_d_tol)
     converged = False
     resid = None
+    state._prefault_downloads(grid)
     if callback is None and _fusable(model, policy, bc, grid) and os.environ.get(
             "MM_FUSE", "1") != "0":
         converged, resid = _solve_fused(grid, model, bc, params, policy, state, r_l_tol)
