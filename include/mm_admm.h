@@ -212,6 +212,38 @@ int mm_profile_read(mm_ctx *ctx, mm_profile *out, int reset);
  *    MR and quadratic).  Any other call first applies a pending ascent. */
 int mm_project_residuals(mm_ctx *ctx, double rho, const double *u_mean, mm_update_stats *out);
 int mm_update_multiplier(mm_ctx *ctx, mm_update_stats *out);
+/* One step of solve()'s fused loop without a host round trip in between
+ * (solver.py:268-296 + the next call's first chunk): the residual sums
+ * (mm_project_residuals), then r_d, r_p, the divergence guard, the penalty
+ * update, the convergence test and the policy tolerance exactly as the
+ * Python loop computes them, then either the ascent alone (the last
+ * iteration, or divergence) or the ascent fused with the next first local
+ * chunk (mm_update_and_sweep). */
+typedef struct {
+    double u_mean[9];        /* macro gradient for this projection */
+    double rho;              /* penalty of this iteration */
+    double npts, mu_rep;
+    double r_l;              /* this iteration's local residual */
+    double r_p_tol, r_d_tol, r_l_tol, divergence_limit;
+    int adapt;               /* SolverParams.adapt */
+    double tau_adapt, kappa_adapt, rho_floor;  /* rho_floor = rho_min_factor * rho_ref */
+    int64_t outer_iter;      /* the iteration counter after this iteration */
+    int last_allowed;        /* this is the last iteration max_outer allows */
+    int ratio_policy;        /* 1: RatioToDual (tol = max(point_tol, ratio r_d)) */
+    double point_tol, ratio;
+    int material;
+    double phi_scale;
+    int64_t chunk;           /* first local chunk of the next iteration */
+} mm_step_params;
+
+typedef struct {
+    double r_p, r_d, rho_next;
+    int diverged, done, swept;  /* swept: the next first chunk ran (ls valid) */
+    double sum_lam[9];          /* sum of lam after the ascent */
+} mm_step_result;
+
+int mm_residuals_and_step(mm_ctx *ctx, const mm_step_params *p, mm_step_result *out,
+                          mm_local_stats *ls);
 int mm_update_and_sweep(mm_ctx *ctx, int material, double rho_next, double tol,
                         int64_t max_sweeps, double phi_scale, int want_points,
                         mm_local_stats *ls, mm_update_stats *us);

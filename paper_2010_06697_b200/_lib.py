@@ -43,7 +43,7 @@ EXPORTS = (
     "mm_create_slab", "mm_slab_buffer", "mm_slab_step", "mm_add_field",
     "mm_equilibrium_residual", "mm_selftest_log", "mm_slab_set_peers", "mm_slab_ipc_handle",
     "mm_slab_open_peers", "mm_bloch_setup", "mm_bloch_start", "mm_bloch_iterate",
-    "mm_bloch_mode", "mm_debug_lce_counters",
+    "mm_bloch_mode", "mm_debug_lce_counters", "mm_residuals_and_step",
 )
 
 SLAB_HALO_T, SLAB_FWD, SLAB_SOLVE, SLAB_INV, SLAB_HALO_U, SLAB_UPDATE, SLAB_GRAD = range(7)
@@ -63,6 +63,25 @@ class LocalStatsC(ctypes.Structure):
 
 class UpdateStatsC(ctypes.Structure):
     _fields_ = [("sum_dG2", ctypes.c_double), ("sum_mis2", ctypes.c_double),
+                ("sum_lam", ctypes.c_double * 9)]
+
+
+class StepParamsC(ctypes.Structure):
+    _fields_ = [("u_mean", ctypes.c_double * 9), ("rho", ctypes.c_double),
+                ("npts", ctypes.c_double), ("mu_rep", ctypes.c_double), ("r_l", ctypes.c_double),
+                ("r_p_tol", ctypes.c_double), ("r_d_tol", ctypes.c_double),
+                ("r_l_tol", ctypes.c_double), ("divergence_limit", ctypes.c_double),
+                ("adapt", ctypes.c_int), ("tau_adapt", ctypes.c_double),
+                ("kappa_adapt", ctypes.c_double), ("rho_floor", ctypes.c_double),
+                ("outer_iter", ctypes.c_int64), ("last_allowed", ctypes.c_int),
+                ("ratio_policy", ctypes.c_int), ("point_tol", ctypes.c_double),
+                ("ratio", ctypes.c_double), ("material", ctypes.c_int),
+                ("phi_scale", ctypes.c_double), ("chunk", ctypes.c_int64)]
+
+
+class StepResultC(ctypes.Structure):
+    _fields_ = [("r_p", ctypes.c_double), ("r_d", ctypes.c_double), ("rho_next", ctypes.c_double),
+                ("diverged", ctypes.c_int), ("done", ctypes.c_int), ("swept", ctypes.c_int),
                 ("sum_lam", ctypes.c_double * 9)]
 
 
@@ -201,6 +220,8 @@ def load_library():
             "mm_bloch_iterate": ([P, I, D, D, D, D, P], I),
             "mm_bloch_mode": ([P, P], I),
             "mm_debug_lce_counters": ([P, I], I),
+            "mm_residuals_and_step": ([P, ctypes.POINTER(StepParamsC), ctypes.POINTER(StepResultC),
+                                       ctypes.POINTER(LocalStatsC)], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -385,6 +406,14 @@ class Context:
         st = UpdateStatsC()
         self.check(self.lib.mm_project_residuals(self.h, float(rho), _ptr(um), ctypes.byref(st)))
         return st
+
+    def residuals_and_step(self, prm):
+        """mm_residuals_and_step: prm is a StepParamsC; returns (result, local stats)."""
+        res = StepResultC()
+        ls = LocalStatsC()
+        self.check(self.lib.mm_residuals_and_step(self.h, ctypes.byref(prm), ctypes.byref(res),
+                                                  ctypes.byref(ls)))
+        return res, ls
 
     def update_multiplier(self):
         st = UpdateStatsC()

@@ -1048,6 +1048,58 @@ int mm_update_and_sweep(mm_ctx *ctx, int material, double rho_next, double tol,
     return mm_run_update(ctx, material, rho_next, tol, max_sweeps, phi_scale, want_points, ls, us);
 }
 
+// the decisions of solver.py's fused loop, in the Python loop's float order
+int mm_residuals_and_step(mm_ctx *ctx, const mm_step_params *p, mm_step_result *out,
+                          mm_local_stats *ls) {
+    if (!ctx || !p || !out || !ls) return MM_ERR_PARAM;
+    int rc = mm_project_residuals(ctx, p->rho, p->u_mean, &ctx->step_us);
+    if (rc) return rc;
+    const mm_update_stats &up = ctx->step_us;
+    memset(out, 0, sizeof *out);
+    memset(ls, 0, sizeof *ls);
+    const double r_d = p->rho * sqrt(up.sum_dG2 / p->npts) / p->mu_rep;
+    const double r_p = sqrt(up.sum_mis2 / p->npts);
+    out->r_d = r_d;
+    out->r_p = r_p;
+    double rho = p->rho;
+    mm_update_stats us;
+    if (!isfinite(r_p) || r_p > p->divergence_limit) {
+        out->diverged = 1;
+        out->rho_next = rho;
+        if ((rc = mm_update_multiplier(ctx, &us))) return rc;
+        memcpy(out->sum_lam, us.sum_lam, sizeof us.sum_lam);
+        return MM_OK;
+    }
+    if (p->adapt && p->outer_iter > 1) {
+        if (r_p > p->tau_adapt * r_d) {
+            rho *= p->kappa_adapt;
+        } else if (r_d > p->tau_adapt * r_p) {
+            const double a = rho / p->kappa_adapt;  // Python max(a, b): a unless b > a
+            rho = (p->rho_floor > a) ? p->rho_floor : a;
+        }
+    }
+    out->rho_next = rho;
+    out->done = (r_p <= p->r_p_tol && r_d <= p->r_d_tol && p->r_l <= p->r_l_tol) ? 1 : 0;
+    if (out->done || p->last_allowed) {
+        if ((rc = mm_update_multiplier(ctx, &us))) return rc;
+    } else {
+        double tol = p->point_tol;
+        if (p->ratio_policy) {
+            if (!isfinite(r_d)) tol = 1.0;
+            else {
+                const double b = p->ratio * r_d;
+                tol = (b > p->point_tol) ? b : p->point_tol;
+            }
+        }
+        if ((rc = mm_update_and_sweep(ctx, p->material, rho, tol * p->mu_rep, p->chunk,
+                                      p->phi_scale, 0, ls, &us)))
+            return rc;
+        out->swept = 1;
+    }
+    memcpy(out->sum_lam, us.sum_lam, sizeof us.sum_lam);
+    return MM_OK;
+}
+
 int mm_project_update(mm_ctx *ctx, double rho, const double *u_mean, mm_update_stats *out) {
     if (!ctx || !u_mean || !out) return MM_ERR_PARAM;
     ctx->gen++;  // invalidates a speculative projection front

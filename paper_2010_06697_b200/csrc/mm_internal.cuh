@@ -89,6 +89,7 @@ struct mm_ctx {
     double front_rho = 0.0;
     uint64_t front_gen = 0;
     cudaEvent_t ev_red = nullptr;
+    mm_update_stats step_us{};  // residual sums of the last mm_residuals_and_step
     bool lam_pending = false;     // multiplier ascent deferred by mm_project_residuals
     double pending_rho = 0.0;
     bool g_implicit = false;

@@ -526,6 +526,26 @@ def _solve_fused(grid, model, bc, params, policy, state, r_l_tol):
     pending = None  # stats of a first local chunk already run by the fused pass
     converged = False
     resid = None
+    # the decisions between the residuals and the next fused pass taken in
+    # the library (MM_HOST_DECIDE=1: here, through two calls)
+    device_step = os.environ.get("MM_HOST_DECIDE", "0") != "1"
+    if device_step:
+        prm = _lib.StepParamsC()
+        prm.npts = float(npts)
+        prm.mu_rep = mu_rep
+        prm.r_p_tol, prm.r_d_tol = params.r_p_tol, params.r_d_tol
+        prm.r_l_tol = r_l_tol
+        prm.divergence_limit = params.divergence_limit
+        prm.adapt = 1 if params.adapt else 0
+        prm.tau_adapt, prm.kappa_adapt = params.tau_adapt, params.kappa_adapt
+        rho_ref = params.rho_init if params.rho_init is not None else model.mu_rep
+        prm.rho_floor = params.rho_min_factor * rho_ref
+        prm.ratio_policy = 1 if isinstance(policy, RatioToDual) else 0
+        prm.point_tol = params.point_tol
+        prm.ratio = getattr(policy, "ratio", 0.0)
+        prm.material = mat
+        prm.phi_scale = phi_scale
+        prm.chunk = min(policy.chunk, params.max_local)
     for it in range(params.max_outer):
         t_start = time.perf_counter()
         tol_pt = policy.target_tol(params, state.r_d_prev)
@@ -547,6 +567,39 @@ def _solve_fused(grid, model, bc, params, policy, state, r_l_tol):
         r_l = float(np.sqrt(stats.sum_res2 / npts)) / mu_rep
         F_mean = (stats.sum_F[: d * d] / npts).reshape(d, d)
         u_mean = macro_gradient(bc, F_mean, eng.lam_mean(), state.rho)
+        if device_step:
+            # residuals, the decisions below and the next ascent + first chunk
+            # in one library call (mm_residuals_and_step): same arithmetic
+            prm.u_mean[:] = np.zeros(9)
+            prm.u_mean[: d * d] = np.asarray(u_mean, dtype=float).reshape(-1)
+            prm.rho = state.rho
+            prm.r_l = r_l
+            prm.outer_iter = state.outer_iter + 1
+            prm.last_allowed = 1 if it == params.max_outer - 1 else 0
+            res, ls = ctx.residuals_and_step(prm)
+            state._mark_device("grad_u", "u_tilde", "lam")
+            r_d, r_p = res.r_d, res.r_p
+            state.u_mean = u_mean
+            state.outer_iter += 1
+            state.r_d_prev = r_d
+            eng.lam_sum = np.array(res.sum_lam[: d * d])
+            if res.diverged:
+                raise DivergenceError(
+                    f"primal residual {r_p:.3e} at outer iteration {state.outer_iter}")
+            state.rho = res.rho_next
+            done = bool(res.done)
+            if res.swept:
+                pending = DeviceLocalStats(None, ls.sweeps,
+                                           float(ls.n_conv) / npts if npts else 1.0,
+                                           ls.sum_res2, list(ls.sum_F), ls.sum_nsw)
+            wall_ms = (time.perf_counter() - t_start) * 1e3
+            resid = Residuals(state.outer_iter, float(r_p), float(r_d), float(r_l),
+                              float(state.rho), wall_ms)
+            state.history.append(resid)
+            if done:
+                converged = True
+                break
+            continue
         up = ctx.project_residuals(state.rho, u_mean)
         state._mark_device("grad_u", "u_tilde", "lam")
         r_d = state.rho * float(np.sqrt(up.sum_dG2 / npts)) / mu_rep

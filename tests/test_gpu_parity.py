@@ -435,3 +435,32 @@ def test_speculative_projection_front_is_exact(n, K, monkeypatch):
     for a, b in zip(out["1"][0], out["0"][0]):
         assert np.array_equal(a, b)
     assert out["1"][1] == out["0"][1] and out["1"][2] == out["0"][2]
+
+
+@pytest.mark.parametrize("dim,n,pol", [(2, 32, "ratio"), (3, 16, "ratio"), (3, 16, "exact"),
+                                       (2, 16, "fraction")])
+def test_library_decision_step_matches_host_loop(dim, n, pol, monkeypatch):
+    """mm_residuals_and_step takes the loop's decisions (r_d, r_p, guard,
+    penalty update, convergence, policy tolerance) in the library; fields,
+    history and sweeps equal the host-decided loop (MM_HOST_DECIDE=1) bit for
+    bit, through convergence."""
+    grid, mu, kap = _laminate(dim, n, 0)
+    Fbar = np.eye(dim)
+    Fbar[0, 0] = 0.95
+    bc = mm.MacroBC.strain(Fbar)
+    m = mm.MooneyRivlin(mu, kap, dim=dim, mu_rep=1.0)
+    policy = {"ratio": mm.RatioToDual(0.3), "exact": mm.ExactAll(),
+              "fraction": mm.FractionConverged(0.9, 2)}[pol]
+    params = mm.SolverParams(max_outer=400)
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("MM_HOST_DECIDE", flag)
+        st = mm.solver.init_state(grid, m, bc, params)
+        st.F = st.F + 1e-3 * np.random.default_rng(1).standard_normal(st.F.shape)
+        st, conv = mm.solve(grid, m, bc, params, policy=policy, state=st, raise_on_max=False)
+        out[flag] = (conv, [np.array(getattr(st, k)) for k in ("F", "lam", "grad_u", "u_tilde")],
+                     [r[:5] for r in st.history], st.total_sweeps, st.rho)
+    a, b = out["0"], out["1"]
+    assert a[0] == b[0] and a[2] == b[2] and a[3] == b[3] and a[4] == b[4]
+    for x, y in zip(a[1], b[1]):
+        assert np.array_equal(x, y)
