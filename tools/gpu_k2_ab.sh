@@ -1,0 +1,17 @@
+# A/B of fused-K2 build variants at the default bench (K = 50): FLAGS_A vs FLAGS_B, twice each
+cd /root/repo
+summ() {
+python - "$1" <<'PY'
+import json,sys
+d=json.load(open('gpurun_out/k2ab.json'))
+st=d['stages']
+print(sys.argv[1], 'ms/it %.3f'%d['ms_per_step'], 'sweeps/vox %.3f'%d['roofline_local_fp64']['point_sweeps_per_voxel_iter'], {k:round(v['ms_per_launch'],3) for k,v in st.items() if v['launches']})
+PY
+}
+for rep in 1 2; do
+for v in "$FLAGS_A" "$FLAGS_B"; do
+  touch paper_2010_06697_b200/csrc/mm_local.cu
+  MM_NVCC_FLAGS="$v" python -c "from paper_2010_06697_b200 import build; build.build()" > gpurun_out/k2ab_b.log 2>&1 || tail -3 gpurun_out/k2ab_b.log
+  timeout 600 python bench.py --no-cpu-baseline > gpurun_out/k2ab.json 2>/dev/null; summ "[$v]"
+done
+done
