@@ -187,18 +187,19 @@ __device__ __forceinline__ void fft_reg_rt(double2 (&v)[R], bool inv) {
 }
 
 // Stockham autosort FFT of TK lines held in shared memory (element n of
-// line c at buf[n*LD + c]) with 8 points per thread: thread t serves line
-// t % TK and butterfly column q = t / TK < N/8.  A pass of radix R (8, 4 or
-// 2) with NS = product of the earlier radices takes butterflies
-// j = q + b*N/8 (b < 8/R): reads x[j + r N/R], multiplies by
+// line c at buf[n*LD + c]) with PPT points per thread: thread t serves line
+// t % TK and butterfly column q = t / TK < N/PPT.  A pass of radix R
+// (<= PPT) with NS = product of the earlier radices takes butterflies
+// j = q + b*N/PPT (b < PPT/R): reads x[j + r N/R], multiplies by
 // W_{NS R}^{(j mod NS) r}, transforms in registers and writes
 // y[(j / NS) NS R + (j mod NS) + r NS]; the last pass leaves natural order.
-// Compared with the two-step register four-step (tile_fft, 16 points per
-// thread) it trades one more shared-memory round trip for half the live
-// registers and twice the threads per tile.
-template <int N, int TK, int R, int NS>
+// PPT = 8 (three passes at N = 256, 80 registers) or 16 (two passes: one
+// shared-memory round trip and two barriers fewer per transform, 168
+// registers, half the threads per tile; the plane pass default: 0.805 ->
+// 0.714 ms at 256^3).
+template <int N, int TK, int R, int NS, int PPT = 8>
 __device__ __forceinline__ void stockham_pass(double2 *buf, const double2 *__restrict__ tw, bool inv) {
-    constexpr int LD = TK + 1, NB = 8 / R, JS = N / 8;
+    constexpr int LD = TK + 1, NB = PPT / R, JS = N / PPT;
     const int c = threadIdx.x % TK, q = threadIdx.x / TK;
     double2 v[NB][R];
 #pragma unroll
@@ -228,10 +229,14 @@ __device__ __forceinline__ void stockham_pass(double2 *buf, const double2 *__res
 }
 
 // radix plan: N = 8 * 8 * 4 (256), 8 * 4 * 4 (128), 8 * 8 (64), 8 * 4 (32), 4 * 4 (16)
-template <int N, int TK>
+template <int N, int TK, int PPT = 8>
 __device__ __forceinline__ void tile_fft_s(double2 *buf, const double2 *__restrict__ tw, bool inv) {
     static_assert(N >= 16 && N <= 256 && (N & (N - 1)) == 0, "N in 16..256, power of two");
-    if constexpr (N == 256) {
+    if constexpr (PPT == 16) {
+        // 16 points per thread: radix-16 first pass, then the remaining factor
+        stockham_pass<N, TK, 16, 1, 16>(buf, tw, inv);
+        if constexpr (N > 16) stockham_pass<N, TK, N / 16, 16, 16>(buf, tw, inv);
+    } else if constexpr (N == 256) {
         stockham_pass<N, TK, 8, 1>(buf, tw, inv);
         stockham_pass<N, TK, 8, 8>(buf, tw, inv);
         stockham_pass<N, TK, 4, 64>(buf, tw, inv);
@@ -897,6 +902,9 @@ k_row_inv_p(const double2 *__restrict__ spec, double *__restrict__ Ut, RowGeom g
 // write it).  The per-line arithmetic (tile_fft, the solve expression and its
 // summation order) is that of k_colp / k_col: results are bitwise identical.
 // ---------------------------------------------------------------------------
+#ifndef MM_PLANE_PPT
+#define MM_PLANE_PPT 16
+#endif
 struct PlaneGeom {
     int n, nh;
     const double *sym;
@@ -906,7 +914,8 @@ struct PlaneGeom {
 template <int N1, int N2, int TK>
 struct PlaneCfg {
     static constexpr int N = N1 * N2;
-    static constexpr int NT = TK * N / 8;  // 8 points per thread (tile_fft_s)
+    static constexpr int PPT = MM_PLANE_PPT;  // points per thread (tile_fft_s)
+    static constexpr int NT = TK * N / PPT;
     static constexpr int IT = (N * TK + NT - 1) / NT;
     // resident CTAs per SM the two tile buffers allow (<= 227 KB of shared
     // memory), requested from the register allocator
@@ -989,7 +998,7 @@ __device__ __forceinline__ void plane_pass(double2 *__restrict__ pl, double2 *sm
 #pragma unroll 1
         for (int ph = 0; ph < NPH; ++ph) {
             asm volatile("" : "+l"(tw));
-            tile_fft_s<N, TK>(buf, tw, KIND == PL_ROW_INV || ph == 1);
+            tile_fft_s<N, TK, C::PPT>(buf, tw, KIND == PL_ROW_INV || ph == 1);
             if (KIND == PL_COL_SOLVE && ph == 0) {
                 const double sl = __ldg(&sym[2 * N + k2]);
 #pragma unroll

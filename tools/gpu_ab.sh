@@ -1,4 +1,5 @@
-# A/B of fused-K2 build variants at the default bench (K = 50): FLAGS_A vs FLAGS_B, twice each
+# A/B of build variants at the default bench (K = 50): FLAGS_A vs FLAGS_B applied to
+# SRC (default mm_local.cu), twice each; TESTS=1 also runs the GPU suite on variant B
 cd /root/repo
 summ() {
 python - "$1" <<'PY'
@@ -10,8 +11,11 @@ PY
 }
 for rep in 1 2; do
 for v in "$FLAGS_A" "$FLAGS_B"; do
-  touch paper_2010_06697_b200/csrc/mm_local.cu
+  touch paper_2010_06697_b200/csrc/${SRC:-mm_local.cu}
   MM_NVCC_FLAGS="$v" python -c "from paper_2010_06697_b200 import build; build.build()" > gpurun_out/k2ab_b.log 2>&1 || tail -3 gpurun_out/k2ab_b.log
   timeout 600 python bench.py --no-cpu-baseline > gpurun_out/k2ab.json 2>/dev/null; summ "[$v]"
+  if [ "$rep" = 1 ] && [ "$v" = "$FLAGS_B" ] && [ -n "$TESTS" ]; then
+    timeout 900 python -m pytest tests -q -m gpu -x > gpurun_out/k2ab_pytest.log 2>&1; echo "pytest [$v] rc=$?"; tail -2 gpurun_out/k2ab_pytest.log
+  fi
 done
 done
