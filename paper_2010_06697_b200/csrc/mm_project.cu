@@ -28,6 +28,19 @@
 
 namespace {
 
+// build-time kernel variants (A/B with tools/gpu_ab.sh)
+#ifndef MM_ROWINV_BAL
+#define MM_ROWINV_BAL 0
+#endif
+#ifndef MM_TW_PROD
+#define MM_TW_PROD 1  // plane pass 0.713 -> 0.695 ms at 256^3
+#endif
+#ifndef MM_ROWINV_REGS
+#define MM_ROWINV_REGS 128  // row_inv_p: 80 spilled 364 B; 164 registers, 0.321 -> 0.220 ms
+#endif
+#ifndef MM_ROWFWD_REGS
+#define MM_ROWFWD_REGS 96
+#endif
 __constant__ double2 c_w32[32];  // exp(-2 pi i k / 32)
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -89,9 +102,10 @@ __device__ __forceinline__ void fft_reg(double2 (&v)[R]) {
 // FFT of TK lines of length N = N1*N2 held in shared memory, element n of
 // line c at buf[n*LD + c], LD = TK + 1.  Requires blockDim >= TK*max(N1,N2).
 // tw: exp(-2 pi i k / N), k < N.
-template <int N1, int N2, int TK, bool INV>
+template <int N1, int N2, int TK, bool INV, int NTH = TK * (N1 > N2 ? N1 : N2)>
 __device__ __forceinline__ void tile_fft(double2 *buf, const double2 *__restrict__ tw) {
     constexpr int LD = TK + 1;
+    static_assert(N2 == 1 || NTH >= TK * N2, "step 1 needs TK * N2 threads");
     const int tid = threadIdx.x;
     const int c = tid % TK;
     if constexpr (N2 == 1) {
@@ -127,18 +141,31 @@ __device__ __forceinline__ void tile_fft(double2 *buf, const double2 *__restrict
             for (int k1 = 0; k1 < N1; ++k1) buf[(k1 * N2 + n2) * LD + c] = v[k1];
         }
         __syncthreads();
-        double2 u[N2];
+        // step 2: N1 columns of N2 points per line; with NTH < TK * N1
+        // threads a thread takes columns k1, k1 + STR, ... (all read before
+        // the barrier, written after it)
+        constexpr int STR = NTH / TK;
+        constexpr int NIT = (N1 + STR - 1) / STR;
+        double2 u[NIT][N2];
         const int k1 = tid / TK;
-        const bool act2 = tid < TK * N1;
-        if (act2) {
+        const bool act2 = tid < TK * STR;
 #pragma unroll
-            for (int j = 0; j < N2; ++j) u[j] = buf[(k1 * N2 + j) * LD + c];
-            fft_reg<N2, INV>(u);
+        for (int it = 0; it < NIT; ++it) {
+            const int kk = k1 + it * STR;
+            if (act2 && kk < N1) {
+#pragma unroll
+                for (int j = 0; j < N2; ++j) u[it][j] = buf[(kk * N2 + j) * LD + c];
+                fft_reg<N2, INV>(u[it]);
+            }
         }
         __syncthreads();
-        if (act2) {
 #pragma unroll
-            for (int k2 = 0; k2 < N2; ++k2) buf[(k1 + N1 * k2) * LD + c] = u[k2];
+        for (int it = 0; it < NIT; ++it) {
+            const int kk = k1 + it * STR;
+            if (act2 && kk < N1) {
+#pragma unroll
+                for (int k2 = 0; k2 < N2; ++k2) buf[(kk + N1 * k2) * LD + c] = u[it][k2];
+            }
         }
         __syncthreads();
     }
@@ -202,6 +229,21 @@ __device__ __forceinline__ void stockham_pass(double2 *buf, const double2 *__res
     constexpr int LD = TK + 1, NB = PPT / R, JS = N / PPT;
     const int c = threadIdx.x % TK, q = threadIdx.x / TK;
     double2 v[NB][R];
+    // MM_TW_PROD (R = 16, one butterfly per thread): the twiddles W^{jm r}
+    // come from four table loads (r = 1, 2, 4, 8), issued before the
+    // shared-memory reads, and at most three products (r = 3 .. 15) instead
+    // of fifteen dependent-latency loads after the barrier
+    constexpr bool TWP = MM_TW_PROD && R == 16 && NB == 1 && NS > 1;
+    double2 wb[4];
+    if constexpr (TWP) {
+        const int jm = q & (NS - 1);
+        constexpr int ST = N / (NS * R);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            wb[e] = __ldg(&tw[jm * (1 << e) * ST]);
+            if (inv) wb[e].y = -wb[e].y;
+        }
+    }
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
 #pragma unroll
@@ -212,7 +254,18 @@ __device__ __forceinline__ void stockham_pass(double2 *buf, const double2 *__res
     for (int b = 0; b < NB; ++b) {
         const int j = q + b * JS;
         const int jm = j & (NS - 1);
-        if constexpr (NS > 1) {
+        if constexpr (TWP) {
+            double2 w[16];
+            w[1] = wb[0]; w[2] = wb[1]; w[4] = wb[2]; w[8] = wb[3];
+            w[3] = cmul(w[1], w[2]);
+            w[5] = cmul(w[1], w[4]);
+            w[6] = cmul(w[2], w[4]);
+            w[7] = cmul(w[3], w[4]);
+#pragma unroll
+            for (int r = 9; r < 16; ++r) w[r] = cmul(w[r - 8], w[8]);
+#pragma unroll
+            for (int r = 1; r < 16; ++r) v[b][r] = cmul(v[b][r], w[r]);
+        } else if constexpr (NS > 1) {
 #pragma unroll
             for (int r = 1; r < R; ++r) {
                 double2 w = __ldg(&tw[jm * r * (N / (NS * R))]);
@@ -282,13 +335,13 @@ __device__ __forceinline__ void tile_dft(double2 *buf, double2 *scr, int N,
     __syncthreads();
 }
 
-template <int N1, int N2, int TK, bool INV>
+template <int N1, int N2, int TK, bool INV, int NTH = TK * (N1 > N2 ? N1 : N2)>
 __device__ __forceinline__ void line_transform(double2 *buf, double2 *scr, int N,
                                                const double2 *__restrict__ tw) {
     if constexpr (N1 == 0)
         tile_dft<TK, INV>(buf, scr, N, tw);
     else
-        tile_fft<N1, N2, TK, INV>(buf, tw);
+        tile_fft<N1, N2, TK, INV, NTH>(buf, tw);
 }
 
 struct RowGeom {
@@ -384,10 +437,16 @@ struct RowCfg {
     static constexpr int TK = DIM * ROWS;  // lines per tile (component x row)
     static constexpr int NT0 = N1 ? TK * (N1 > N2 ? N1 : N2) : 256;
     static constexpr int NT = NT0 < 64 ? 64 : NT0;
-    static constexpr int MINB0 = 65536 / (NT * 96);
+    // inverse (C2R) kernels with MM_ROWINV_BAL: TK * N2 threads, every thread
+    // busy in both steps of the four-step (two step-2 columns each)
+    static constexpr int NTI0 = (N1 && MM_ROWINV_BAL && N2 > 1) ? TK * N2 : NT0;
+    static constexpr int NTI = NTI0 < 64 ? 64 : NTI0;
+    static constexpr int MINB0 = 65536 / (NT * MM_ROWFWD_REGS);
     static constexpr int MINB = MINB0 < 1 ? 1 : MINB0;  // aim at <= 96 registers
-    // the C2R pass fits 80 registers without spilling: one more resident tile
-    static constexpr int MINB_INV0 = 65536 / (NT * 80);
+    // the C2R pass: a register budget of 80 (4 tiles per SM) spilled 364 B
+    // per thread in the persistent kernel; 128 (2 tiles, 164 registers used,
+    // no spills) runs it in 0.22 instead of 0.32 ms
+    static constexpr int MINB_INV0 = 65536 / (NTI * MM_ROWINV_REGS);
     static constexpr int MINB_INV = MINB_INV0 < 1 ? 1 : MINB_INV0;
     static constexpr int NC = N1 * N2;                  // compile-time line length (0: runtime)
 };
@@ -480,7 +539,7 @@ k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho
         }
     }
     __syncthreads();
-    line_transform<N1, N2, TK, false>(buf, scr, N, tw_line);
+    line_transform<N1, N2, TK, false, C::NT>(buf, scr, N, tw_line);
     // split (packed) and store k = 0 .. n/2
     const int nh = packed ? N + 1 : g.n / 2 + 1;
     for (int w = threadIdx.x; w < TK * nh; w += C::NT) {
@@ -533,7 +592,7 @@ __device__ __forceinline__ void row_inv_tile(double2 *buf, double2 *scr, double 
     if (packed) {
         // Z[k] = A[k] + i B[k], A = X[k] + conj X[N-k], B = (X[k] - conj X[N-k]) conj(W^k)
         const int npair = N / 2 + 1;
-        for (int w = threadIdx.x; w < TK * npair; w += C::NT) {
+        for (int w = threadIdx.x; w < TK * npair; w += C::NTI) {
             const int line = w / npair, k = w - line * npair;
             const int kc = N - k;
             const double2 Xk = buf[k * LD + line];
@@ -550,15 +609,15 @@ __device__ __forceinline__ void row_inv_tile(double2 *buf, double2 *scr, double 
         }
     } else {
         // odd n: full Hermitian spectrum
-        for (int w = threadIdx.x; w < TK * (N - nh); w += C::NT) {
+        for (int w = threadIdx.x; w < TK * (N - nh); w += C::NTI) {
             const int line = w / (N - nh), k = nh + (w - line * (N - nh));
             buf[k * LD + line] = cconj(buf[(N - k) * LD + line]);
         }
     }
     __syncthreads();
-    line_transform<N1, N2, TK, true>(buf, scr, N, tw_line);
+    line_transform<N1, N2, TK, true, C::NTI>(buf, scr, N, tw_line);
     // store: a work item (row r, slot m) writes every component of the slot
-    for (int w = threadIdx.x; w < ROWS * N; w += C::NT) {
+    for (int w = threadIdx.x; w < ROWS * N; w += C::NTI) {
         const int r = w / N, m = w - r * N;
         const int64_t row = row0 + r;
         if (row >= g.nrows) continue;
@@ -576,7 +635,7 @@ __device__ __forceinline__ void row_inv_tile(double2 *buf, double2 *scr, double 
 }
 
 template <int N1, int N2, int DIM, int ROWS>
-__global__ void __launch_bounds__(RowCfg<N1, N2, DIM, ROWS>::NT, RowCfg<N1, N2, DIM, ROWS>::MINB_INV)
+__global__ void __launch_bounds__(RowCfg<N1, N2, DIM, ROWS>::NTI, RowCfg<N1, N2, DIM, ROWS>::MINB_INV)
 k_row_inv(const double2 *__restrict__ spec, double *__restrict__ Ut, RowGeom g,
           const double2 *__restrict__ tw_line, const double2 *__restrict__ tw_r2c) {
     using C = RowCfg<N1, N2, DIM, ROWS>;
@@ -588,7 +647,7 @@ k_row_inv(const double2 *__restrict__ spec, double *__restrict__ Ut, RowGeom g,
     double2 *scr = smem_c + (size_t)(N + 1) * LD;
     const int64_t row0 = (int64_t)blockIdx.x * ROWS;
     const int nh = packed ? N + 1 : g.n / 2 + 1;
-    for (int w = threadIdx.x; w < TK * nh; w += C::NT) {
+    for (int w = threadIdx.x; w < TK * nh; w += C::NTI) {
         int line, k;
         if (g.plane) {
             const int r0 = w % ROWS, t = w / ROWS;
@@ -852,7 +911,7 @@ k_colp(double2 *__restrict__ spec, ColGeom g, const double2 *__restrict__ tw, Ti
 // buffer while the current tile is transformed, so loads stay in flight (the
 // one-tile kernel is global-load-latency bound: ncu long_scoreboard).
 template <int N1, int N2, int DIM, int ROWS>
-__global__ void __launch_bounds__(RowCfg<N1, N2, DIM, ROWS>::NT, RowCfg<N1, N2, DIM, ROWS>::MINB_INV)
+__global__ void __launch_bounds__(RowCfg<N1, N2, DIM, ROWS>::NTI, RowCfg<N1, N2, DIM, ROWS>::MINB_INV)
 k_row_inv_p(const double2 *__restrict__ spec, double *__restrict__ Ut, RowGeom g,
             const double2 *__restrict__ tw_line, const double2 *__restrict__ tw_r2c, int ntiles) {
     using C = RowCfg<N1, N2, DIM, ROWS>;
@@ -860,7 +919,7 @@ k_row_inv_p(const double2 *__restrict__ spec, double *__restrict__ Ut, RowGeom g
     extern __shared__ double2 smem_c[];
     auto issue = [&](int t, double2 *dst) {
         const int64_t row0 = (int64_t)t * ROWS;
-        for (int w = threadIdx.x; w < TK * NH; w += C::NT) {
+        for (int w = threadIdx.x; w < TK * NH; w += C::NTI) {
             const int r0 = w % ROWS, tt = w / ROWS;
             const int k = tt % NH, line = (tt / NH) * ROWS + r0;
             const int c = line / ROWS;
@@ -1368,18 +1427,19 @@ int run_rows_t(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double
         const size_t smem2 = sizeof(double2) * (size_t)(g.N + 1) * (C::TK + 1) * 2;
         int rc = launch_smem(ctx, kern, dim3(1), threads, smem2);
         if (rc) return rc;
+        using CI = RowCfg<N1 * N2 >= 16 ? N1 : 4, N1 * N2 >= 16 ? N2 : 4, 3, ROWS>;
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem2);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CI::NTI, smem2);
         if (per_sm < 1) per_sm = 1;
         const int ntiles = (int)grid.x;
         const int blocks = std::min(ntiles, per_sm * ctx->num_sms);
-        kern<<<blocks, threads, smem2, ctx->stream>>>(ctx->spec, u_out, g, tw_line, ctx->tw_r2c,
+        kern<<<blocks, CI::NTI, smem2, ctx->stream>>>(ctx->spec, u_out, g, tw_line, ctx->tw_r2c,
                                                       ntiles);
     } else {
         auto kern = k_row_inv<N1, N2, DIM, ROWS>;
-        int rc = launch_smem(ctx, kern, grid, threads, smem);
+        int rc = launch_smem(ctx, kern, grid, C::NTI, smem);
         if (rc) return rc;
-        kern<<<grid, threads, smem, ctx->stream>>>(ctx->spec, u_out, g, tw_line, ctx->tw_r2c);
+        kern<<<grid, C::NTI, smem, ctx->stream>>>(ctx->spec, u_out, g, tw_line, ctx->tw_r2c);
     }
     MM_LAUNCH_CHECK(ctx);
     return MM_OK;
