@@ -38,6 +38,9 @@ namespace {
 #ifndef MM_ROWINV_REGS
 #define MM_ROWINV_REGS 128  // row_inv_p: 80 spilled 364 B; 164 registers, 0.321 -> 0.220 ms
 #endif
+#ifndef MM_COL32_MINB
+#define MM_COL32_MINB 2
+#endif
 #ifndef MM_ROWFWD_REGS
 #define MM_ROWFWD_REGS 96
 #endif
@@ -693,13 +696,20 @@ struct ColGeom {
 // field's transform; equilibrium_residual, solver.py:364-371)
 enum { COL_FWD = 0, COL_INV = 1, COL_SOLVE = 2, COL_NORM = 3 };
 
+// resident CTAs of the persistent column kernel (TK + 1 = 9 column pitch)
+// that shared memory admits, at most 3
+constexpr int colp_minb(int smem_bytes) {
+    return (227 * 1024) / (smem_bytes + 1024) >= 3 ? 3
+           : (227 * 1024) / (smem_bytes + 1024) < 1 ? 1
+                                                     : (227 * 1024) / (smem_bytes + 1024);
+}
 template <int N1, int N2>
 struct ColCfg {
     static constexpr int TK = 8;
     static constexpr int NT = N1 ? (TK * (N1 > N2 ? N1 : N2) < 64 ? 64 : TK * (N1 > N2 ? N1 : N2))
                                  : 256;
     // resident blocks per SM requested from the register allocator
-    static constexpr int MINB = N1 ? (NT <= 128 ? 5 : 2) : 1;
+    static constexpr int MINB = N1 ? (NT <= 128 ? 5 : (N1 >= 32 ? MM_COL32_MINB : 2)) : 1;
 };
 
 #ifndef COL_SOLVE_MINB
@@ -829,7 +839,11 @@ struct TileMap {
 };
 
 template <int N1, int N2, int MODE>
-__global__ void __launch_bounds__(ColCfg<N1, N2>::NT, 3)
+// persistent column kernel: two tile buffers; the register allocator is asked
+// for no more resident CTAs than shared memory admits (at N = 512 one: a
+// request for 3 capped it at 80 registers and spilled 1.8 KB per thread;
+// col_fwd / col_inv at 512^3 5.2 / 5.0 -> 2.8 / 2.6 ms)
+__global__ void __launch_bounds__(ColCfg<N1, N2>::NT, colp_minb(2 * N1 * N2 * 9 * 16))
 k_colp(double2 *__restrict__ spec, ColGeom g, const double2 *__restrict__ tw, TileMap tm,
        int ntiles) {
     using C = ColCfg<N1, N2>;
