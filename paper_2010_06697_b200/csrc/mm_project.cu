@@ -41,6 +41,12 @@ namespace {
 #ifndef MM_COL32_MINB
 #define MM_COL32_MINB 2
 #endif
+#ifndef MM_ROWINV_P_ROWS
+#define MM_ROWINV_P_ROWS 1
+#endif
+#ifndef MM_ROWINV_P_MAXN
+#define MM_ROWINV_P_MAXN 256
+#endif
 #ifndef MM_ROWFWD_REGS
 #define MM_ROWFWD_REGS 96
 #endif
@@ -934,12 +940,23 @@ k_row_inv_p(const double2 *__restrict__ spec, double *__restrict__ Ut, RowGeom g
     auto issue = [&](int t, double2 *dst) {
         const int64_t row0 = (int64_t)t * ROWS;
         for (int w = threadIdx.x; w < TK * NH; w += C::NTI) {
-            const int r0 = w % ROWS, tt = w / ROWS;
-            const int k = tt % NH, line = (tt / NH) * ROWS + r0;
+            int k, line, r0;
+            if (g.plane) {  // ROWS x 16 B runs per (c, k2)
+                r0 = w % ROWS;
+                const int tt = w / ROWS;
+                k = tt % NH;
+                line = (tt / NH) * ROWS + r0;
+            } else {        // row layout: consecutive k of one row
+                line = w / NH;
+                k = w - line * NH;
+                r0 = line % ROWS;
+            }
             const int c = line / ROWS;
             const int64_t row = row0 + r0;
             const bool ok = row < g.nrows;
-            const double2 *src = spec + ((int64_t)c * NH + k) * g.nrows + (ok ? row : 0);
+            const double2 *src =
+                g.plane ? spec + ((int64_t)c * NH + k) * g.nrows + (ok ? row : 0)
+                        : spec + ((int64_t)c * g.nrows + (ok ? row : 0)) * g.P + k;
             cp_async16(&dst[k * LD + line], src, ok ? 16 : 0);
         }
         cp_async_commit();
@@ -1434,9 +1451,10 @@ int run_rows_t(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double
             kern<<<grid, threads, smem, ctx->stream>>>(ctx->F, ctx->Lam, rho, ctx->spec, g,
                                                        tw_line, ctx->tw_r2c);
         }
-    } else if (DIM == 3 && N1 * N2 >= 16 && N1 * N2 <= 128 && g.plane && g.packed &&
-               ctx->opt_rowinv_p) {
-        // persistent, double-buffered (plane layout)
+    } else if (DIM == 3 && N1 * N2 >= 16 && N1 * N2 <= MM_ROWINV_P_MAXN && g.packed &&
+               (g.plane || (MM_ROWINV_P_ROWS && !ctx->slab_mode)) && ctx->opt_rowinv_p) {
+        // persistent, double-buffered (plane layout, and the row layout of
+        // single-GPU grids up to n = 2 * MM_ROWINV_P_MAXN)
         auto kern = k_row_inv_p<N1 * N2 >= 16 ? N1 : 4, N1 * N2 >= 16 ? N2 : 4, 3, ROWS>;
         const size_t smem2 = sizeof(double2) * (size_t)(g.N + 1) * (C::TK + 1) * 2;
         int rc = launch_smem(ctx, kern, dim3(1), threads, smem2);
