@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define MM_ABI_VERSION 1
+#define MM_ABI_VERSION 2  /* 2: mm_local_stats gained sum_nsw; mm_struct_size */
 
 enum mm_status {
     MM_OK = 0,
@@ -120,6 +120,13 @@ typedef struct {
 } mm_lce_params;
 
 int mm_abi_version(void);
+/* sizeof of the public structs, so a binding can check its declarations:
+ * which = MM_STRUCT_* below; -1 for an unknown id. */
+enum mm_struct_id {
+    MM_STRUCT_LOCAL_STATS = 0, MM_STRUCT_UPDATE_STATS = 1, MM_STRUCT_STEP_PARAMS = 2,
+    MM_STRUCT_STEP_RESULT = 3, MM_STRUCT_PROFILE = 4, MM_STRUCT_LCE_PARAMS = 5
+};
+int64_t mm_struct_size(int which);
 
 /* Context = one periodic grid on one device (Grid, grid.py:55-122).
  * dim in {2,3}, n >= 4, length > 0 (half edge L). */

@@ -34,7 +34,7 @@ MAT_MR, MAT_QUADRATIC, MAT_LCE, MAT_MR_DESCENT = range(4)
 
 # every symbol include/mm_admm.h declares (checked by the CPU test suite)
 EXPORTS = (
-    "mm_abi_version", "mm_create", "mm_create_points", "mm_destroy", "mm_last_error",
+    "mm_abi_version", "mm_struct_size", "mm_create", "mm_create_points", "mm_destroy", "mm_last_error",
     "mm_synchronize", "mm_device_bytes", "mm_upload", "mm_download", "mm_copy_field",
     "mm_field_sums", "mm_set_symbols", "mm_local_sweeps", "mm_set_lce", "mm_download_points",
     "mm_prepare_frozen", "mm_project", "mm_project_update", "mm_stencil",
@@ -180,6 +180,7 @@ def load_library():
         PP = ctypes.POINTER(ctypes.c_void_p)
         sig = {
             "mm_abi_version": ([], I),
+            "mm_struct_size": ([I], I64),
             "mm_create": ([I, I, D, I, PP], I),
             "mm_create_points": ([I, I64, I, PP], I),
             "mm_destroy": ([P], None),

@@ -40,6 +40,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     headers.append(os.path.join(HERE, "..", "include", "mm_admm.h"))
     newest_hdr = max(os.path.getmtime(h) for h in headers)
     objs = []
+    cmds = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(objdir, src.replace(".cu", ".o"))
@@ -50,10 +51,18 @@ def build(verbose: bool = False, force: bool = False) -> str:
         flags = list(COMMON) + os.environ.get("MM_NVCC_FLAGS", "").split()
         if src in NOFMA:
             flags += ["-fmad=false"]
-        cmd = [nvcc, *ARCH, *flags, "-c", s, "-o", o]
+        cmds.append([nvcc, *ARCH, *flags, "-c", s, "-o", o])
+    # translation units compile independently: run them side by side
+    from concurrent.futures import ThreadPoolExecutor
+
+    def run(cmd):
         if verbose:
-            print(" ".join(cmd))
+            print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        for f in [ex.submit(run, c) for c in cmds]:
+            f.result()
     if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB)
                                                for o in objs):
         cmd = [nvcc, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lpthread"]

@@ -462,6 +462,18 @@ extern "C" {
 
 int mm_abi_version(void) { return MM_ABI_VERSION; }
 
+int64_t mm_struct_size(int which) {
+    switch (which) {
+        case MM_STRUCT_LOCAL_STATS: return (int64_t)sizeof(mm_local_stats);
+        case MM_STRUCT_UPDATE_STATS: return (int64_t)sizeof(mm_update_stats);
+        case MM_STRUCT_STEP_PARAMS: return (int64_t)sizeof(mm_step_params);
+        case MM_STRUCT_STEP_RESULT: return (int64_t)sizeof(mm_step_result);
+        case MM_STRUCT_PROFILE: return (int64_t)sizeof(mm_profile);
+        case MM_STRUCT_LCE_PARAMS: return (int64_t)sizeof(mm_lce_params);
+        default: return -1;
+    }
+}
+
 const char *mm_last_error(const mm_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 int64_t mm_device_bytes(const mm_ctx *ctx) { return ctx ? ctx->bytes : 0; }

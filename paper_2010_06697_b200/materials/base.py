@@ -17,7 +17,7 @@ import numpy as np
 from .. import _lib
 from ..errors import InadmissibleStateError
 
-__all__ = ["MaterialModel", "LocalStats", "BACKTRACK_SHRINK", "BACKTRACK_DECREASE",
+__all__ = ["MaterialModel", "LocalStats", "DeviceParam", "BACKTRACK_SHRINK", "BACKTRACK_DECREASE",
            "MAX_BACKTRACKS", "MEAS_EPS", "descent_sweeps_numpy"]
 
 # Armijo constants of the reference (base.py:36-41); the CUDA kernels use the
@@ -61,8 +61,43 @@ class DeviceLocalStats(LocalStats):
         self._res = v
 
 
+class DeviceParam:
+    """A model parameter array that is mirrored on the device.
+
+    The reference re-reads its moduli on every ``local_sweeps`` call
+    (mooney_rivlin.py:111-116); the device keeps an uploaded copy and a cached
+    energy scale instead.  To keep the two consistent the value is stored as
+    a private read-only copy: assigning a new value bumps the model's
+    ``_device_version`` (the engine and the point-set context re-upload, the
+    cached maxima are recomputed), and an in-place edit raises instead of
+    silently leaving stale moduli on the device."""
+
+    def __init__(self, convert=None):
+        self.convert = convert
+
+    def __set_name__(self, owner, name):
+        self.name = name
+        self.slot = "_param_" + name
+
+    def __get__(self, obj, objtype=None):
+        if obj is None:
+            return self
+        return obj.__dict__[self.slot]
+
+    def __set__(self, obj, value):
+        a = self.convert(value) if self.convert is not None else np.array(value, dtype=float)
+        if a is value or (isinstance(value, np.ndarray) and np.shares_memory(a, value)):
+            a = a.copy()
+        a.flags.writeable = False
+        obj.__dict__[self.slot] = a
+        obj.__dict__["_device_version"] = obj.__dict__.get("_device_version", 0) + 1
+
+
 class MaterialModel:
     """Base class; concrete models override the pointwise physics."""
+
+    #: bumped whenever a DeviceParam is assigned (see DeviceParam)
+    _device_version = 0
 
     dim: int = 2
     name: str = "base"
@@ -116,9 +151,27 @@ class MaterialModel:
         ctx = getattr(self, "_pts_ctx", None)
         if ctx is None or ctx.npts != npts or ctx.dim != self.dim:
             ctx = _lib.Context(self.dim, npts=npts)
-            self._device_bind(ctx, npts)
             self._pts_ctx = ctx
+            self._pts_ver = None
+        if self._pts_ver != self._device_version:
+            self._device_bind(ctx, npts)
+            self._pts_ver = self._device_version
         return ctx
+
+    def _cached_max(self, key, fn):
+        """Host maxima of the moduli (the energy scale), recomputed only when
+        a DeviceParam was reassigned."""
+        cache = self.__dict__.setdefault("_max_cache", {})
+        hit = cache.get(key)
+        if hit is None or hit[0] != self._device_version:
+            hit = (self._device_version, float(fn()))
+            cache[key] = hit
+        return hit[1]
+
+    def _override_max(self, key, value):
+        """Pin a cached maximum (slab ranks hold part of the moduli: the
+        energy scale is the global one, reduced across ranks)."""
+        self.__dict__.setdefault("_max_cache", {})[key] = (self._device_version, float(value))
 
 
 def descent_sweeps_numpy(*args, **kwargs):

@@ -22,7 +22,7 @@ import numpy as np
 
 from .. import _lib
 from ..errors import ParameterError
-from .base import DeviceLocalStats, LocalStats, MaterialModel
+from .base import DeviceLocalStats, DeviceParam, LocalStats, MaterialModel
 
 __all__ = ["LiquidCrystalElastomer", "step_length_tensor", "step_length_sqrt"]
 
@@ -72,6 +72,7 @@ class LiquidCrystalElastomer(MaterialModel):
     has_tangent = False
     has_dissipation = True
     _material_id = _lib.MAT_LCE
+    n0 = DeviceParam(lambda v: _unit_rows(np.atleast_2d(np.asarray(v, dtype=float)), "n0"))
 
     def __init__(self, mu, r, alpha, frank_kappa, n0, dim: int = 2, nu_F: float = 0.0,
                  nu_n: float = 0.0, gamma_inc: float | None = None, det_tol: float = 1e-8,
@@ -86,7 +87,7 @@ class LiquidCrystalElastomer(MaterialModel):
                 or self.nu_F < 0 or self.nu_n < 0:
             raise ParameterError("LCE needs mu > 0, r >= 1, alpha >= 0, frank_kappa >= 0 "
                                  "and nonnegative viscosities")
-        self.n0 = _unit_rows(np.atleast_2d(n0), "n0")
+        self.n0 = n0
         if self.n0.shape[-1] != self.dim:
             raise ParameterError(f"n0 has {self.n0.shape[-1]} components, model is {self.dim}D")
         self.gamma_inc = float(gamma_inc) if gamma_inc is not None else 50.0 * self.mu

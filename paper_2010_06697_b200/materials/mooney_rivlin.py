@@ -17,7 +17,7 @@ import numpy as np
 
 from .. import _lib
 from ..errors import ParameterError
-from .base import DeviceLocalStats, LocalStats, MaterialModel
+from .base import DeviceLocalStats, DeviceParam, LocalStats, MaterialModel
 
 __all__ = ["MooneyRivlin"]
 
@@ -26,11 +26,13 @@ class MooneyRivlin(MaterialModel):
     name = "mooney_rivlin"
     has_tangent = True
     _material_id = _lib.MAT_MR
+    mu = DeviceParam()
+    kappa = DeviceParam()
 
     def __init__(self, mu, kappa, dim: int = 2, mu_rep: float | None = None):
         self.dim = int(dim)
-        self.mu = np.asarray(mu, dtype=float)
-        self.kappa = np.asarray(kappa, dtype=float)
+        self.mu = mu
+        self.kappa = kappa
         if np.any(self.mu <= 0) or np.any(self.kappa < 0):
             raise ParameterError("MooneyRivlin needs mu > 0 and kappa >= 0")
         self.mu_rep = float(mu_rep) if mu_rep is not None else float(np.max(self.mu))
@@ -78,15 +80,10 @@ class MooneyRivlin(MaterialModel):
         return mu, kap
 
     def _phi_scale(self):
-        """max mu + max kappa (mooney_rivlin.py:116), cached per moduli arrays
-        (a host max over the full grid would otherwise cost more than the
-        device local step)."""
-        key = (id(self.mu), id(self.kappa))
-        cached = getattr(self, "_phi_cache", None)
-        if cached is None or cached[0] != key:
-            cached = (key, float(np.max(self.mu) + np.max(self.kappa)))
-            self._phi_cache = cached
-        return cached[1]
+        """max mu + max kappa (mooney_rivlin.py:116), cached until the moduli
+        are reassigned (a host max over the full grid would otherwise cost
+        more than the device local step)."""
+        return self._cached_max("phi", lambda: np.max(self.mu) + np.max(self.kappa))
 
     def _fused_material(self):
         """Material id and energy scale for the fused ascent + first chunk."""

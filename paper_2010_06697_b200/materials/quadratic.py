@@ -12,7 +12,7 @@ import numpy as np
 
 from .. import _lib
 from ..errors import ParameterError
-from .base import DeviceLocalStats, LocalStats, MaterialModel
+from .base import DeviceLocalStats, DeviceParam, LocalStats, MaterialModel
 
 __all__ = ["QuadraticMaterial"]
 
@@ -21,10 +21,11 @@ class QuadraticMaterial(MaterialModel):
     name = "quadratic"
     has_tangent = True
     _material_id = _lib.MAT_QUADRATIC
+    c = DeviceParam()
 
     def __init__(self, c, dim: int = 2, mu_rep: float | None = None):
         self.dim = int(dim)
-        self.c = np.asarray(c, dtype=float)
+        self.c = c
         if np.any(self.c <= 0):
             raise ParameterError("QuadraticMaterial needs c > 0")
         self.mu_rep = float(mu_rep) if mu_rep is not None else float(np.max(self.c))
@@ -44,11 +45,7 @@ class QuadraticMaterial(MaterialModel):
         return c[..., None, None, None, None] * np.einsum("ik,jl->ijkl", eye, eye)
 
     def _cmax(self):
-        cached = getattr(self, "_cmax_cache", None)
-        if cached is None or cached[0] != id(self.c):
-            cached = (id(self.c), float(np.max(self.c)))
-            self._cmax_cache = cached
-        return cached[1]
+        return self._cached_max("cmax", lambda: np.max(self.c))
 
     def _fused_material(self):
         return _lib.MAT_QUADRATIC, self._cmax()

@@ -497,7 +497,7 @@ class SlabSolver:
             # the Armijo noise floor uses the global max mu + max kappa
             mx = comm.ordered_sum([float(np.max(model.mu)), float(np.max(model.kappa))],
                                   ops=[1, 1])
-            model._phi_cache = ((id(model.mu), id(model.kappa)), float(mx[0] + mx[1]))
+            model._override_max("phi", mx[0] + mx[1])
         self.ctx.upload(_lib.FIELD_F, F)
         self.ctx.upload(_lib.FIELD_G, grad_u)
         self.ctx.upload(_lib.FIELD_LAM, lam)

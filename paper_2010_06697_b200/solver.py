@@ -179,13 +179,17 @@ class ADMMState:
 
     def _writeback_inplace(self):
         """Download F and lam into the caller's arrays they were given as
-        (the reference mutates those arrays in place); the arrays become the
-        state's read-only snapshots, as any downloaded field."""
+        (the reference mutates those arrays in place).  The arrays stay
+        registered, so every later solve() on this state writes into them
+        again and ``state.F is F0`` holds throughout, as in the reference;
+        they become read-only, so an in-place edit between solves raises
+        instead of being silently lost (assign ``state.F = ...`` instead:
+        the device copy is authoritative while the state is attached)."""
         eng = self._engine
         if eng is None:
             return
         for nm in INPLACE_FIELDS:
-            target = self._inplace.pop(nm, None)
+            target = self._inplace.get(nm)
             if target is None or nm not in self._stale:
                 continue
             fid, rank = STATE_FIELDS[nm]

@@ -404,8 +404,18 @@ def test_solve_updates_caller_F_and_lam_in_place():
         if writeable:
             assert st.F is F0 and st.lam is lam0
             assert not F0.flags.writeable
+            # the arrays stay the state's F / lam through later solves, and
+            # receive every solve's result (reference: state.F keeps identity)
+            st, _ = mm.solve(grid, m, bc, params, policy=mm.RatioToDual(0.3), state=st,
+                             raise_on_max=False)
+            assert st.F is F0 and st.lam is lam0
+            eng = st._engine
+            assert np.array_equal(F0, eng.ctx.download(mm._lib.FIELD_F, F0.shape))
+            assert np.array_equal(lam0, eng.ctx.download(mm._lib.FIELD_LAM, lam0.shape))
         else:
             assert np.array_equal(F0, keep[0]) and np.array_equal(lam0, keep[1])
+            st, _ = mm.solve(grid, m, bc, params, policy=mm.RatioToDual(0.3), state=st,
+                             raise_on_max=False)
         runs.append((np.array(st.F), np.array(st.lam)))
     assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][1], runs[1][1])
 
@@ -464,3 +474,30 @@ def test_library_decision_step_matches_host_loop(dim, n, pol, monkeypatch):
     assert a[0] == b[0] and a[2] == b[2] and a[3] == b[3] and a[4] == b[4]
     for x, y in zip(a[1], b[1]):
         assert np.array_equal(x, y)
+
+
+def test_reassigned_moduli_reach_the_device():
+    """Assigning new moduli to a model between solves on the same state is
+    seen by the device (upload + energy scale), as the reference re-reads
+    them on every local_sweeps call (mooney_rivlin.py:111-116): the result
+    equals a solve with a fresh model holding the new moduli."""
+    grid, mu, kap = _laminate(3, 8, 0)
+    bc = mm.MacroBC.strain(np.diag([0.95, 1.0, 1.0]))
+    params = mm.SolverParams(max_outer=3)
+    out = []
+    for reassign in (True, False):
+        m = mm.MooneyRivlin(mu, kap, dim=3, mu_rep=1.0)
+        st = mm.solver.init_state(grid, m, bc, params)
+        st.F = st.F + 1e-3 * np.random.default_rng(0).standard_normal(st.F.shape)
+        st, _ = mm.solve(grid, m, bc, params, policy=mm.RatioToDual(0.3), state=st,
+                         raise_on_max=False)
+        if reassign:
+            m.mu = 3.0 * mu
+            m.kappa = 2.0 * kap
+        else:
+            m = mm.MooneyRivlin(3.0 * mu, 2.0 * kap, dim=3, mu_rep=1.0)
+        st, _ = mm.solve(grid, m, bc, params, policy=mm.RatioToDual(0.3), state=st,
+                         raise_on_max=False)
+        out.append((np.array(st.F), np.array(st.lam), [r[:5] for r in st.history]))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert out[0][2] == out[1][2]

@@ -61,7 +61,7 @@ def test_slab_solver_matches_single_gpu(n, P, K, exchange):
             sl = lay.plane_slice()
             pts = slice(r * lay.npts_local, (r + 1) * lay.npts_local)
             mloc = mm.MooneyRivlin(mu[pts], kap[pts], dim=3, mu_rep=1.0)
-            mloc._phi_cache = ((id(mloc.mu), id(mloc.kappa)), float(mu.max() + kap.max()))
+            mloc._override_max("phi", mu.max() + kap.max())
             sv = SlabSolver(lay, mloc, bc, params, pol, ThreadComm(shared, r), F[sl], G[sl],
                             lam[sl], exchange=exchange)
             sv.solve()

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     assert set(declared) == set(_lib.EXPORTS)
     L = _lib.load_library()
-    assert L.mm_abi_version() == 1
+    assert L.mm_abi_version() == 2
 
 
 def test_status_mapping():
@@ -159,3 +159,22 @@ def test_bench_fp64_peak_is_the_measured_one():
     pk, src = bench.fp64_peak_tflops()
     assert 30.0 < pk < 45.0
     assert "measured" in src
+
+
+def test_moduli_are_read_only_and_reassignment_bumps_the_device_version():
+    """Device-mirrored moduli cannot drift from their device copy: in-place
+    edits raise, reassignment re-versions the model (engine re-upload) and
+    recomputes the energy scale."""
+    mu = np.ones(8)
+    m = mm.MooneyRivlin(mu, 9.8 * mu, dim=3)
+    mu[0] = 5.0                      # the caller's array is not aliased
+    assert m.mu[0] == 1.0
+    with pytest.raises(ValueError):
+        m.mu[0] = 2.0
+    v, phi = m._device_version, m._phi_scale()
+    m.kappa = 20.0 * np.ones(8)
+    assert m._device_version > v and m._phi_scale() == 21.0 != phi
+    q = mm.QuadraticMaterial(np.full(4, 2.0), dim=2)
+    assert q._cmax() == 2.0
+    q.c = np.full(4, 3.0)
+    assert q._cmax() == 3.0
