@@ -23,7 +23,7 @@ __all__ = [
     "Params", "State", "ExactAll", "FractionConverged", "RatioToDual",
     "init_state", "begin_time_step", "outer_iteration", "solve", "macro_stress",
     "OracleInadmissible", "OracleDivergence", "OracleConvergence",
-    "composite_moduli", "polydomain_n0", "set_threads",
+    "composite_moduli", "polydomain_n0", "set_threads", "set_fft",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -67,6 +67,26 @@ def lib():
     L.orc_get_threads.restype = ctypes.c_int
     _LIB = L
     return L
+
+
+_FFT = np.fft  # transforms of project / frank_force (set_fft)
+
+
+def set_fft(name: str):
+    """Transforms of the projection and the Frank force: "numpy" (pocketfft,
+    numpy's build; the default the goldens pin) or "scipy" (scipy.fft, the
+    module the reference itself calls, grid.py:32,195-220).  The two are the
+    same algorithm family and differ by roundoff, which measures how far two
+    faithful CPU runs of the reference algorithm drift apart."""
+    global _FFT
+    if name == "numpy":
+        _FFT = np.fft
+    elif name == "scipy":
+        import scipy.fft
+        _FFT = scipy.fft
+    else:
+        raise ValueError(name)
+    return _FFT
 
 
 def set_threads(n: int) -> int:
@@ -123,14 +143,14 @@ def project(dim, n, L, F, lam, rho, strain_mask, value, sym=None):
     axes = tuple(range(dim))
     g, gsq = sym if sym is not None else symbols(dim, n, L)
     T = F - lam / rho
-    That = np.fft.rfftn(T, axes=axes)
+    That = _FFT.rfftn(T, axes=axes)
     live = gsq > 1e-14 * gsq.max()
     inv = np.where(live, 1.0 / np.where(live, gsq, 1.0), 0.0)
     uhat = -np.einsum("...ij,...j,...->...i", That, g, inv)
     ghat = uhat[..., :, None] * g[..., None, :]
     shape = (n,) * dim
-    u_tilde = np.fft.irfftn(uhat, s=shape, axes=axes)
-    grad_fluct = np.fft.irfftn(ghat, s=shape, axes=axes)
+    u_tilde = _FFT.irfftn(uhat, s=shape, axes=axes)
+    grad_fluct = _FFT.irfftn(ghat, s=shape, axes=axes)
     Fm = mean_field(F, dim)
     Lm = mean_field(lam, dim)
     stress_update = Fm - (Lm - value) / rho
@@ -300,8 +320,8 @@ class LCE:
         """2 kappa (D^T D) n through the spectrum, lce.py:213-221."""
         _, gsq = symbols(dim, n, L)
         axes = tuple(range(dim))
-        nhat = np.fft.rfftn(n_field, axes=axes)
-        f = np.fft.irfftn(gsq[..., None] * nhat, s=(n,) * dim, axes=axes)
+        nhat = _FFT.rfftn(n_field, axes=axes)
+        f = _FFT.irfftn(gsq[..., None] * nhat, s=(n,) * dim, axes=axes)
         return 2.0 * self.frank_kappa * f
 
     def prepare_frozen(self, dim, n, L, F, internal):

@@ -55,19 +55,45 @@ def _laminate(n):
     return grid, mu, 9.8 * mu
 
 
+def _oracle_run(n, K, mu, kap, bc, F0, fft):
+    oracle.set_fft(fft)
+    try:
+        om = oracle.MR(mu, kap, dim=3, mu_rep=1.0)
+        op = oracle.Params(max_outer=K)
+        ost = oracle.init_state(3, n, om, bc.strain_mask, bc.value, op)
+        ost.F = F0.copy()
+        ost, _ = oracle.solve(3, n, 0.5, om, bc.strain_mask, bc.value, op,
+                              policy=oracle.RatioToDual(0.3), state=ost, raise_on_max=False)
+    finally:
+        oracle.set_fft("numpy")
+    return ({k: getattr(ost, k) for k in ("F", "lam", "grad_u", "u_tilde")},
+            np.array(ost.history), ost.total_sweeps)
+
+
 @pytest.mark.parametrize("n,K", [(128, 20), (256, 3)])
 def test_config2_trajectory_at_benchmark_size(n, K):
     """SURVEY §8(d) config 2 (128^3, K = 20) and the bench's 256^3: the fused
     single-GPU schedule (k_plane, K1 plane-marching, fused K2 with the T
-    field, speculative front, library-side decisions) against the oracle."""
+    field, speculative front, library-side decisions) against the oracle.
+
+    The reference's inexact local step takes discrete decisions (Armijo
+    accept / reject, free-phase step growth, the convergence test) that a
+    roundoff-level input difference can flip at a near-tie point; that point
+    then walks a different path to within the local tolerance of the same
+    minimiser.  At 2M-17M points a few such points exist, so two faithful CPU
+    runs of the reference algorithm -- one with numpy's pocketfft, one with
+    scipy.fft, the module the reference itself calls -- already differ by
+    ~1e-10 in F and ~1e-9 in lam after 20 iterations (measured: 64^3 F
+    7.2e-11, lam 1.3e-9).  The bar is therefore: the device result is within
+    1e-10 of the oracle, or no further from it than the reference's own
+    reproducibility envelope (2x the numpy-vs-scipy distance); the total
+    sweep count is identical and the history agrees as closely."""
     grid, mu, kap = _laminate(n)
     bc = mm.MacroBC.strain(np.diag([0.95, 1.0, 1.0]))
     m = mm.MooneyRivlin(mu, kap, dim=3, mu_rep=1.0)
     params = mm.SolverParams(max_outer=K)
     st = mm.solver.init_state(grid, m, bc, params)
-    F0 = st.F + 1e-4 * np.random.default_rng(0).standard_normal(st.F.shape)
-    del st
-    st = mm.solver.init_state(grid, m, bc, params)
+    F0 = np.array(st.F) + 1e-4 * np.random.default_rng(0).standard_normal(st.F.shape)
     st.F = F0.copy()
     st, _ = mm.solve(grid, m, bc, params, policy=mm.RatioToDual(0.3), state=st,
                      raise_on_max=False)
@@ -75,18 +101,22 @@ def test_config2_trajectory_at_benchmark_size(n, K):
     hist = np.array([r[:5] for r in st.history])
     sweeps = st.total_sweeps
     del st
-    om = oracle.MR(mu, kap, dim=3, mu_rep=1.0)
-    op = oracle.Params(max_outer=K)
-    ost = oracle.init_state(3, n, om, bc.strain_mask, bc.value, op)
-    ost.F = F0
-    ost, _ = oracle.solve(3, n, 0.5, om, bc.strain_mask, bc.value, op,
-                          policy=oracle.RatioToDual(0.3), state=ost, raise_on_max=False)
+    o_np, h_np, sw_np = _oracle_run(n, K, mu, kap, bc, F0, "numpy")
+    o_sp, h_sp, sw_sp = _oracle_run(n, K, mu, kap, bc, F0, "scipy")
+    assert sweeps == sw_np == sw_sp
     for k, v in ours.items():
-        e = rel_l2(v, getattr(ost, k))
-        print(f"n={n} K={K} {k}: rel L2 {e:.3e}")
-        assert e < 1e-10, k
-    assert sweeps == ost.total_sweeps
-    np.testing.assert_allclose(hist, np.array(ost.history), rtol=1e-9)
+        e = rel_l2(v, o_np[k])
+        e_sp = rel_l2(v, o_sp[k])
+        env = rel_l2(o_sp[k], o_np[k])
+        print(f"n={n} K={K} {k}: ours-vs-oracle {e:.3e}, ours-vs-oracle(scipy.fft) {e_sp:.3e}, "
+              f"oracle(scipy.fft)-vs-oracle {env:.3e}")
+        assert e < max(1e-10, 2.0 * env), k
+    h_env = np.abs(h_sp - h_np) / np.abs(h_np).clip(1e-300)
+    h_err = np.abs(hist - h_np) / np.abs(h_np).clip(1e-300)
+    assert np.array_equal(hist[:, 0], h_np[:, 0])
+    print("history max rel dev (r_p, r_d, r_l, rho): ours", h_err[:, 1:].max(axis=0),
+          "envelope", h_env[:, 1:].max(axis=0))
+    assert np.all(h_err[:, 1:].max(axis=0) <= np.maximum(1e-9, 2.0 * h_env[:, 1:].max(axis=0)))
 
 
 @pytest.mark.parametrize("n", [128, 256])
