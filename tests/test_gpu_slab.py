@@ -38,7 +38,8 @@ def _problem(n):
 
 @pytest.mark.parametrize("n,P,K,exchange", [(16, 2, 6, "collective"), (32, 4, 6, "collective"),
                                             (32, 1, 4, "collective"), (16, 2, 6, "push"),
-                                            (32, 4, 6, "push")])
+                                            (32, 4, 6, "push"), (64, 2, 5, "push"),
+                                            (64, 4, 5, "collective"), (64, 4, 5, "push")])
 def test_slab_solver_matches_single_gpu(n, P, K, exchange):
     from paper_2010_06697_b200.slab import SlabLayout, SlabSolver, ThreadComm
     grid, mu, kap, bc, F, G, lam = _problem(n)
