@@ -178,11 +178,22 @@ def setup_problem(mm, n, device_params=None):
     return grid, model, bc, params, st
 
 
+def _stage_report(stage_ms, stage_launch, sb):
+    per_stage = {}
+    for s_name, ms in stage_ms.items():
+        nl = stage_launch.get(s_name, 0)
+        if nl and s_name in sb:
+            avg = ms / nl
+            per_stage[s_name] = {"ms_total": round(ms, 4), "launches": nl,
+                                 "ms_per_launch": round(avg, 5),
+                                 "GBps": round(sb[s_name] / (avg / 1e3) / 1e9, 1)}
+    return per_stage
+
+
 def run_ours(args, rank, world, dist):
     import torch
 
     import paper_2010_06697_b200 as mm
-    from paper_2010_06697_b200 import _lib
 
     dev = bench_device()
     torch.cuda.set_device(dev)
@@ -196,9 +207,17 @@ def run_ours(args, rank, world, dist):
     mm.solve(grid, model, bc, params, policy=pol, state=st, raise_on_max=False)
     eng = st._engine
     ctx = eng.ctx
+    # the CPU baseline continues from this state (iterations W+1, W+2: the
+    # first iterations of the GPU's timed window); grad_u is implicit on the
+    # device (u_mean + D u_tilde), so the host rebuilds it instead of reading it
+    cpu_start = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu_start = dict(F=np.array(st.F), lam=np.array(st.lam), u_tilde=np.array(st.u_tilde),
+                         u_mean=np.array(st.u_mean), rho=st.rho, r_d_prev=st.r_d_prev,
+                         outer_iter=st.outer_iter)
     ctx.synchronize()
-    ctx.profile_read(reset=True)
-    ctx.profile_enable(True)
+    ctx.profile_enable(False)
+    ctx.profile_read(reset=True)  # launch counts are kept with profiling off
     sampler = ClockSampler(dev)
     sampler.start()
     sampler.wait_ready()
@@ -208,7 +227,7 @@ def run_ours(args, rank, world, dist):
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     # the library runs on its own stream; bracket it from the torch stream with
-    # full synchronisation on both sides (outer_iteration ends in a host sync)
+    # full synchronisation on both sides (solve() ends in a host sync)
     t0.record()
     torch.cuda.synchronize()
     w0 = time.perf_counter()
@@ -224,14 +243,25 @@ def run_ours(args, rank, world, dist):
     torch.cuda.synchronize()
     clocks = sampler.stop()
     ms_total = max(t0.elapsed_time(t1), (w1 - w0) * 1e3)
-    ctx.profile_enable(False)
-    stage_ms, stage_launch = ctx.profile_read(reset=True)
+    _, launches_timed = ctx.profile_read(reset=True)
     if dist is not None:
         t = torch.tensor([ms_total], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     sweeps = st.total_sweeps
     point_sweeps = eng.point_sweeps - ps0
+
+    # ---- per-stage device times: a SEPARATE profiled pass (the next K
+    # iterations of the same trajectory, CUDA events around every stage on
+    # the library's stream), so the timed region above carries no event
+    # instrumentation
+    ctx.profile_enable(True)
+    ps1 = eng.point_sweeps
+    mm.solve(grid, model, bc, params, policy=pol, state=st, raise_on_max=False)
+    ctx.synchronize()
+    ctx.profile_enable(False)
+    stage_ms, stage_launch = ctx.profile_read(reset=True)
+    prof_point_sweeps = eng.point_sweeps - ps1
 
     # ---- e2e through the public API with host buffers: solve() on a host
     # state (fresh engine: H2D of F, grad_u, lam, moduli), K iterations, then
@@ -271,15 +301,7 @@ def run_ours(args, rank, world, dist):
     value = world * M * args.steps / (ms_total / 1e3)
     e2e_value = world * M * args.steps / (e2e_ms / 1e3)
     peak, peak_kind = measured_peak()
-    sb = stage_bytes(n)
-    per_stage = {}
-    for s_name, ms in stage_ms.items():
-        nl = stage_launch.get(s_name, 0)
-        if nl and s_name in sb:
-            avg = ms / nl
-            per_stage[s_name] = {"ms_total": round(ms, 4), "launches": nl,
-                                 "ms_per_launch": round(avg, 5),
-                                 "GBps": round(sb[s_name] / (avg / 1e3) / 1e9, 1)}
+    per_stage = _stage_report(stage_ms, stage_launch, stage_bytes(n))
     dom = max(per_stage, key=lambda k: per_stage[k]["ms_total"]) if per_stage else None
     traffic = None
     try:
@@ -293,15 +315,17 @@ def run_ours(args, rank, world, dist):
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic,
                 "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"
-                if peak_kind == "measured" else "fallback B200_PROFILING.md"}
+                if peak_kind == "measured" else "fallback B200_PROFILING.md",
+                "timing": "average launch duration from CUDA events on the library stream in "
+                          "the profiled pass (iterations after the timed window)"}
     it_ms = ms_total / args.steps
     roof_it = {"bound": "hbm", "B_alg_per_voxel": B_ALG_MR3,
                "achieved": round(B_ALG_MR3 * M / (it_ms / 1e3) / 1e9, 1), "peak": peak,
                "unit": "GB/s", "frac": round(B_ALG_MR3 * M / (it_ms / 1e3) / 1e9 / peak, 4)}
     local_ms = sum(stage_ms.get(k, 0.0) for k in ("local", "fused"))
     local_fp64 = None
-    if local_ms > 0 and point_sweeps > 0:
-        tf = point_sweeps * F_SWEEP_MR3 / (local_ms / 1e3) / 1e12
+    if local_ms > 0 and prof_point_sweeps > 0:
+        tf = prof_point_sweeps * F_SWEEP_MR3 / (local_ms / 1e3) / 1e12
         pk, pk_src = fp64_peak_tflops()
         local_fp64 = {"bound": "fp64", "stages": ["local", "fused"],
                       "point_sweeps_per_voxel_iter": round(point_sweeps / (M * args.steps), 3),
@@ -333,10 +357,12 @@ def run_ours(args, rank, world, dist):
         "residuals_last": {"r_p": hist[-1].r_p, "r_d": hist[-1].r_d, "r_l": hist[-1].r_l,
                            "rho": hist[-1].rho},
         "stages": per_stage,
+        "stages_pass": f"profiled pass, outer iterations {args.warmup + args.steps + 1}.."
+                       f"{args.warmup + 2 * args.steps} (not the timed region)",
         "roofline": roof,
         "roofline_iteration": roof_it,
         "roofline_local_fp64": local_fp64,
-        "gpu_launches": int(sum(stage_launch.values())),
+        "gpu_launches": int(sum(launches_timed.values())),
         "clocks": clocks,
         "e2e": {"value": e2e_value, "unit": "voxel-iter/s", "h2d_bytes_per_step": h2d / args.steps,
                 "d2h_bytes_per_step": d2h / args.steps,
@@ -347,8 +373,8 @@ def run_ours(args, rank, world, dist):
                        "updates both in place, and of grad_u, u_tilde into fresh host arrays; "
                        "wall clock"},
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.cpu_n, args.cpu_steps)
+    if cpu_start is not None:
+        line["cpu_baseline"] = cpu_baseline(n, args.cpu_steps, cpu_start)
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -445,44 +471,54 @@ def run_slab(args, rank, world, dist):
 
 
 
-def cpu_baseline(n, steps, warm=1):
-    """Oracle port on the host cores, bounded sample of the same workload."""
+def _oracle_setup(n):
     import oracle
 
     cores = len(os.sched_getaffinity(0))
     oracle.set_threads(cores)
+    # the reference's transforms: scipy.fft with workers = the host cores
+    # (grid.py:213-220 with set_workers(available_cores()))
+    oracle.set_fft("scipy", cores)
     mu, kap = laminate(n, 3)
     om = oracle.MR(mu, kap, dim=3, mu_rep=1.0)
     mask = np.ones((3, 3), bool)
     val = np.diag([0.95, 1.0, 1.0])
+    return oracle, cores, om, mask, val
+
+
+def cpu_baseline(n, steps, start):
+    """Oracle port on the host cores, bounded sample of the same workload:
+    outer iterations W+1 .. W+steps of the same trajectory, continued from the
+    GPU's state after its W warm-up iterations (the first iterations of the
+    GPU's timed window), so the sample needs no CPU warm-up."""
+    oracle, cores, om, mask, val = _oracle_setup(n)
     params = oracle.Params()
     st = oracle.init_state(3, n, om, mask, val, params)
-    st.F = st.F + 1e-4 * np.random.default_rng(0).standard_normal(st.F.shape)
+    st.F = np.array(start["F"])
+    st.lam = np.array(start["lam"])
+    st.u_tilde = np.array(start["u_tilde"])
+    st.u_mean = np.array(start["u_mean"])
+    st.grad_u = oracle.core.stencil_grad(3, n, 0.5, st.u_tilde) + st.u_mean
+    st.rho, st.r_d_prev, st.outer_iter = start["rho"], start["r_d_prev"], start["outer_iter"]
     sym = oracle.symbols(3, n, 0.5)
     pol = oracle.RatioToDual(0.3)
-    for _ in range(warm):
-        oracle.outer_iteration(3, n, 0.5, om, st, params, mask, val, pol, sym=sym)
     t0 = time.perf_counter()
     for _ in range(steps):
         oracle.outer_iteration(3, n, 0.5, om, st, params, mask, val, pol, sym=sym)
     dt = time.perf_counter() - t0
+    i0 = start["outer_iter"]
     return {"value": n ** 3 * steps / dt, "unit": "voxel-iter/s", "cores": cores, "kind": "port",
-            "sample": f"oracle port (C local kernels + numpy FFT), same laminate at {n}^3, "
-                      f"outer iterations {warm + 1}..{warm + steps}, {dt:.1f} s"}
+            "sample": f"oracle port (C local kernels on {cores} threads + scipy.fft with "
+                      f"{cores} workers, numpy einsum), same laminate at {n}^3, outer "
+                      f"iterations {i0 + 1}..{i0 + steps} (the first {steps} of the GPU's "
+                      f"timed window, continued from its warm-up state), {dt:.1f} s"}
 
 
 def run_reference(args, rank):
     if rank != 0:
         return
-    import oracle
-
-    n = args.cpu_n
-    cores = len(os.sched_getaffinity(0))
-    oracle.set_threads(cores)
-    mu, kap = laminate(n, 3)
-    om = oracle.MR(mu, kap, dim=3, mu_rep=1.0)
-    mask = np.ones((3, 3), bool)
-    val = np.diag([0.95, 1.0, 1.0])
+    n = args.n
+    oracle, cores, om, mask, val = _oracle_setup(n)
     params = oracle.Params()
     st = oracle.init_state(3, n, om, mask, val, params)
     st.F = st.F + 1e-4 * np.random.default_rng(0).standard_normal(st.F.shape)
@@ -495,15 +531,19 @@ def run_reference(args, rank):
         oracle.outer_iteration(3, n, 0.5, om, st, params, mask, val, pol, sym=sym)
     dt = time.perf_counter() - t0
     v = n ** 3 * args.steps / dt
-    sample = (f"oracle port (C local kernels + numpy FFT) of the same laminate workload at {n}^3, "
-              f"outer iterations {args.warmup + 1}..{args.warmup + args.steps}")
+    sample = (f"oracle port (C local kernels on {cores} threads + scipy.fft with {cores} workers, "
+              f"numpy einsum) of the same laminate workload at {n}^3, outer iterations "
+              f"{args.warmup + 1}..{args.warmup + args.steps} (the GPU arm's timed window)")
     print(json.dumps({
         "impl": "reference", "metric": "voxel-ADMM-iterations/sec (fp64)", "value": v,
         "unit": "voxel-iter/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (config-2 laminate inputs, seeded)",
-        "config": {"workload": f"3D neo-Hookean laminate (SURVEY 8(d) config 2 inputs), CPU "
-                               f"sample at {n}^3", "grid": n},
+        "config": {"workload": f"3D neo-Hookean laminate {n}^3 (SURVEY 8(d) config 2 inputs at "
+                               f"the metric's {n}^3), same as the GPU arm", "grid": n,
+                   "same_config": True,
+                   "steps_are": f"outer iterations {args.warmup + 1}..{args.warmup + args.steps}"
+                                f" from init_state"},
         "cpu_baseline": {"value": v, "unit": "voxel-iter/s", "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": v, "unit": "voxel-iter/s", "h2d_bytes_per_step": 0,
@@ -518,7 +558,6 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-n", type=int, default=128)
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--exchange", default="push", choices=["push", "collective"],

@@ -72,7 +72,7 @@ def lib():
 _FFT = np.fft  # transforms of project / frank_force (set_fft)
 
 
-def set_fft(name: str):
+def set_fft(name: str, workers: int | None = None):
     """Transforms of the projection and the Frank force: "numpy" (pocketfft,
     numpy's build; the default the goldens pin) or "scipy" (scipy.fft, the
     module the reference itself calls, grid.py:32,195-220).  The two are the
@@ -83,10 +83,24 @@ def set_fft(name: str):
         _FFT = np.fft
     elif name == "scipy":
         import scipy.fft
-        _FFT = scipy.fft
+        _FFT = scipy.fft if workers is None else _ScipyWorkers(scipy.fft, int(workers))
     else:
         raise ValueError(name)
     return _FFT
+
+
+class _ScipyWorkers:
+    """scipy.fft with a fixed worker count, as the reference calls it
+    (grid.py:213-220: ``workers=get_workers()``)."""
+
+    def __init__(self, mod, workers):
+        self.mod, self.workers = mod, workers
+
+    def rfftn(self, a, **kw):
+        return self.mod.rfftn(a, workers=self.workers, **kw)
+
+    def irfftn(self, a, **kw):
+        return self.mod.irfftn(a, workers=self.workers, **kw)
 
 
 def set_threads(n: int) -> int:

@@ -21,18 +21,19 @@ def _run(args, timeout=600):
 
 
 def test_reference_arm_line():
-    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "1", "--cpu-n", "16"])
+    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "1", "--n", "16"])
     assert d["impl"] == "reference"
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
               "higher_is_better", "scaling", "dtype", "config", "cpu_baseline", "e2e"):
         assert k in d, k
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"] > 0
+    assert d["config"]["grid"] == 16 and d["config"]["same_config"]
 
 
 @pytest.mark.gpu
 def test_our_line_small_grid():
-    d = _run(["--n", "32", "--steps", "3", "--warmup", "3", "--no-cpu-baseline"])
+    d = _run(["--n", "32", "--steps", "3", "--warmup", "3"])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
               "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
               "roofline", "e2e", "gpu_launches", "clocks"):
@@ -43,3 +44,5 @@ def test_our_line_small_grid():
     assert r["unit"] == "GB/s" and 0 < r["frac"] and r["peak"] > 0
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    c = d["cpu_baseline"]
+    assert c["kind"] == "port" and c["value"] > 0 and "4..5" in c["sample"]
