@@ -200,6 +200,14 @@ class ADMMState:
             self._host[nm] = target
             self._stale.discard(nm)
 
+    def detach_caller_arrays(self):
+        """Stop writing solve() results back into the F / lam arrays the
+        caller handed in (see _writeback_inplace).  Those arrays keep the
+        values of the last solve; the state's attributes keep returning the
+        current (device) values.  For device-resident loops that never read
+        the caller's arrays: saves one D2H of F and lam per solve() call."""
+        self._inplace.clear()
+
     def _mark_device(self, *names):
         """Fields just rewritten on the device: host copies are stale."""
         for nm in names:
