@@ -466,15 +466,19 @@ def run_lce(args, rank, world, dist):
         om = oracle.LCE(n0=on0, **kw)
         op = oracle.Params()
         ost = oracle.init_state(3, cn, om, np.zeros((3, 3), bool), np.zeros((3, 3)), op)
+        z = (np.zeros((3, 3), bool), np.zeros((3, 3)))
+        # iteration 1 runs at the RatioToDual start tolerance (1.0); the timed
+        # iterations 2..3 are in the capped-Newton regime of the GPU's window
+        oracle.outer_iteration(3, cn, 0.5, om, ost, op, *z, oracle.RatioToDual(0.3))
         t0c = time.perf_counter()
-        oracle.outer_iteration(3, cn, 0.5, om, ost, op, np.zeros((3, 3), bool),
-                               np.zeros((3, 3)), oracle.RatioToDual(0.3))
+        for _ in range(2):
+            oracle.outer_iteration(3, cn, 0.5, om, ost, op, *z, oracle.RatioToDual(0.3))
         dtc = time.perf_counter() - t0c
         line["cpu_baseline"] = {
-            "value": cn ** 3 / dtc, "unit": "voxel-iter/s", "cores": cores, "kind": "port",
+            "value": 2 * cn ** 3 / dtc, "unit": "voxel-iter/s", "cores": cores, "kind": "port",
             "sample": f"oracle port (C LCE Newton kernels on {cores} threads), the same material "
-                      f"on a {cn}^3 polydomain grid, outer iteration 1, {dtc:.1f} s (the full "
-                      f"{n}^3 iteration is ~45 min of CPU time, SURVEY 8(d))"}
+                      f"on a {cn}^3 polydomain grid, outer iterations 2..3, {dtc:.1f} s (the "
+                      f"full {n}^3 iteration is ~45 min of CPU time, SURVEY 8(d))"}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
