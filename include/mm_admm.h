@@ -257,13 +257,25 @@ int mm_update_and_sweep(mm_ctx *ctx, int material, double rho_next, double tol,
 
 /* Slab decomposition: rank `rank` of `nranks` holds planes
  * [rank*n/nranks, (rank+1)*n/nranks) of a 3D n^3 grid (n divisible by
- * nranks, n even).  Fields (upload/download/local_sweeps) are the local
- * slab's.  The projection runs as the steps below, with the host moving the
- * halo planes between neighbours (HALO_OUT -> neighbour's HALO_IN) and doing
- * the two all-to-all exchanges of SEND -> RECV (after MM_SLAB_FWD) and RECV ->
- * SEND (after MM_SLAB_SOLVE), e.g. NCCL via torch.distributed:
- *   HALO_T, [exchange], FWD, [all-to-all], SOLVE, [all-to-all back], INV,
- *   HALO_U, [exchange], UPDATE (sums[0..10] = |dG|^2, |misfit|^2, sum lam)
+ * nranks, n even).  Fields (upload/download/local sweeps/the fused update
+ * calls) are the local slab's; mm_local_sweeps, mm_update_and_sweep and
+ * mm_update_multiplier run unchanged on a slab context (their u stencil
+ * reads the ghost planes below).  The projection + residual pass of the
+ * fused schedule (mm_project_residuals on one context) is the step sequence
+ *   HALO_T, [T halo exchange: HALO_OUT_LO -> lower neighbour's HALO_IN_HI,
+ *            HALO_OUT_HI -> upper neighbour's HALO_IN_LO],
+ *   FWD, [all-to-all SEND -> RECV], SOLVE, [all-to-all RECV -> SEND], INV,
+ *   [u ghost exchange of the MM_SLAB_FIELD_U_NEW buffer], RES
+ * and the LCE frozen data (mm_prepare_frozen on one context) is
+ *   DIRECTOR, [2-plane ghost exchange of MM_SLAB_FIELD_DIRECTOR], FRANK.
+ * Ghost exchange of a field (mm_slab_field: ncomp components, component
+ * stride cs doubles, g ghost planes of n*n doubles on each face, base = plane
+ * 0): planes 0..g-1 go to the lower neighbour's planes nl..nl+g-1, planes
+ * nl-g..nl-1 to the upper neighbour's planes -g..-1.
+ * Every step only enqueues work on the context stream (mm_slab_stream), so
+ * NCCL exchanges issued on that stream between the steps need no host
+ * synchronisation; RES returns its two local sums (|dG|^2, |misfit|^2) and
+ * is the one step that waits for the stream.
  * Buffers: MM_SLAB_BUF_SEND / RECV  nranks * 3 * (n/nranks)^2 * pitch complex,
  * [peer][c][i0l][i1l][k2]; HALO_*  3 * n^2 doubles [c][i1][i2]. */
 /* Peer-memory variant of the two transposes (no separate all-to-all):
@@ -273,22 +285,35 @@ int mm_update_and_sweep(mm_ctx *ctx, int material, double rho_next, double tol,
  * tile into the SEND buffer of its source rank -- the transfer overlaps the
  * FFT tile by tile over NVLink/NVSwitch peer stores.  Sequence:
  *   HALO_T, [exchange], FWD_PUSH, [barrier], SOLVE_PUSH, [barrier], INV, ...
- * The barriers are host-side (every rank's step has returned, i.e. its
- * kernels completed); no kernel waits on another rank.  Peer buffers are
+ * The barrier orders every rank's push kernel before the next step on any
+ * rank (a stream-ordered collective, or a host barrier after a stream
+ * synchronise); no kernel waits on another rank.  Peer buffers are
  * registered with mm_slab_set_peers (device pointers usable in this process,
  * e.g. ranks sharing one process) or mm_slab_open_peers (CUDA IPC handles of
  * the other processes' buffers, from mm_slab_ipc_handle). */
 enum mm_slab_step {
-    MM_SLAB_HALO_T = 0, MM_SLAB_FWD = 1, MM_SLAB_SOLVE = 2, MM_SLAB_INV = 3, MM_SLAB_HALO_U = 4,
-    MM_SLAB_UPDATE = 5, MM_SLAB_GRAD = 6, MM_SLAB_FWD_PUSH = 7, MM_SLAB_SOLVE_PUSH = 8
+    MM_SLAB_HALO_T = 0, MM_SLAB_FWD = 1, MM_SLAB_SOLVE = 2, MM_SLAB_INV = 3,
+    /* 4..6 retired in ABI 2 (explicit-gradient slab steps) */
+    MM_SLAB_FWD_PUSH = 7, MM_SLAB_SOLVE_PUSH = 8, MM_SLAB_RES = 9, MM_SLAB_DIRECTOR = 10,
+    MM_SLAB_FRANK = 11
 };
 enum mm_slab_buffer {
     MM_SLAB_BUF_SEND = 0, MM_SLAB_BUF_RECV = 1, MM_SLAB_BUF_HALO_OUT_LO = 2,
     MM_SLAB_BUF_HALO_OUT_HI = 3, MM_SLAB_BUF_HALO_IN_LO = 4, MM_SLAB_BUF_HALO_IN_HI = 5
 };
+enum mm_slab_field_id {
+    MM_SLAB_FIELD_U_NEW = 0,    /* u_tilde being produced by INV (consumed by RES) */
+    MM_SLAB_FIELD_U = 1,        /* current u_tilde */
+    MM_SLAB_FIELD_DIRECTOR = 2  /* LCE director written by DIRECTOR (consumed by FRANK) */
+};
 int mm_create_slab(int n, double length, int nranks, int rank, int device, mm_ctx **out);
 int mm_slab_buffer(mm_ctx *ctx, int which, void **dev_ptr, int64_t *nbytes);
+/* u_mean (9 doubles) is read by RES only; sums (>= 2 doubles) written by RES only. */
 int mm_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, double *sums);
+int mm_slab_field(mm_ctx *ctx, int which, void **base, int64_t *cstride, int *ncomp,
+                  int *ghost);
+/* The context's CUDA stream (cudaStream_t), for collectives ordered with its work. */
+int mm_slab_stream(mm_ctx *ctx, void **stream);
 /* which = MM_SLAB_BUF_RECV (targets of FWD_PUSH) or MM_SLAB_BUF_SEND (targets
  * of SOLVE_PUSH).  ptrs[q] = rank q's buffer, P = nranks. */
 int mm_slab_set_peers(mm_ctx *ctx, int which, void *const *ptrs, int P);

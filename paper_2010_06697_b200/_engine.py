@@ -27,11 +27,25 @@ STATE_FIELDS = {
 
 
 class Engine:
-    """Device context for one grid (mm_create) with symbols uploaded."""
+    """Device context for one grid (mm_create) with symbols uploaded, or --
+    with a communicator -- this rank's slab of it (slab.SlabContext: the
+    same surface, global reductions)."""
 
-    def __init__(self, grid: Grid, device=None):
+    def __init__(self, grid: Grid, device=None, comm=None):
         self.grid = grid
-        self.ctx = _lib.Context(grid.dim, n=grid.n, length=grid.length, device=device)
+        self.comm = comm
+        if comm is not None:
+            from .slab import DeviceSlabBackend, SlabContext, SlabLayout
+            lay = SlabLayout(grid.n, comm.P, comm.rank, grid.length, grid.dim)
+            make = getattr(comm, "make_backend", None)
+            backend = make(lay) if make is not None else DeviceSlabBackend(lay, device)
+            self.ctx = SlabContext(lay, comm, backend)
+            self.shape = lay.local_shape
+            self.npts = lay.npts_local
+        else:
+            self.ctx = _lib.Context(grid.dim, n=grid.n, length=grid.length, device=device)
+            self.shape = grid.shape
+            self.npts = grid.npoints
         tab, thresh = axis_symbol_tables(grid)
         self.ctx.set_symbols(tab, thresh)
         # grad_u storage policy (include/mm_admm.h, MM_OPT_IMPLICIT_GRAD)
@@ -46,14 +60,32 @@ class Engine:
         self.lam_sum = None        # device-side sum of lam (None: recompute)
         self.point_sweeps = 0.0    # local sweeps summed over points (work counter)
 
-    def matches(self, grid: Grid) -> bool:
-        return self.grid == grid
+    @property
+    def distributed(self) -> bool:
+        return self.comm is not None
+
+    def matches(self, grid: Grid, comm=None) -> bool:
+        return self.grid == grid and self.comm is comm
+
+    def field_shape(self, rank: int):
+        return self.shape + (self.grid.dim,) * rank
+
+    def check_field(self, val, rank, name):
+        if self.comm is None:
+            self.grid.check_field(val, rank, name)
+            return
+        want = self.field_shape(rank)
+        if np.shape(val) != want:
+            from .errors import ConfigurationError
+            raise ConfigurationError(f"{name} has shape {np.shape(val)}, this rank's slab is {want}")
 
     def bind_model(self, model):
         ver = getattr(model, "_device_version", 0)
         if self.model is model and self.model_version == ver:
             return
-        model._device_bind(self.ctx, self.grid.npoints)
+        model._device_bind(self.ctx, self.npts)
+        if self.comm is not None:
+            model._globalize(self.comm)
         self.model = model
         self.model_version = ver
 

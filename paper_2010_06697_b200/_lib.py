@@ -43,11 +43,13 @@ EXPORTS = (
     "mm_create_slab", "mm_slab_buffer", "mm_slab_step", "mm_add_field",
     "mm_equilibrium_residual", "mm_selftest_log", "mm_slab_set_peers", "mm_slab_ipc_handle",
     "mm_slab_open_peers", "mm_bloch_setup", "mm_bloch_start", "mm_bloch_iterate",
-    "mm_bloch_mode", "mm_debug_lce_counters", "mm_residuals_and_step",
+    "mm_bloch_mode", "mm_debug_lce_counters", "mm_residuals_and_step", "mm_slab_field",
+    "mm_slab_stream",
 )
 
-SLAB_HALO_T, SLAB_FWD, SLAB_SOLVE, SLAB_INV, SLAB_HALO_U, SLAB_UPDATE, SLAB_GRAD = range(7)
-SLAB_FWD_PUSH, SLAB_SOLVE_PUSH = 7, 8
+SLAB_HALO_T, SLAB_FWD, SLAB_SOLVE, SLAB_INV = range(4)
+SLAB_FWD_PUSH, SLAB_SOLVE_PUSH, SLAB_RES, SLAB_DIRECTOR, SLAB_FRANK = 7, 8, 9, 10, 11
+SLAB_FIELD_U_NEW, SLAB_FIELD_U, SLAB_FIELD_DIRECTOR = range(3)
 SLAB_BUF_SEND, SLAB_BUF_RECV, SLAB_BUF_HALO_OUT_LO, SLAB_BUF_HALO_OUT_HI = range(4)
 SLAB_BUF_HALO_IN_LO, SLAB_BUF_HALO_IN_HI = 4, 5
 
@@ -221,6 +223,9 @@ def load_library():
             "mm_bloch_iterate": ([P, I, D, D, D, D, P], I),
             "mm_bloch_mode": ([P, P], I),
             "mm_debug_lce_counters": ([P, I], I),
+            "mm_slab_field": ([P, I, PP, ctypes.POINTER(I64), ctypes.POINTER(I),
+                               ctypes.POINTER(I)], I),
+            "mm_slab_stream": ([P, PP], I),
             "mm_residuals_and_step": ([P, ctypes.POINTER(StepParamsC), ctypes.POINTER(StepResultC),
                                        ctypes.POINTER(LocalStatsC)], I),
         }
@@ -480,10 +485,29 @@ class Context:
 
     def slab_step(self, step, rho, u_mean=None):
         sums = np.zeros(11)
-        um = None if u_mean is None else np.ascontiguousarray(u_mean, dtype=np.float64).reshape(-1)
+        um = None
+        if u_mean is not None:
+            um = np.zeros(9)
+            u = np.asarray(u_mean, dtype=np.float64).reshape(-1)
+            um[: u.size] = u
         self.check(self.lib.mm_slab_step(self.h, int(step), float(rho),
                                          _ptr(um) if um is not None else None, _ptr(sums)))
         return sums
+
+    def slab_field(self, which):
+        """(device pointer of plane 0, component stride, components, ghost planes)."""
+        base = ctypes.c_void_p()
+        cs = ctypes.c_int64()
+        nc = ctypes.c_int()
+        g = ctypes.c_int()
+        self.check(self.lib.mm_slab_field(self.h, int(which), ctypes.byref(base), ctypes.byref(cs),
+                                          ctypes.byref(nc), ctypes.byref(g)))
+        return base.value, cs.value, nc.value, g.value
+
+    def slab_stream(self):
+        st = ctypes.c_void_p()
+        self.check(self.lib.mm_slab_stream(self.h, ctypes.byref(st)))
+        return st.value
 
 
 class DeviceArray:

@@ -347,20 +347,27 @@ static bool is_pinned(const void *p) {
 }
 
 static void launch_xpose(mm_ctx *ctx, bool to_soa, bool add, double *dev, int64_t p0, int64_t np,
-                         int ncomp) {
+                         int ncomp, int64_t cs) {
     const int threads = 256;
     const int blocks = (int)std::min<int64_t>((np * ncomp + threads - 1) / threads, 148 * 32);
     if (!to_soa)
-        k_soa_to_aos<<<blocks, threads, 0, ctx->stream>>>(dev, ctx->stage, p0, np, ncomp, ctx->M);
+        k_soa_to_aos<<<blocks, threads, 0, ctx->stream>>>(dev, ctx->stage, p0, np, ncomp, cs);
     else if (add)
-        k_aos_add_soa<<<blocks, threads, 0, ctx->stream>>>(ctx->stage, dev, p0, np, ncomp, ctx->M);
+        k_aos_add_soa<<<blocks, threads, 0, ctx->stream>>>(ctx->stage, dev, p0, np, ncomp, cs);
     else
-        k_aos_to_soa<<<blocks, threads, 0, ctx->stream>>>(ctx->stage, dev, p0, np, ncomp, ctx->M);
+        k_aos_to_soa<<<blocks, threads, 0, ctx->stream>>>(ctx->stage, dev, p0, np, ncomp, cs);
+}
+
+// component stride of a field's device storage (u_tilde keeps ghost planes
+// on a slab)
+static int64_t field_cs(const mm_ctx *ctx, int field) {
+    return field == MM_FIELD_UT ? ctx->uM : ctx->M;
 }
 
 static int transfer(mm_ctx *ctx, double *dev, int ncomp, const double *hsrc, double *hdst,
-                    bool add = false) {
+                    bool add = false, int64_t cs = -1) {
     const int64_t M = ctx->M;
+    if (cs < 0) cs = M;
     const int64_t chunk_pts =
         std::max<int64_t>(1, std::min<int64_t>(M, (int64_t)(kChunkBytes / (8 * ncomp))));
     int rc = ensure_stage(ctx, chunk_pts * ncomp);
@@ -380,9 +387,9 @@ static int transfer(mm_ctx *ctx, double *dev, int ncomp, const double *hsrc, dou
             if (up) {
                 MM_CUDA(ctx, cudaMemcpyAsync(ctx->stage, hsrc + p0 * ncomp, bytes,
                                              cudaMemcpyHostToDevice, ctx->stream));
-                launch_xpose(ctx, true, add, dev, p0, np, ncomp);
+                launch_xpose(ctx, true, add, dev, p0, np, ncomp, cs);
             } else {
-                launch_xpose(ctx, false, false, dev, p0, np, ncomp);
+                launch_xpose(ctx, false, false, dev, p0, np, ncomp, cs);
                 MM_CUDA(ctx, cudaMemcpyAsync(hdst + p0 * ncomp, ctx->stage, bytes,
                                              cudaMemcpyDeviceToHost, ctx->stream));
             }
@@ -405,7 +412,7 @@ static int transfer(mm_ctx *ctx, double *dev, int ncomp, const double *hsrc, dou
             MM_CUDA(ctx, cudaMemcpyAsync(ctx->stage, g_pinned.half[h], bytes,
                                          cudaMemcpyHostToDevice, ctx->stream));
             MM_CUDA(ctx, cudaEventRecord(ctx->xfer_ev[h], ctx->stream));
-            launch_xpose(ctx, true, add, dev, p0, np, ncomp);
+            launch_xpose(ctx, true, add, dev, p0, np, ncomp, cs);
             MM_LAUNCH_CHECK(ctx);
         }
     } else {
@@ -414,7 +421,7 @@ static int transfer(mm_ctx *ctx, double *dev, int ncomp, const double *hsrc, dou
                 int64_t p0, np;
                 span(i, p0, np);
                 const int h = (int)(i & 1);
-                launch_xpose(ctx, false, false, dev, p0, np, ncomp);
+                launch_xpose(ctx, false, false, dev, p0, np, ncomp, cs);
                 MM_LAUNCH_CHECK(ctx);
                 MM_CUDA(ctx, cudaMemcpyAsync(g_pinned.half[h], ctx->stage,
                                              sizeof(double) * np * ncomp,
@@ -495,6 +502,7 @@ int mm_create(int dim, int n, double length, int device, mm_ctx **out) {
     ctx->nh = n / 2 + 1;
     ctx->P = (ctx->nh + 7) / 8 * 8;
     ctx->nrows = ctx->M / n;
+    ctx->uM = ctx->dM = ctx->M;
     ctx->device = device;
     *out = ctx;
     int rc;
@@ -570,7 +578,13 @@ int mm_create_slab(int n, double length, int nranks, int rank, int device, mm_ct
     TRY(mm_alloc(ctx, (void **)&ctx->F, sizeof(double) * 9 * M));
     TRY(mm_alloc(ctx, (void **)&ctx->G, sizeof(double) * 9 * M));
     TRY(mm_alloc(ctx, (void **)&ctx->Lam, sizeof(double) * 9 * M));
-    TRY(mm_alloc(ctx, (void **)&ctx->Ut, sizeof(double) * 3 * M));
+    // u_tilde double buffer with one ghost plane on each slab face
+    ctx->uM = M + 2 * nn;
+    ctx->dM = M + 4 * nn;
+    TRY(mm_alloc(ctx, (void **)&ctx->Ut_base, sizeof(double) * 3 * ctx->uM));
+    TRY(mm_alloc(ctx, (void **)&ctx->Ut2_base, sizeof(double) * 3 * ctx->uM));
+    ctx->Ut = ctx->Ut_base + nn;
+    ctx->Ut2 = ctx->Ut2_base + nn;
     TRY(mm_alloc(ctx, (void **)&ctx->spec, sizeof(double2) * 3 * ctx->nrows * ctx->P));
     const int64_t bufc = (int64_t)nranks * 3 * nl * nl * ctx->P;
     // exchange buffers by plain cudaMalloc: CUDA IPC exports need it
@@ -589,7 +603,8 @@ int mm_create_slab(int n, double length, int nranks, int rank, int device, mm_ct
     MM_CUDA(ctx, cudaMemset(ctx->F, 0, sizeof(double) * 9 * M));
     MM_CUDA(ctx, cudaMemset(ctx->G, 0, sizeof(double) * 9 * M));
     MM_CUDA(ctx, cudaMemset(ctx->Lam, 0, sizeof(double) * 9 * M));
-    MM_CUDA(ctx, cudaMemset(ctx->Ut, 0, sizeof(double) * 3 * M));
+    MM_CUDA(ctx, cudaMemset(ctx->Ut_base, 0, sizeof(double) * 3 * ctx->uM));
+    MM_CUDA(ctx, cudaMemset(ctx->Ut2_base, 0, sizeof(double) * 3 * ctx->uM));
     MM_CUDA(ctx, cudaMemset(ctx->spec, 0, sizeof(double2) * 3 * ctx->nrows * ctx->P));
     MM_CUDA(ctx, cudaMemset(ctx->sendbuf, 0, sizeof(double2) * bufc));
     MM_CUDA(ctx, cudaMemset(ctx->recvbuf, 0, sizeof(double2) * bufc));
@@ -626,10 +641,40 @@ int mm_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, double
     if (!(rho > 0.0) || !isfinite(rho))
         return mm_fail(ctx, MM_ERR_PARAM, "rho must be positive and finite, got %g", rho);
     if (!ctx->have_sym) return mm_fail(ctx, MM_ERR_CONFIG, "symbols were never set");
-    if ((step == MM_SLAB_UPDATE || step == MM_SLAB_GRAD) && !u_mean) return MM_ERR_PARAM;
-    if (step == MM_SLAB_UPDATE && !sums) return MM_ERR_PARAM;
+    if (step == MM_SLAB_RES && (!u_mean || !sums)) return MM_ERR_PARAM;
+    if (step >= 4 && step <= 6) return mm_fail(ctx, MM_ERR_PARAM, "slab step %d was retired", step);
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    // the projection reads F and lam (or T): a deferred ascent lands first
+    if (step == MM_SLAB_HALO_T || step == MM_SLAB_DIRECTOR) {
+        int rc = mm_flush_pending(ctx);
+        if (rc) return rc;
+    }
+    if (step == MM_SLAB_DIRECTOR || step == MM_SLAB_FRANK) return mm_run_slab_lce(ctx, step);
     return mm_run_slab_step(ctx, step, rho, u_mean, sums);
+}
+
+int mm_slab_field(mm_ctx *ctx, int which, void **base, int64_t *cstride, int *ncomp,
+                  int *ghost) {
+    if (!ctx || !base || !cstride || !ncomp || !ghost) return MM_ERR_PARAM;
+    if (!ctx->slab_mode) return mm_fail(ctx, MM_ERR_CONFIG, "not a slab context");
+    *ncomp = 3;
+    switch (which) {
+        case MM_SLAB_FIELD_U_NEW: *base = ctx->Ut2; *cstride = ctx->uM; *ghost = 1; break;
+        case MM_SLAB_FIELD_U: *base = ctx->Ut; *cstride = ctx->uM; *ghost = 1; break;
+        case MM_SLAB_FIELD_DIRECTOR: {
+            int rc = mm_slab_alloc_director(ctx);
+            if (rc) return rc;
+            *base = ctx->dirbuf; *cstride = ctx->dM; *ghost = 2; break;
+        }
+        default: return mm_fail(ctx, MM_ERR_PARAM, "unknown slab field %d", which);
+    }
+    return MM_OK;
+}
+
+int mm_slab_stream(mm_ctx *ctx, void **stream) {
+    if (!ctx || !stream) return MM_ERR_PARAM;
+    *stream = (void *)ctx->stream;
+    return MM_OK;
 }
 
 static int peer_table(mm_ctx *ctx, int which, double2 ****slot) {
@@ -700,6 +745,7 @@ int mm_create_points(int dim, int64_t npts, int device, mm_ctx **out) {
     ctx->dim = dim;
     ctx->n = 0;
     ctx->M = npts;
+    ctx->uM = ctx->dM = npts;
     ctx->D = dim * dim;
     ctx->device = device;
     ctx->points_only = true;
@@ -726,6 +772,9 @@ void mm_destroy(mm_ctx *ctx) {
     mm_drain_timings(ctx);
     for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
     mm_bloch_free(ctx);
+    if (ctx->Ut_base) ctx->Ut = ctx->Ut_base;
+    if (ctx->Ut2_base) ctx->Ut2 = ctx->Ut2_base;
+    if (ctx->dir_base) ctx->dirbuf = ctx->dir_base;
     double *ptrs[] = {ctx->F, ctx->G, ctx->Lam, ctx->Ut, ctx->prevF, ctx->modA, ctx->modB,
                       ctx->ang, ctx->chart, ctx->pinc, ctx->n0, ctx->ff, ctx->prevAng,
                       ctx->prevChart, ctx->prevPinc, ctx->dirbuf, ctx->Ut2, ctx->halo_in_lo,
@@ -808,7 +857,7 @@ int mm_upload(mm_ctx *ctx, int field, const double *host, int64_t count) {
         ctx->g_implicit = false;
         ctx->g_buf_valid = true;
     }
-    return transfer(ctx, *slot, ncomp, host, nullptr);
+    return transfer(ctx, *slot, ncomp, host, nullptr, false, field_cs(ctx, field));
 }
 
 int mm_add_field(mm_ctx *ctx, int field, const double *host, int64_t count) {
@@ -883,7 +932,7 @@ int mm_download(mm_ctx *ctx, int field, double *host, int64_t count) {
     if (!*slot) return mm_fail(ctx, MM_ERR_CONFIG, "field %d was never set", field);
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
     if (field == MM_FIELD_G && (rc = mm_materialize_G(ctx))) return rc;
-    return transfer(ctx, *slot, ncomp, nullptr, host);
+    return transfer(ctx, *slot, ncomp, nullptr, host, false, field_cs(ctx, field));
 }
 
 int mm_copy_field(mm_ctx *ctx, int dst_field, int src_field) {
@@ -912,8 +961,14 @@ int mm_copy_field(mm_ctx *ctx, int dst_field, int src_field) {
     }
     rc = ensure_field(ctx, ds, nd);
     if (rc) return rc;
-    MM_CUDA(ctx, cudaMemcpyAsync(*ds, *ss, sizeof(double) * nd * ctx->M,
-                                 cudaMemcpyDeviceToDevice, ctx->stream));
+    const int64_t dcs = field_cs(ctx, dst_field), scs = field_cs(ctx, src_field);
+    if (dcs == ctx->M && scs == ctx->M)
+        MM_CUDA(ctx, cudaMemcpyAsync(*ds, *ss, sizeof(double) * nd * ctx->M,
+                                     cudaMemcpyDeviceToDevice, ctx->stream));
+    else
+        for (int c = 0; c < nd; ++c)
+            MM_CUDA(ctx, cudaMemcpyAsync(*ds + c * dcs, *ss + c * scs, sizeof(double) * ctx->M,
+                                         cudaMemcpyDeviceToDevice, ctx->stream));
     if (dst_field == MM_FIELD_PREV_F) ctx->have_prev_F = true;
     if (dst_field == MM_FIELD_PREV_ANG) ctx->have_prev_int = true;
     if (dst_field == MM_FIELD_F) ctx->F_checked = false;
@@ -931,6 +986,8 @@ int mm_field_sums(mm_ctx *ctx, int field, double *out) {
     int rc = field_info(ctx, field, &slot, &ncomp);
     if (rc) return rc;
     if (!*slot) return mm_fail(ctx, MM_ERR_CONFIG, "field %d was never set", field);
+    if (field_cs(ctx, field) != ctx->M)
+        return mm_fail(ctx, MM_ERR_CONFIG, "field sums of u_tilde on a slab are not supported");
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
     return mm_run_field_sums(ctx, *slot, ncomp, out);
 }
@@ -1003,6 +1060,9 @@ int mm_prepare_frozen(mm_ctx *ctx) {
     if (!ctx) return MM_ERR_PARAM;
     ctx->gen++;  // invalidates a speculative projection front
     if (!ctx->have_lce) return mm_fail(ctx, MM_ERR_CONFIG, "LCE parameters were never set");
+    if (ctx->slab_mode)
+        return mm_fail(ctx, MM_ERR_CONFIG,
+                       "slab context: run MM_SLAB_DIRECTOR, the ghost exchange, MM_SLAB_FRANK");
     if (ctx->points_only) return mm_fail(ctx, MM_ERR_CONFIG, "point-set context has no grid");
     MM_CUDA(ctx, cudaSetDevice(ctx->device));
     int rc = mm_flush_pending(ctx);

@@ -108,6 +108,13 @@ struct mm_ctx {
     // slab decomposition (3D, split along axis 0)
     bool slab_mode = false;
     int slab_P = 1, slab_rank = 0, slab_nl = 0;
+    // component strides of the stencil inputs: u_tilde (Ut, Ut2) and the LCE
+    // director (dirbuf).  M on a single context; a slab keeps ghost planes
+    // on both faces (1 for u, 2 for the director: the radius-2 Frank stencil)
+    // so that axis-0 neighbours are plain offsets and the halo exchange
+    // writes straight into them.  Ut / Ut2 / dirbuf point at plane 0.
+    int64_t uM = 0, dM = 0;
+    double *Ut_base = nullptr, *Ut2_base = nullptr, *dir_base = nullptr;
     // peer-memory transposes: device tables of every rank's RECV / SEND buffer
     double2 **peer_recv = nullptr, **peer_send = nullptr;
     std::vector<void *> ipc_opened;  // closed at destroy
@@ -230,7 +237,7 @@ __device__ void grid_finalize(const double (&vals)[K], const int (&ops)[K], doub
 // when n is a power of two (shift/mask), else -1 (32-bit division)
 template <int DIM>
 __device__ __forceinline__ void nbr_offsets(int64_t p64, int n, int lgn, int (&off_p)[DIM],
-                                            int (&off_m)[DIM]) {
+                                            int (&off_m)[DIM], bool wrap0 = true) {
     const unsigned p = (unsigned)p64;
     unsigned c[DIM];
     if (lgn >= 0) {
@@ -253,6 +260,11 @@ __device__ __forceinline__ void nbr_offsets(int64_t p64, int n, int lgn, int (&o
         off_m[j] = (c[j] == 0) ? (n - 1) * stride : -stride;
         stride *= n;
     }
+    if (!wrap0) {  // slab: the planes beyond the slab faces are ghost planes
+        stride /= n;
+        off_p[0] = stride;
+        off_m[0] = -stride;
+    }
 }
 
 // Source of grad_u for the local step: the explicit field, or (implicit
@@ -265,6 +277,8 @@ struct GSrc {
     int n, lgn;
     double inv2h;
     int64_t M;
+    int64_t uM;       // component stride of U (M; slab: M + 2 ghost planes)
+    int wrap0;        // 0 (slab): axis-0 neighbours across the faces are U's ghost planes
 };
 
 template <int DIM>
@@ -276,10 +290,10 @@ __device__ __forceinline__ void gsrc_load(const GSrc &s, int64_t p, double (&g)[
         return;
     }
     int op[DIM], om[DIM];
-    nbr_offsets<DIM>(p, s.n, s.lgn, op, om);
+    nbr_offsets<DIM>(p, s.n, s.lgn, op, om, s.wrap0 != 0);
 #pragma unroll
     for (int i = 0; i < DIM; ++i) {
-        const double *u = s.U + (int64_t)i * s.M + p;
+        const double *u = s.U + (int64_t)i * s.uM + p;
 #pragma unroll
         for (int j = 0; j < DIM; ++j)
             g[i * DIM + j] = (__ldg(u + op[j]) - __ldg(u + om[j])) * s.inv2h + s.ubar[i * DIM + j];
@@ -319,6 +333,9 @@ int mm_run_frank_of_ff(mm_ctx *ctx);
 int mm_ilog2(int n);
 int mm_run_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, double *sums);
 GSrc mm_gsrc(mm_ctx *ctx);
+int mm_slab_res(mm_ctx *ctx, double rho, const double *u_mean, double *sums);
+int mm_run_slab_lce(mm_ctx *ctx, int step);
+int mm_slab_alloc_director(mm_ctx *ctx);
 int mm_materialize_G(mm_ctx *ctx);
 int mm_ensure_points(mm_ctx *ctx);
 int mm_flush_pending(mm_ctx *ctx);

@@ -864,29 +864,31 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
 // ---------------------------------------------------------------------------
 template <int DIM>
 __global__ void k_director(const double *__restrict__ ang, const double *__restrict__ chart,
-                           double *__restrict__ nout, int64_t M) {
+                           double *__restrict__ nout, int64_t M, int64_t cs) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
          p += (int64_t)gridDim.x * blockDim.x) {
         if (DIM == 2) {
             double s, c;
             sincos(ang[p], &s, &c);
             nout[p] = c;
-            nout[M + p] = s;
+            nout[cs + p] = s;
         } else {
             double E[9], n[3];
 #pragma unroll
             for (int i = 0; i < 9; ++i) E[i] = chart[i * M + p];
             n_from_chart(ang[p], ang[M + p], E, n);
 #pragma unroll
-            for (int i = 0; i < 3; ++i) nout[i * M + p] = n[i];
+            for (int i = 0; i < 3; ++i) nout[i * cs + p] = n[i];
         }
     }
 }
 
 // ff_i = 2 kappa / (4 h^2) sum_j (2 n_i - n_i(x + 2 e_j) - n_i(x - 2 e_j))
+// cs: component stride of nf; wrap0 = 0 (slab): nf keeps two ghost planes
+// on each face, so the axis-0 neighbours are plain offsets
 template <int DIM>
 __global__ void k_frank(const double *__restrict__ nf, double *__restrict__ ff, int n, int64_t M,
-                        double coef) {
+                        double coef, int64_t cs, int wrap0) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
          p += (int64_t)gridDim.x * blockDim.x) {
         unsigned q = (unsigned)p, c[DIM];
@@ -904,11 +906,15 @@ __global__ void k_frank(const double *__restrict__ nf, double *__restrict__ ff, 
             const int cm2 = (int)((c[j] + (unsigned)n - 2) % (unsigned)n);
             op[j] = (cp2 - (int)c[j]) * stride;
             om[j] = (cm2 - (int)c[j]) * stride;
+            if (j == 0 && !wrap0) {
+                op[0] = 2 * stride;
+                om[0] = -2 * stride;
+            }
             stride *= n;
         }
 #pragma unroll
         for (int i = 0; i < DIM; ++i) {
-            const double *v = nf + (int64_t)i * M + p;
+            const double *v = nf + (int64_t)i * cs + p;
             const double c0 = v[0];
             double s = 0.0;
 #pragma unroll
@@ -1057,29 +1063,66 @@ int mm_run_lce(mm_ctx *ctx, double rho, double tol, int64_t max_sweeps, int want
 }
 
 // director from the stored angles into `dst` (d components)
-static int run_director(mm_ctx *ctx, double *dst) {
+static int run_director(mm_ctx *ctx, double *dst, int64_t cs = -1) {
     const int64_t M = ctx->M;
+    if (cs < 0) cs = M;
     const int threads = 256;
     const int blocks = lce_blocks(M, threads);
     if (ctx->dim == 2)
-        k_director<2><<<blocks, threads, 0, ctx->stream>>>(ctx->ang, nullptr, dst, M);
+        k_director<2><<<blocks, threads, 0, ctx->stream>>>(ctx->ang, nullptr, dst, M, cs);
     else
-        k_director<3><<<blocks, threads, 0, ctx->stream>>>(ctx->ang, ctx->chart, dst, M);
+        k_director<3><<<blocks, threads, 0, ctx->stream>>>(ctx->ang, ctx->chart, dst, M, cs);
     MM_LAUNCH_CHECK(ctx);
     return MM_OK;
 }
 
-static int run_frank(mm_ctx *ctx, const double *nf) {
+static int run_frank(mm_ctx *ctx, const double *nf, int64_t cs = -1, int wrap0 = 1) {
     const int64_t M = ctx->M;
+    if (cs < 0) cs = M;
     const int threads = 256;
     const int blocks = lce_blocks(M, threads);
     const double coef = 2.0 * ctx->lce.frank_kappa / (4.0 * ctx->h * ctx->h);
     if (ctx->dim == 2)
-        k_frank<2><<<blocks, threads, 0, ctx->stream>>>(nf, ctx->ff, ctx->n, M, coef);
+        k_frank<2><<<blocks, threads, 0, ctx->stream>>>(nf, ctx->ff, ctx->n, M, coef, cs, wrap0);
     else
-        k_frank<3><<<blocks, threads, 0, ctx->stream>>>(nf, ctx->ff, ctx->n, M, coef);
+        k_frank<3><<<blocks, threads, 0, ctx->stream>>>(nf, ctx->ff, ctx->n, M, coef, cs, wrap0);
     MM_LAUNCH_CHECK(ctx);
     return MM_OK;
+}
+
+// slab: the director buffer keeps two ghost planes on each face (the
+// radius-2 Frank stencil); dirbuf points at plane 0
+int mm_slab_alloc_director(mm_ctx *ctx) {
+    if (ctx->dir_base) return MM_OK;
+    const int64_t nn = (int64_t)ctx->n * ctx->n;
+    int rc = mm_alloc(ctx, (void **)&ctx->dir_base, sizeof(double) * 3 * ctx->dM);
+    if (rc) return rc;
+    MM_CUDA(ctx, cudaMemsetAsync(ctx->dir_base, 0, sizeof(double) * 3 * ctx->dM, ctx->stream));
+    ctx->dirbuf = ctx->dir_base + 2 * nn;
+    return MM_OK;
+}
+
+// LCE frozen data on a slab (lce.py:223-229): DIRECTOR writes the director
+// into the data planes of the ghosted buffer; after the caller's 2-plane
+// ghost exchange FRANK applies the radius-2 stencil
+int mm_run_slab_lce(mm_ctx *ctx, int step) {
+    int rc;
+    if (!ctx->have_lce) return mm_fail(ctx, MM_ERR_CONFIG, "LCE parameters were never set");
+    if (!ctx->ang || !ctx->chart) return mm_fail(ctx, MM_ERR_CONFIG, "LCE angles were never uploaded");
+    if (ctx->slab_nl < 2)
+        return mm_fail(ctx, MM_ERR_CONFIG, "the Frank stencil needs >= 2 planes per rank");
+    if ((rc = mm_slab_alloc_director(ctx))) return rc;
+    if (!ctx->ff) {
+        if ((rc = mm_alloc(ctx, (void **)&ctx->ff, sizeof(double) * 3 * ctx->M))) return rc;
+    }
+    StageScope ss(ctx, MM_STAGE_FROZEN);
+    if (!(ctx->lce.frank_kappa > 0.0)) {  // lce.py:225-228
+        if (step == MM_SLAB_FRANK)
+            MM_CUDA(ctx, cudaMemsetAsync(ctx->ff, 0, sizeof(double) * 3 * ctx->M, ctx->stream));
+        return MM_OK;
+    }
+    if (step == MM_SLAB_DIRECTOR) return run_director(ctx, ctx->dirbuf, ctx->dM);
+    return run_frank(ctx, ctx->dirbuf, ctx->dM, 0);
 }
 
 int mm_run_frozen(mm_ctx *ctx) {

@@ -979,7 +979,7 @@ static int launch_update_local(mm_ctx *ctx, double rho_next, double tol, double 
     // T = F - lam / rho_next for the next projection (single-context grids
     // with packed even-length rows, where row_fwd uses this expression)
     double *Tout = nullptr;
-    if (SWEEP && !ctx->slab_mode && !ctx->points_only && ctx->n % 2 == 0 && ctx->opt_tfield) {
+    if (SWEEP && !ctx->points_only && ctx->n % 2 == 0 && ctx->opt_tfield) {
         if (!ctx->Tbuf && (rc = mm_alloc(ctx, (void **)&ctx->Tbuf, sizeof(double) * D * ctx->M)))
             return rc;
         Tout = ctx->Tbuf;

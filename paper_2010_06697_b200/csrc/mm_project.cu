@@ -365,6 +365,7 @@ struct RowGeom {
     // above the last local plane come from neighbour ranks ([c][i1*n + x]).
     int nl;
     const double *hlo, *hhi;
+    int64_t uM;     // component stride of the real rows written by the inverse pass
     // spectrum layout: 0 = rows ((c*nrows + row)*P + k); 1 = planes
     // ((c*nh + k)*nrows + row), every (c, k) an n x n plane [i0][i1] (k_plane)
     int plane;
@@ -633,7 +634,7 @@ __device__ __forceinline__ void row_inv_tile(double2 *buf, double2 *scr, double 
 #pragma unroll
         for (int c = 0; c < DIM; ++c) {
             const double2 z = buf[m * LD + c * ROWS + r];
-            double *dst = Ut + (int64_t)c * g.M + row * g.n;
+            double *dst = Ut + (int64_t)c * g.uM + row * g.n;
             if (packed) {
                 *reinterpret_cast<double2 *>(dst + 2 * m) = z;
             } else {
@@ -1157,7 +1158,7 @@ __global__ void __launch_bounds__(256)
 k_grad(const double *__restrict__ Ut, const double *__restrict__ Uold, double *__restrict__ G,
        const double *__restrict__ F, double *__restrict__ Lam, int n, int lgn, int64_t M,
        double inv2h, double rho, Mean9 um, Mean9 um_old, double *partials, double *red_out,
-       unsigned int *count) {
+       unsigned int *count, int64_t uM, int wrap0) {
     constexpr int D = DIM * DIM;
     constexpr int K = 2 + D;
     __shared__ double smem[32 * K];
@@ -1167,12 +1168,12 @@ k_grad(const double *__restrict__ Ut, const double *__restrict__ Uold, double *_
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
          p += (int64_t)gridDim.x * blockDim.x) {
         int off_p[DIM], off_m[DIM];
-        nbr_offsets<DIM>(p, n, lgn, off_p, off_m);
+        nbr_offsets<DIM>(p, n, lgn, off_p, off_m, wrap0 != 0);
         // issue every load before any store
         double up[D], dn[D];
 #pragma unroll
         for (int i = 0; i < DIM; ++i) {
-            const double *u = Ut + (int64_t)i * M + p;
+            const double *u = Ut + (int64_t)i * uM + p;
 #pragma unroll
             for (int j = 0; j < DIM; ++j) {
                 up[i * DIM + j] = __ldg(u + off_p[j]);
@@ -1184,7 +1185,7 @@ k_grad(const double *__restrict__ Ut, const double *__restrict__ Uold, double *_
         if (MODE == GRAD_IMPL || MODE == GRAD_RES_IMPL) {
 #pragma unroll
             for (int i = 0; i < DIM; ++i) {
-                const double *u = Uold + (int64_t)i * M + p;
+                const double *u = Uold + (int64_t)i * uM + p;
 #pragma unroll
                 for (int j = 0; j < DIM; ++j)
                     gold[i * DIM + j] = (__ldg(u + off_p[j]) - __ldg(u + off_m[j])) * inv2h +
@@ -1267,7 +1268,7 @@ __device__ __forceinline__ void ring_cell(int r, int x0, int y0, int n, int &off
 __global__ void __launch_bounds__(RT_X * RT_Y, 2)
 k_res_march(const double *__restrict__ Un, const double *__restrict__ Uo,
             const double *__restrict__ F, int n, int64_t M, double inv2h, Mean9 um, Mean9 umo,
-            double *partials, double *red_out, unsigned int *count) {
+            double *partials, double *red_out, unsigned int *count, int64_t uM, int wrap0) {
     __shared__ double sm[2][3][RT_Y + 2][RT_X + 2];
     __shared__ double red_sm[32 * 2];
     // 1D block (block_reduce / grid_finalize index threads by threadIdx.x)
@@ -1281,15 +1282,16 @@ k_res_march(const double *__restrict__ Un, const double *__restrict__ Uo,
     int roff = 0, rsy = 0, rsx = 0;
     if (ringer) ring_cell(threadIdx.x, x0, y0, n, roff, rsy, rsx);
     auto uval = [&](int f, int c, int z, int off) {
-        return __ldg((f ? Uo : Un) + (int64_t)c * M + (int64_t)z * nn + off);
+        return __ldg((f ? Uo : Un) + (int64_t)c * uM + (int64_t)z * nn + off);
     };
     // software pipeline: everything plane z needs is in registers before
     // the iteration for z starts; the loads for z + 1 are issued before the
     // arithmetic of z
     double prv[2][3], cur[2][3], nxt[2][3], ring[2][3], fv[9];
     {
-        const int zm = (z0 == 0) ? n - 1 : z0 - 1;
-        const int zn = (z0 + 1 == n) ? 0 : z0 + 1;
+        // slab (wrap0 = 0): planes -1 and nl are the ghost planes of u
+        const int zm = (z0 == 0 && wrap0) ? n - 1 : z0 - 1;
+        const int zn = (z0 + 1 == n && wrap0) ? 0 : z0 + 1;
 #pragma unroll
         for (int f = 0; f < 2; ++f)
 #pragma unroll
@@ -1314,7 +1316,7 @@ k_res_march(const double *__restrict__ Un, const double *__restrict__ Uo,
         __syncthreads();
         // prefetch plane z + 1 (ring, F) and z + 2 (column)
         const bool more = z + 1 < z0 + RT_ZC;
-        const int z1 = (z + 1) % n, z2 = (z + 2) % n;
+        const int z1 = wrap0 ? (z + 1) % n : z + 1, z2 = wrap0 ? (z + 2) % n : z + 2;
         double nn2[2][3], ring1[2][3], fv1[9];
 #pragma unroll
         for (int f = 0; f < 2; ++f)
@@ -1508,6 +1510,7 @@ int run_rows(mm_ctx *ctx, bool fwd, double rho, double *u_out = nullptr,
     g.nl = ctx->slab_mode ? ctx->slab_nl : ctx->n;
     g.hlo = ctx->slab_mode ? ctx->halo_in_lo : nullptr;
     g.hhi = ctx->slab_mode ? ctx->halo_in_hi : nullptr;
+    g.uM = ctx->uM;
     const double2 *tw = g.packed ? ctx->tw_half : ctx->tw_full;
     int N1, N2;
     factor(g.N, N1, N2);
@@ -1762,16 +1765,18 @@ int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
     k_grad<DIM, MODE><<<blocks, threads, 0, ctx->stream>>>(u_new, ctx->Ut, ctx->G, ctx->F,       \
                                                            ctx->Lam, n, lgn, ctx->M, inv2h, rho, \
                                                            um, umo, ctx->partials, ctx->red_out, \
-                                                           ctx->red_count)
-    const bool march = d == 3 && mode == GRAD_RES_IMPL && !ctx->slab_mode && n % RT_X == 0 &&
-                       n % RT_Y == 0 && n % RT_ZC == 0 && ctx->opt_march;
+                                                           ctx->red_count, ctx->uM,              \
+                                                           ctx->slab_mode ? 0 : 1)
+    const int nplanes = ctx->slab_mode ? ctx->slab_nl : n;
+    const bool march = d == 3 && mode == GRAD_RES_IMPL && n % RT_X == 0 && n % RT_Y == 0 &&
+                       nplanes % RT_ZC == 0 && ctx->opt_march;
     if (march) {
         StageScope ss(ctx, MM_STAGE_GRAD);
-        dim3 grid(n / RT_X, n / RT_Y, n / RT_ZC);
+        dim3 grid(n / RT_X, n / RT_Y, nplanes / RT_ZC);
         if ((rc = mm_ensure_partials(ctx, (int64_t)grid.x * grid.y * grid.z))) return rc;
         k_res_march<<<grid, RT_X * RT_Y, 0, ctx->stream>>>(
             u_new, ctx->Ut, ctx->F, n, ctx->M, inv2h, um, umo, ctx->partials, ctx->red_out,
-            ctx->red_count);
+            ctx->red_count, ctx->uM, ctx->slab_mode ? 0 : 1);
     } else {
         StageScope ss(ctx, MM_STAGE_GRAD);
         if (d == 2) {
@@ -1889,6 +1894,8 @@ GSrc mm_gsrc(mm_ctx *ctx) {
     s.lgn = ctx->points_only ? -1 : ilog2_(ctx->n);
     s.inv2h = ctx->points_only ? 0.0 : 1.0 / (2.0 * ctx->h);
     s.M = ctx->M;
+    s.uM = ctx->uM;
+    s.wrap0 = ctx->slab_mode ? 0 : 1;
     return s;
 }
 
@@ -1906,11 +1913,11 @@ int mm_materialize_G(mm_ctx *ctx) {
         if (ctx->dim == 2)
             k_grad<2, GRAD_WRITE><<<blocks, threads, 0, ctx->stream>>>(
                 ctx->Ut, ctx->Ut, ctx->G, ctx->F, ctx->Lam, ctx->n, lgn, ctx->M, inv2h, 0.0, um,
-                umo, nullptr, nullptr, nullptr);
+                umo, nullptr, nullptr, nullptr, ctx->uM, ctx->slab_mode ? 0 : 1);
         else
             k_grad<3, GRAD_WRITE><<<blocks, threads, 0, ctx->stream>>>(
                 ctx->Ut, ctx->Ut, ctx->G, ctx->F, ctx->Lam, ctx->n, lgn, ctx->M, inv2h, 0.0, um,
-                umo, nullptr, nullptr, nullptr);
+                umo, nullptr, nullptr, nullptr, ctx->uM, ctx->slab_mode ? 0 : 1);
     }
     MM_LAUNCH_CHECK(ctx);
     ctx->g_buf_valid = true;
@@ -1928,11 +1935,11 @@ int mm_run_stencil(mm_ctx *ctx, int op) {
         if (ctx->dim == 2)
             k_grad<2, GRAD_WRITE><<<blocks, threads, 0, ctx->stream>>>(
                 ctx->Ut, ctx->Ut, ctx->G, ctx->F, ctx->Lam, ctx->n, ilog2_(ctx->n), ctx->M, inv2h,
-                0.0, um, um, nullptr, nullptr, nullptr);
+                0.0, um, um, nullptr, nullptr, nullptr, ctx->uM, 1);
         else
             k_grad<3, GRAD_WRITE><<<blocks, threads, 0, ctx->stream>>>(
                 ctx->Ut, ctx->Ut, ctx->G, ctx->F, ctx->Lam, ctx->n, ilog2_(ctx->n), ctx->M, inv2h,
-                0.0, um, um, nullptr, nullptr, nullptr);
+                0.0, um, um, nullptr, nullptr, nullptr, ctx->uM, 1);
         ctx->g_implicit = false;
         ctx->g_buf_valid = true;
     } else {
@@ -2070,73 +2077,6 @@ k_col_slab(ColGeom g, SlabCol sc, const double2 *__restrict__ tw) {
     }
 }
 
-// gradient + multiplier ascent on a slab; axis-0 neighbours across the slab
-// faces come from the u halo planes.  Writes G and lam (explicit grad_u).
-// slots: 0 sum dG^2, 1 sum misfit^2, 2.. sum lam
-__global__ void __launch_bounds__(256)
-k_grad_slab(const double *__restrict__ Ut, const double *__restrict__ hlo,
-            const double *__restrict__ hhi, double *__restrict__ G, const double *__restrict__ F,
-            double *__restrict__ Lam, int n, int nl, int64_t M, double inv2h, double rho, Mean9 um,
-            int update, double *partials, double *red_out, unsigned int *count) {
-    constexpr int K = 11;
-    __shared__ double smem[32 * K];
-    double acc[K];
-#pragma unroll
-    for (int q = 0; q < K; ++q) acc[q] = 0.0;
-    const int64_t nn = (int64_t)n * n;
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        const int i0 = (int)(p / nn);
-        const int64_t q = p - i0 * nn;
-        const int i1 = (int)(q / n), i2 = (int)(q - (int64_t)i1 * n);
-        const int op1 = (i1 + 1 == n) ? -(n - 1) * n : n, om1 = (i1 == 0) ? (n - 1) * n : -n;
-        const int op2 = (i2 + 1 == n) ? -(n - 1) : 1, om2 = (i2 == 0) ? (n - 1) : -1;
-        double up[9], dn[9];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            const double *u = Ut + (int64_t)i * M + p;
-            up[i * 3 + 0] = (i0 + 1 == nl) ? hhi[i * nn + q] : u[nn];
-            dn[i * 3 + 0] = (i0 == 0) ? hlo[i * nn + q] : u[-nn];
-            up[i * 3 + 1] = u[op1];
-            dn[i * 3 + 1] = u[om1];
-            up[i * 3 + 2] = u[op2];
-            dn[i * 3 + 2] = u[om2];
-        }
-        double gold[9], fv[9], lv[9];
-        if (update) {
-#pragma unroll
-            for (int c = 0; c < 9; ++c) {
-                const int64_t o = (int64_t)c * M + p;
-                gold[c] = G[o];
-                fv[c] = F[o];
-                lv[c] = Lam[o];
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < 9; ++c) {
-            const double gnew = (up[c] - dn[c]) * inv2h + um.v[c];
-            const int64_t o = (int64_t)c * M + p;
-            if (update) {
-                const double dg = gnew - gold[c];
-                const double mis = gnew - fv[c];
-                const double lnew = lv[c] + rho * mis;
-                Lam[o] = lnew;
-                acc[0] += dg * dg;
-                acc[1] += mis * mis;
-                acc[2 + c] += lnew;
-            }
-            G[o] = gnew;
-        }
-    }
-    if (update) {
-        int ops[K];
-#pragma unroll
-        for (int q = 0; q < K; ++q) ops[q] = RED_SUM;
-        block_reduce<K>(acc, ops, smem);
-        grid_finalize<K>(acc, ops, partials, red_out, count, smem);
-    }
-}
-
 template <int MODE>
 int run_col_slab(mm_ctx *ctx, const ColGeom &g, const SlabCol &sc, int n_outer) {
     int N1, N2;
@@ -2164,6 +2104,63 @@ int run_col_slab(mm_ctx *ctx, const ColGeom &g, const SlabCol &sc, int n_outer) 
 
 }  // namespace
 
+// K1 of the fused schedule on a slab (mm_run_project's residual pass): the
+// u_new buffer (Ut2) was written by MM_SLAB_INV and its ghost planes filled
+// by the halo exchange; u_old (Ut) keeps the ghosts of the previous
+// exchange.  Then u_new becomes current, grad_u = ubar + D u (implicit) and
+// the ascent is left pending for the fused update + local pass.
+int mm_slab_res(mm_ctx *ctx, double rho, const double *u_mean, double *sums) {
+    int rc;
+    const int n = ctx->n;
+    Mean9 um, umo;
+    for (int i = 0; i < 9; ++i) {
+        um.v[i] = u_mean[i];
+        umo.v[i] = ctx->ubar[i];
+    }
+    const double inv2h = 1.0 / (2.0 * ctx->h);
+    const int lgn = ilog2_(n);
+    const int mode = ctx->g_implicit && !ctx->g_buf_valid ? GRAD_RES_IMPL : GRAD_RES_EXPL;
+    double *u_new = ctx->Ut2;
+    const int nl = ctx->slab_nl;
+    const bool march = mode == GRAD_RES_IMPL && n % RT_X == 0 && n % RT_Y == 0 &&
+                       nl % RT_ZC == 0 && ctx->opt_march;
+    {
+        StageScope ss(ctx, MM_STAGE_GRAD);
+        if (march) {
+            dim3 grid(n / RT_X, n / RT_Y, nl / RT_ZC);
+            if ((rc = mm_ensure_partials(ctx, (int64_t)grid.x * grid.y * grid.z))) return rc;
+            k_res_march<<<grid, RT_X * RT_Y, 0, ctx->stream>>>(
+                u_new, ctx->Ut, ctx->F, n, ctx->M, inv2h, um, umo, ctx->partials, ctx->red_out,
+                ctx->red_count, ctx->uM, 0);
+        } else {
+            const int threads = 256;
+            const int blocks = (int)std::min<int64_t>((ctx->M + threads - 1) / threads, 148 * 8);
+            if ((rc = mm_ensure_partials(ctx, blocks))) return rc;
+            if (mode == GRAD_RES_IMPL)
+                k_grad<3, GRAD_RES_IMPL><<<blocks, threads, 0, ctx->stream>>>(
+                    u_new, ctx->Ut, ctx->G, ctx->F, ctx->Lam, n, lgn, ctx->M, inv2h, rho, um, umo,
+                    ctx->partials, ctx->red_out, ctx->red_count, ctx->uM, 0);
+            else
+                k_grad<3, GRAD_RES_EXPL><<<blocks, threads, 0, ctx->stream>>>(
+                    u_new, ctx->Ut, ctx->G, ctx->F, ctx->Lam, n, lgn, ctx->M, inv2h, rho, um, umo,
+                    ctx->partials, ctx->red_out, ctx->red_count, ctx->uM, 0);
+        }
+    }
+    MM_LAUNCH_CHECK(ctx);
+    for (int i = 0; i < 9; ++i) ctx->ubar[i] = um.v[i];
+    std::swap(ctx->Ut, ctx->Ut2);
+    ctx->g_implicit = true;
+    ctx->g_buf_valid = false;
+    ctx->lam_pending = true;
+    ctx->pending_rho = rho;
+    double r[MM_MAX_PARTIALS];
+    const int K = march ? 2 : 2 + ctx->D;
+    if ((rc = mm_fetch_reduction(ctx, K, r))) return rc;
+    sums[0] = r[0];
+    sums[1] = r[1];
+    return MM_OK;
+}
+
 int mm_run_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, double *sums) {
     int rc = ensure_constants(ctx);
     if (rc) return rc;
@@ -2184,25 +2181,27 @@ int mm_run_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, do
     const int64_t spec_cs = (int64_t)nl * n * Pp, spec_os = (int64_t)n * Pp;
     const int64_t blk = 3LL * nl * nl * Pp;  // one destination block
     switch (step) {
-        case MM_SLAB_HALO_T:
-        case MM_SLAB_HALO_U: {
+        case MM_SLAB_HALO_T: {
+            // T_c0 = (F - lam / rho)_{i0} of the first / last local plane: from
+            // the T field the fused pass left when it is current for rho
             StageScope ss(ctx, MM_STAGE_OTHER);
-            const bool T = step == MM_SLAB_HALO_T;
+            const bool tf = ctx->T_valid && ctx->T_rho == rho && ctx->Tbuf;
             const int blocks = (int)std::min<int64_t>((3 * nn + threads - 1) / threads, 148 * 8);
             k_slab_halo<<<blocks, threads, 0, ctx->stream>>>(
-                T ? ctx->F : ctx->Ut, T ? ctx->Lam : nullptr, 1.0 / rho, T ? 3 : 1, 3, n, nl, M,
+                tf ? ctx->Tbuf : ctx->F, tf ? nullptr : ctx->Lam, 1.0 / rho, 3, 3, n, nl, M,
                 ctx->halo_out_lo, ctx->halo_out_hi);
             MM_LAUNCH_CHECK(ctx);
-            return mm_synchronize(ctx);
+            return MM_OK;
         }
         case MM_SLAB_FWD:
         case MM_SLAB_FWD_PUSH: {
             const bool push = step == MM_SLAB_FWD_PUSH;
             if (push && !ctx->peer_recv)
                 return mm_fail(ctx, MM_ERR_CONFIG, "FWD_PUSH: peer RECV buffers were never set");
+            const bool tf = ctx->T_valid && ctx->T_rho == rho && ctx->Tbuf;
             {
                 StageScope ss(ctx, MM_STAGE_ROW_FWD);
-                if ((rc = run_rows(ctx, true, rho))) return rc;
+                if ((rc = run_rows(ctx, true, rho, nullptr, tf ? ctx->Tbuf : nullptr))) return rc;
             }
             SlabCol sc;
             sc.peers = push ? ctx->peer_recv : nullptr;
@@ -2215,8 +2214,7 @@ int mm_run_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, do
             sc.d_sq = blk; sc.d_es = Pp; sc.d_os = (int64_t)nl * Pp; sc.d_cs = (int64_t)nl * nl * Pp;
             sc.outer_off = 0;
             StageScope ss(ctx, MM_STAGE_COL_FWD);
-            if ((rc = run_col_slab<COL_FWD>(ctx, g, sc, nl))) return rc;
-            return mm_synchronize(ctx);
+            return run_col_slab<COL_FWD>(ctx, g, sc, nl);
         }
         case MM_SLAB_SOLVE:
         case MM_SLAB_SOLVE_PUSH: {
@@ -2236,10 +2234,11 @@ int mm_run_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, do
             sc.s_cs = sc.d_cs = (int64_t)nl * nl * Pp;
             sc.outer_off = ctx->slab_rank * nl;
             StageScope ss(ctx, MM_STAGE_COL_SOLVE);
-            if ((rc = run_col_slab<COL_SOLVE>(ctx, g, sc, nl))) return rc;
-            return mm_synchronize(ctx);
+            return run_col_slab<COL_SOLVE>(ctx, g, sc, nl);
         }
         case MM_SLAB_INV: {
+            // inverse axis-1 FFT from the returned send buffer, C2R rows into
+            // the u_new buffer (data planes; its ghosts come from the exchange)
             SlabCol sc;
             sc.peers = nullptr;
             sc.peer_off = 0;
@@ -2255,34 +2254,12 @@ int mm_run_slab_step(mm_ctx *ctx, int step, double rho, const double *u_mean, do
                 if ((rc = run_col_slab<COL_INV>(ctx, g, sc, nl))) return rc;
             }
             StageScope ss(ctx, MM_STAGE_ROW_INV);
-            if ((rc = run_rows(ctx, false, rho, ctx->Ut))) return rc;
-            return mm_synchronize(ctx);
+            return run_rows(ctx, false, rho, ctx->Ut2);
         }
-        case MM_SLAB_UPDATE:
-        case MM_SLAB_GRAD: {
-            Mean9 um;
-            for (int i = 0; i < 9; ++i) um.v[i] = u_mean[i];
-            const int blocks = (int)std::min<int64_t>((M + threads - 1) / threads, 148 * 8);
-            if ((rc = mm_ensure_partials(ctx, blocks))) return rc;
-            const int upd = step == MM_SLAB_UPDATE;
-            {
-                StageScope ss(ctx, MM_STAGE_GRAD);
-                k_grad_slab<<<blocks, threads, 0, ctx->stream>>>(
-                    ctx->Ut, ctx->halo_in_lo, ctx->halo_in_hi, ctx->G, ctx->F, ctx->Lam, n, nl, M,
-                    1.0 / (2.0 * ctx->h), rho, um, upd, ctx->partials, ctx->red_out,
-                    ctx->red_count);
-            }
-            MM_LAUNCH_CHECK(ctx);
-            ctx->g_implicit = false;
-            ctx->g_buf_valid = true;
-            for (int i = 0; i < 9; ++i) ctx->ubar[i] = um.v[i];
-            if (!upd) return mm_synchronize(ctx);
-            double r[MM_MAX_PARTIALS];
-            if ((rc = mm_fetch_reduction(ctx, 11, r))) return rc;
-            for (int i = 0; i < 11; ++i) sums[i] = r[i];
-            return MM_OK;
-        }
+        case MM_SLAB_RES: return mm_slab_res(ctx, rho, u_mean, sums);
         default: return mm_fail(ctx, MM_ERR_PARAM, "unknown slab step %d", step);
     }
     (void)P;
+    (void)u_mean;
+    (void)sums;
 }

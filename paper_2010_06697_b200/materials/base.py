@@ -168,6 +168,24 @@ class MaterialModel:
             cache[key] = hit
         return hit[1]
 
+    def _globalize(self, comm):
+        """Slab ranks hold part of the per-point parameters: pin the cached
+        energy scales to their global values and check that every rank
+        uses the same mu_rep (the default max(mu) of a rank's own part would
+        differ between ranks)."""
+        reps = comm.gather_objects(float(self.mu_rep))
+        if any(r != reps[0] for r in reps):
+            from ..errors import ConfigurationError
+            raise ConfigurationError(f"mu_rep differs between ranks {reps}: pass the global value")
+        for key, fn in self._scale_terms().items():
+            loc = [float(np.max(a)) if np.size(a) else -np.inf for a in fn()]
+            glob = comm.ordered_sum(loc, ops=[1] * len(loc))
+            self._override_max(key, float(np.sum(glob)))
+
+    def _scale_terms(self):
+        """Cached maxima: key -> arrays whose maxima sum to the scale."""
+        return {}
+
     def _override_max(self, key, value):
         """Pin a cached maximum (slab ranks hold part of the moduli: the
         energy scale is the global one, reduced across ranks)."""

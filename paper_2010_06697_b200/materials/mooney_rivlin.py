@@ -85,6 +85,9 @@ class MooneyRivlin(MaterialModel):
         more than the device local step)."""
         return self._cached_max("phi", lambda: np.max(self.mu) + np.max(self.kappa))
 
+    def _scale_terms(self):
+        return {"phi": lambda: (self.mu, self.kappa)}
+
     def _fused_material(self):
         """Material id and energy scale for the fused ascent + first chunk."""
         return _lib.MAT_MR, self._phi_scale()

@@ -47,6 +47,9 @@ class QuadraticMaterial(MaterialModel):
     def _cmax(self):
         return self._cached_max("cmax", lambda: np.max(self.c))
 
+    def _scale_terms(self):
+        return {"cmax": lambda: (self.c,)}
+
     def _fused_material(self):
         return _lib.MAT_QUADRATIC, self._cmax()
 

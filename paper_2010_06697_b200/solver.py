@@ -112,6 +112,8 @@ class ADMMState:
         object.__setattr__(self, "_stale", set())   # host copy out of date
         object.__setattr__(self, "_dirty", set())   # host copy must be uploaded
         object.__setattr__(self, "_engine", None)
+        # communicator of a slab-decomposed state (slab.py); None: one GPU
+        object.__setattr__(self, "_comm", None)
         # caller arrays updated in place at the end of solve() (F, lam)
         object.__setattr__(self, "_inplace", {})
         self.u_mean = np.asarray(u_mean, dtype=float)
@@ -135,7 +137,7 @@ class ADMMState:
             grid = eng.grid
             if name in STATE_FIELDS:
                 fid, rank = STATE_FIELDS[name]
-                val = eng.ctx.download(fid, field_shape(grid, rank))
+                val = eng.ctx.download(fid, eng.field_shape(rank))
                 val.flags.writeable = False
             else:
                 val = eng.model._download_internal(eng.ctx, name)
@@ -170,6 +172,8 @@ class ADMMState:
         """Fields the caller holds on the host (other than the in-place F and
         lam) are re-read after the solve as fresh arrays: prepare those host
         arrays while the device iterates (_lib.prefault_async)."""
+        if self._comm is not None:
+            return  # slab fields: local shapes, not worth it
         shapes = []
         for nm in ("grad_u", "u_tilde"):
             if self._host.get(nm) is not None:
@@ -193,7 +197,7 @@ class ADMMState:
             if target is None or nm not in self._stale:
                 continue
             fid, rank = STATE_FIELDS[nm]
-            if target.shape != field_shape(eng.grid, rank):
+            if target.shape != eng.field_shape(rank):
                 continue
             eng.ctx.download_into(fid, target)
             target.flags.writeable = False
@@ -233,12 +237,12 @@ class ADMMState:
     # -- device attachment -------------------------------------------------------
     def _attach(self, grid: Grid, model) -> Engine:
         eng = self._engine
-        if eng is None or not eng.matches(grid):
+        if eng is None or not eng.matches(grid, self._comm):
             if eng is not None:
                 # leaving an old engine: bring everything home first
                 for nm in list(self._stale):
                     self._get(nm)
-            eng = Engine(grid)
+            eng = Engine(grid, comm=self._comm)
             object.__setattr__(self, "_engine", eng)
             self._dev.clear()
             self._stale.clear()
@@ -253,7 +257,7 @@ class ADMMState:
             if val is None:
                 continue
             if nm in self._dirty or nm not in self._dev:
-                grid.check_field(val, rank, nm)
+                eng.check_field(val, rank, nm)
                 ctx.upload(fid, val)
                 if nm == "lam":
                     eng.lam_sum = None
@@ -361,21 +365,43 @@ def _needs_points(policy) -> bool:
 # state setup and the outer iteration
 # ---------------------------------------------------------------------------
 
-def init_state(grid: Grid, model, bc: MacroBC, params: SolverParams, rng=None) -> ADMMState:
-    """Uniform state at the pinned macroscopic strain (solver.py:206-227)."""
+def init_state(grid: Grid, model, bc: MacroBC, params: SolverParams, rng=None,
+               comm=None) -> ADMMState:
+    """Uniform state at the pinned macroscopic strain (solver.py:206-227).
+    With a communicator (slab decomposition, slab.py) the fields are this
+    rank's slab (n/P, n, n, ...) and the model holds this rank's per-point
+    parameters."""
     d = grid.dim
     if bc.strain_mask.shape != (d, d):
         raise ParameterError("boundary control dimension mismatch")
+    comm = _as_comm(comm, grid)
+    shape = grid.shape
+    npts = grid.npoints
+    if comm is not None:
+        from .slab import SlabLayout
+        lay = SlabLayout(grid.n, comm.P, comm.rank, grid.length, grid.dim)
+        shape, npts = lay.local_shape, lay.npts_local
     Fbar0 = np.where(bc.strain_mask, bc.value, np.eye(d))
-    F = np.empty(grid.shape + (d, d))
+    F = np.empty(shape + (d, d))
     F[...] = Fbar0
     state = ADMMState(
-        u_mean=Fbar0.copy(), u_tilde=np.zeros(grid.shape + (d,)), grad_u=F.copy(), F=F,
-        lam=np.zeros(grid.shape + (d, d)), internal=model.init_internal(grid.npoints, rng),
+        u_mean=Fbar0.copy(), u_tilde=np.zeros(shape + (d,)), grad_u=F.copy(), F=F,
+        lam=np.zeros(shape + (d, d)), internal=model.init_internal(npts, rng),
         rho=float(params.rho_init if params.rho_init is not None else model.mu_rep))
+    object.__setattr__(state, "_comm", comm)
     if state.rho <= 0:
         raise ParameterError("initial penalty must be positive")
     return state
+
+
+def _as_comm(comm, grid):
+    if comm is None:
+        return None
+    from .slab import as_comm
+    comm = as_comm(comm)
+    if grid.dim != 3:
+        raise ConfigurationError("the slab decomposition is implemented for 3D grids")
+    return comm
 
 
 def begin_time_step(state: ADMMState):
@@ -406,6 +432,9 @@ def outer_iteration(grid: Grid, model, state: ADMMState, params: SolverParams, b
         from .errors import ConfigurationError
         raise ConfigurationError(f"MacroBC dim {bc.dim} does not match grid dim {grid.dim}")
     eng = state._attach(grid, model)
+    if eng.distributed and _needs_points(policy):
+        raise ConfigurationError("slab decomposition: custom policies see only this rank's "
+                                 "points; use a built-in policy")
     ctx = eng.ctx
     d = grid.dim
     npts = grid.npoints
@@ -470,13 +499,24 @@ def outer_iteration(grid: Grid, model, state: ADMMState, params: SolverParams, b
 
 def solve(grid: Grid, model, bc: MacroBC, params: SolverParams,
           policy: LocalPolicy | None = None, state: ADMMState | None = None, dt: float = 0.0,
-          rng=None, callback=None, raise_on_max: bool = True):
+          rng=None, callback=None, raise_on_max: bool = True, comm=None):
     """Iterate to joint primal/dual/local tolerance; returns (state, converged)
-    (solver.py:305-339)."""
+    (solver.py:305-339).
+
+    ``comm`` (extension): a communicator (slab.TorchComm /
+    ThreadComm, or torch.distributed) -- the grid is split along axis 0 over
+    its ranks, one GPU each; `state` and the model's per-point parameters
+    are this rank's slab (init_state(..., comm=comm)), and every rank takes
+    identical decisions from rank-ordered global sums."""
     if policy is None:
         policy = ExactAll()
+    comm = _as_comm(comm, grid)
     if state is None:
-        state = init_state(grid, model, bc, params, rng)
+        state = init_state(grid, model, bc, params, rng, comm=comm)
+    elif comm is not None and state._comm is not comm:
+        if state._engine is not None:
+            raise ConfigurationError("state is attached to another communicator")
+        object.__setattr__(state, "_comm", comm)
     r_l_tol = params.r_l_tol if params.r_l_tol is not None else max(params.r_p_tol,
                                                                    params.r_d_tol)
     converged = False
@@ -540,7 +580,7 @@ def _solve_fused(grid, model, bc, params, policy, state, r_l_tol):
     resid = None
     # the decisions between the residuals and the next fused pass taken in
     # the library (MM_HOST_DECIDE=1: here, through two calls)
-    device_step = os.environ.get("MM_HOST_DECIDE", "0") != "1"
+    device_step = os.environ.get("MM_HOST_DECIDE", "0") != "1" and not eng.distributed
     if device_step:
         prm = _lib.StepParamsC()
         prm.npts = float(npts)
