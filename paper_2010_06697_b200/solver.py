@@ -719,7 +719,12 @@ def macro_stress(grid: Grid, state: ADMMState) -> np.ndarray:
     """Volume average of the multiplier (solver.py:374-377); from the device
     reduction when the state is resident."""
     eng = state._engine
-    if eng is not None and eng.matches(grid) and "lam" in state._dev \
+    if eng is not None and eng.matches(grid, state._comm) and "lam" in state._dev \
             and "lam" not in state._dirty:
         return eng.lam_mean().copy()
+    if state._comm is not None:
+        # this rank holds a slab: rank-ordered global sum of the local sums
+        d = grid.dim
+        loc = np.asarray(state.lam, dtype=float).reshape(-1, d * d).sum(axis=0)
+        return (state._comm.ordered_sum(loc) / grid.npoints).reshape(d, d)
     return mean_field(grid, state.lam)
