@@ -9,14 +9,15 @@ outer iteration of solver.solve (local step, projection, multiplier ascent,
 residuals, penalty update); the exit tolerances are set to 1e-300 so that
 exactly W warm-up iterations (from init_state), then K timed ones, run.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--n 256] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--grid 256] [--workload mr|lce]
+                  [--impl ours|reference]
 
 Under torchrun (N > 1) the same n^3 grid is split into N slabs along axis
 0, one per GPU (solve(..., comm=TorchComm)): the total work is
 fixed, so every line says "scaling": "strong"; the timed region is
 bracketed by a barrier + synchronize and the max over ranks is reported.
-``--n 512`` is SURVEY config 4 (512^3 over 1/2/4/8 GPUs); ``--workload lce``
-is config 3 (add ``--n 512`` / ``--n 1024`` under torchrun for config 5).
+``--grid 512`` is SURVEY config 4 (512^3 over 1/2/4/8 GPUs); ``--workload lce``
+is config 3 (add ``--grid 512`` / ``--grid 1024`` under torchrun for config 5).
 ``--impl reference`` times the CPU restatement of the reference (oracle/,
 the "port") on the host cores over the same window.
 """
@@ -392,7 +393,7 @@ def run_ours(args, rank, world, dist):
                    "bc": "strain diag(0.95,1,1)", "policy": "RatioToDual(0.3)",
                    "steps_are": f"outer iterations {args.warmup + 1}..{args.warmup + args.steps}"
                                 f" from init_state",
-                   "l2": f"inputs larger than L2 (state {32 * 8 * M / world / 1e9:.1f} GB per GPU)",
+                   "l2": f"inputs larger than L2 (state {32 * 8 * M / world / 1e9:.2f} GB per GPU)",
                    "parallelism": par},
         "local_sweeps_total": int(sweeps),
         "residuals_last": {"r_p": hist[-1].r_p, "r_d": hist[-1].r_d, "r_l": hist[-1].r_l,
@@ -614,7 +615,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--grid", dest="n", type=int, default=256,
+                    help="n of the n^3 grid (not --n: torchrun would claim it)")
     ap.add_argument("--workload", default="mr", choices=["mr", "lce"],
                     help="mr: SURVEY 8(d) config 2 inputs (headline); lce: config 3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -21,7 +21,7 @@ def _run(args, timeout=600):
 
 
 def test_reference_arm_line():
-    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "1", "--n", "16"])
+    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "1", "--grid", "16"])
     assert d["impl"] == "reference"
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
               "higher_is_better", "scaling", "dtype", "config", "cpu_baseline", "e2e"):
@@ -33,7 +33,7 @@ def test_reference_arm_line():
 
 @pytest.mark.gpu
 def test_our_line_small_grid():
-    d = _run(["--n", "32", "--steps", "3", "--warmup", "3"])
+    d = _run(["--grid", "32", "--steps", "3", "--warmup", "3"])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
               "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
               "roofline", "e2e", "gpu_launches", "clocks"):

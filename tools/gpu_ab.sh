@@ -1,7 +1,7 @@
 # A/B of build variants at the default bench (K = 50): each argument is a set of
 # nvcc flags applied to SRC (default mm_local.cu); REPS rounds (default 2);
 # TESTS=1 also runs the GPU suite once on the last variant; BENCH_ARGS are
-# passed to bench.py (e.g. "--n 512 --steps 10 --warmup 3").
+# passed to bench.py (e.g. "--grid 512 --steps 10 --warmup 3").
 # e.g.  SRC=mm_project.cu bash tools/gpu_ab.sh "-DMM_PLANE_PPT=8" "-DMM_PLANE_PPT=16"
 cd /root/repo
 summ() {

@@ -7,5 +7,5 @@ python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ev_plain.log
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ev_launches.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ev_launch.log 2>&1
 bash tools/gpu_ncu_full.sh  # one full capture per stage kernel, steady state
-timeout 900 python bench.py --n 512 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/ev_bench512.json 2> gpurun_out/ev_bench512.err
+timeout 900 python bench.py --grid 512 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/ev_bench512.json 2> gpurun_out/ev_bench512.err
 echo done
