@@ -2069,6 +2069,9 @@ k_col_slab(ColGeom g, SlabCol sc, const double2 *__restrict__ tw) {
             if (k0 + c < g.ncol)
                 sc.peers[n / sc.blk_d][loc + (n % sc.blk_d) * sc.d_es + c] = buf[n * LD + c];
         }
+        // the peer stores are complete and visible system-wide before this
+        // CTA retires, hence before the barrier that follows the kernel
+        __threadfence_system();
         return;
     }
     for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
