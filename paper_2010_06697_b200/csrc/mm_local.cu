@@ -37,6 +37,9 @@ constexpr int LOCAL_THREADS = MM_LOCAL_THREADS;
 #ifndef LOCAL_MIN_BLOCKS
 #define LOCAL_MIN_BLOCKS 4
 #endif
+#ifndef MM_PREFETCH  // L2 prefetch of the next grid-stride point (prefetch_point)
+#define MM_PREFETCH 1
+#endif
 
 // ---------------------------------------------------------------------------
 // log(J) of the Mooney-Rivlin objective, table-driven.  x = 2^k z with z in
@@ -519,6 +522,8 @@ k_descent(double *__restrict__ F, const GSrc gs, const double *__restrict__ Lam,
         double X[D], B[D];
         double cG = 0.0;
         gsrc_load<(D == 4 ? 2 : 3)>(gs, p, B);  // B holds grad_u until the next line
+        if (MM_PREFETCH) prefetch_point<(D == 4 ? 2 : 3)>(gs, F, Lam, modA, modB,
+                                                          p + (int64_t)gridDim.x * blockDim.x);
 #pragma unroll
         for (int i = 0; i < D; ++i) {
             X[i] = F[i * M + p];
@@ -613,6 +618,8 @@ k_update_local(double *__restrict__ F, double *__restrict__ Lam, double *__restr
          p += (int64_t)gridDim.x * blockDim.x) {
         double G[D], X[D], L[D];
         gsrc_load<(D == 4 ? 2 : 3)>(gs, p, G);
+        if (MM_PREFETCH && SWEEP) prefetch_point<(D == 4 ? 2 : 3)>(gs, F, Lam, modA, modB,
+                                                                   p + (int64_t)gridDim.x * blockDim.x);
 #pragma unroll
         for (int i = 0; i < D; ++i) {
             X[i] = F[i * M + p];
