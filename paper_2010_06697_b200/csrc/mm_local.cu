@@ -37,6 +37,9 @@ constexpr int LOCAL_THREADS = MM_LOCAL_THREADS;
 #ifndef LOCAL_MIN_BLOCKS
 #define LOCAL_MIN_BLOCKS 4
 #endif
+#ifndef MM_B_SMEM  // fused pass: B and lam_{k+1} in shared memory instead of registers
+#define MM_B_SMEM 1
+#endif
 #ifndef MM_PREFETCH  // L2 prefetch of the next grid-stride point (prefetch_point):
 #define MM_PREFETCH 0  // measured 2.05 -> 2.13 ms in the fused pass at 256^3, off
 #endif
@@ -296,14 +299,26 @@ __device__ __forceinline__ void cof_t(const double (&X)[D], double (&C)[D]) {
     }
 }
 
+// Per-thread column in shared memory ([i][thread], conflict-free): the fused
+// pass keeps B = lam + rho G (read-only across the sweeps) there instead of
+// in 18 registers, so more warps fit an SM (MM_B_SMEM).
+struct SmemCol {
+    const double *p;
+    // volatile: a plain load is loop-invariant in the sweep loop and the
+    // compiler would hoist all nine back into registers
+    __device__ __forceinline__ double operator[](int i) const {
+        return *(const volatile double *)(p + i * LOCAL_THREADS);
+    }
+};
+
 // The per-point coupling  -lam:X + rho/2 |G - X|^2  is carried as
 //   rho/2 |X|^2 - B:X + cG,   B = lam + rho G,  cG = rho/2 |G|^2,
 // (identical up to roundoff) so only 9 + 1 doubles of (G, lam) stay live in
 // registers across the sweep loop instead of 18.
 
 // objective (mooney_rivlin.py:132-141 / quadratic.py:52-55); +inf if det <= 0
-template <int MAT, int D>
-__device__ __forceinline__ double objective(const double (&X)[D], const double (&B)[D],
+template <int MAT, int D, typename BT>
+__device__ __forceinline__ double objective(const double (&X)[D], const BT &B,
                                             double cG, double m, double k, double rho,
                                             const double *__restrict__ LT) {
     double bx = 0.0, I1 = 0.0;
@@ -321,8 +336,8 @@ __device__ __forceinline__ double objective(const double (&X)[D], const double (
 }
 
 // objective given det X (>0) already computed by the admissibility test
-template <int MAT, int D>
-__device__ __forceinline__ double objective_J(const double (&X)[D], double J, const double (&B)[D],
+template <int MAT, int D, typename BT>
+__device__ __forceinline__ double objective_J(const double (&X)[D], double J, const BT &B,
                                               double cG, double m, double k, double rho,
                                               const double *__restrict__ LT) {
     double bx = 0.0, I1 = 0.0;
@@ -339,8 +354,8 @@ __device__ __forceinline__ double objective_J(const double (&X)[D], double J, co
 
 // gradient S(X) - lam - rho (G - X) = S(X) + rho X - B
 // (mooney_rivlin.py:143-151 / quadratic.py:57-58)
-template <int MAT, int D>
-__device__ __forceinline__ void gradient(const double (&X)[D], const double (&B)[D], double m,
+template <int MAT, int D, typename BT>
+__device__ __forceinline__ void gradient(const double (&X)[D], const BT &B, double m,
                                          double k, double rho, double (&g)[D]) {
     if constexpr (MAT == MAT_QUAD) {
 #pragma unroll
@@ -359,8 +374,8 @@ __device__ __forceinline__ void gradient(const double (&X)[D], const double (&B)
 }
 
 // gradient at X with det X = J already known (the accepted trial's det)
-template <int MAT, int D>
-__device__ __forceinline__ void gradient_J(const double (&X)[D], double J, const double (&B)[D],
+template <int MAT, int D, typename BT>
+__device__ __forceinline__ void gradient_J(const double (&X)[D], double J, const BT &B,
                                            double m, double k, double rho, double (&g)[D]) {
     if constexpr (MAT == MAT_QUAD) {
 #pragma unroll
@@ -387,8 +402,8 @@ __device__ __forceinline__ bool admissible(const double (&X)[D]) {
 // tol_gs = gs_threshold(tol): the activity test res > tol is evaluated as
 // |g|^2 > tol_gs (exactly equivalent); res = sqrt(|g|^2) is formed only for
 // the free-mode trend test and on return.
-template <int MAT, int D>
-__device__ __forceinline__ void descent_point(double (&X)[D], const double (&B)[D], double cG,
+template <int MAT, int D, typename BT>
+__device__ __forceinline__ void descent_point(double (&X)[D], const BT &B, double cG,
                                               double m, double k, double rho, double tol_gs,
                                               double phi_scale, int s0, int s1, double tmax,
                                               double &t, bool &freem, int &nsw, double &res,
@@ -608,7 +623,13 @@ k_update_local(double *__restrict__ F, double *__restrict__ Lam, double *__restr
                double *__restrict__ res_out, int32_t *__restrict__ nsw_out, double *partials,
                double *red_out, unsigned int *count) {
     constexpr int K = 5 + 2 * D;  // ..., last slot: sum of per-point sweeps
-    __shared__ double smem[32 * K];
+    // MM_B_SMEM: B = lam + rho G and lam_{k+1} (for the T store) live in
+    // per-thread shared-memory columns across the sweeps; the block
+    // reduction's scratch reuses that space after the loop
+    constexpr bool BSM = MM_B_SMEM && SWEEP && ALGO == 0;
+    __shared__ double sBL[BSM ? 2 * D * LOCAL_THREADS : 32 * K];
+    double *smem = sBL;
+    static_assert(!BSM || 2 * D * LOCAL_THREADS >= 32 * K, "reduction scratch fits");
     __shared__ double sacc[K * LOCAL_THREADS];
     __shared__ double ltab[(SWEEP && ALGO == 0) ? 3 * LOGTAB_N : 1];
     if constexpr (SWEEP && ALGO == 0) load_logtab(ltab);
@@ -647,6 +668,21 @@ k_update_local(double *__restrict__ F, double *__restrict__ Lam, double *__restr
                 nsw = (int)nsw64;
                 moved = nsw > 0;
                 X[0] = a; X[1] = b; X[2] = c; X[3] = d;
+            } else if constexpr (BSM) {
+                double *Bs = sBL + threadIdx.x, *Ls = sBL + D * LOCAL_THREADS + threadIdx.x;
+                double cG = 0.0;
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                    Bs[i * LOCAL_THREADS] = L[i] + rho * G[i];
+                    Ls[i * LOCAL_THREADS] = L[i];
+                    cG += G[i] * G[i];
+                }
+                cG *= 0.5 * rho;
+                const double t0 = (MAT == MAT_MR) ? 1.0 / (rho + m + 4.0 * k) : 1.0 / (rho + m);
+                double t = t0;
+                bool freem = false;
+                descent_point<MAT, D>(X, SmemCol{Bs}, cG, m, k, rho, tol_gs, phi_scale, 0, chunk,
+                                      t0 * 16.0, t, freem, nsw, res, moved, ltab);
             } else {
                 double B[D];
                 double cG = 0.0;
@@ -668,8 +704,15 @@ k_update_local(double *__restrict__ F, double *__restrict__ Lam, double *__restr
             }
             if (Tout) {  // T = F - lam / rho for the next projection (row_fwd's expression)
                 const double irho = 1.0 / rho;
+                if constexpr (BSM) {
+                    const double *Ls = sBL + D * LOCAL_THREADS + threadIdx.x;
 #pragma unroll
-                for (int i = 0; i < D; ++i) Tout[i * M + p] = fma(-L[i], irho, X[i]);
+                    for (int i = 0; i < D; ++i)
+                        Tout[i * M + p] = fma(-Ls[i * LOCAL_THREADS], irho, X[i]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < D; ++i) Tout[i * M + p] = fma(-L[i], irho, X[i]);
+                }
             }
             if (res_out) {
                 res_out[p] = res;
@@ -690,6 +733,7 @@ k_update_local(double *__restrict__ F, double *__restrict__ Lam, double *__restr
 #pragma unroll
     for (int q = 0; q < K; ++q) ops[q] = RED_SUM;
     ops[2] = RED_MAX;
+    if constexpr (BSM) __syncthreads();  // every thread is done with its sBL column
     block_reduce<K>(acc, ops, smem);
     grid_finalize<K>(acc, ops, partials, red_out, count, smem);
 }
