@@ -37,8 +37,8 @@ constexpr int LOCAL_THREADS = MM_LOCAL_THREADS;
 #ifndef LOCAL_MIN_BLOCKS
 #define LOCAL_MIN_BLOCKS 4
 #endif
-#ifndef MM_B_SMEM  // fused pass: B and lam_{k+1} in shared memory instead of registers
-#define MM_B_SMEM 1
+#ifndef MM_B_SMEM  // fused pass: B and lam_{k+1} in shared memory instead of registers:
+#define MM_B_SMEM 0  // measured 2.05 -> 2.27 ms (4 blocks/SM), 2.70 ms (5 blocks): off
 #endif
 #ifndef MM_PREFETCH  // L2 prefetch of the next grid-stride point (prefetch_point):
 #define MM_PREFETCH 0  // measured 2.05 -> 2.13 ms in the fused pass at 256^3, off
