@@ -12,6 +12,8 @@
 #include <sched.h>
 #include <string.h>
 #include <thread>
+
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges per pipeline stage
 #include <vector>
 
 #include "mm_internal.cuh"
@@ -109,14 +111,30 @@ static cudaEvent_t pool_get(mm_ctx *ctx) {
     return e;
 }
 
+// NVTX ranges around every pipeline stage (host-side launch windows, for
+// nsys / ncu --nvtx), on when MM_NVTX=1 in the environment at context creation
+static const char *const kStageName[MM_NSTAGE] = {
+    "mm:local", "mm:row_fwd", "mm:col_fwd", "mm:col_solve", "mm:col_inv", "mm:row_inv",
+    "mm:grad", "mm:frozen", "mm:other", "mm:fused", "mm:plane"};
+
+static bool nvtx_on() {
+    static const bool on = [] {
+        const char *e = getenv("MM_NVTX");
+        return e && atoi(e) != 0;
+    }();
+    return on;
+}
+
 void mm_stage_begin(mm_ctx *ctx, int stage, cudaEvent_t *ev) {
     *ev = nullptr;
+    if (nvtx_on()) nvtxRangePushA(kStageName[stage]);
     if (!ctx->prof_on) return;
     *ev = pool_get(ctx);
     cudaEventRecord(*ev, ctx->stream);
 }
 
 void mm_stage_end(mm_ctx *ctx, int stage, cudaEvent_t ev, int nlaunch) {
+    if (nvtx_on()) nvtxRangePop();
     ctx->launches[stage] += nlaunch;
     if (!ctx->prof_on || !ev) return;
     cudaEvent_t b = pool_get(ctx);

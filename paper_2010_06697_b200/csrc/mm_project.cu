@@ -318,6 +318,9 @@ __device__ __forceinline__ void tile_fft_s(double2 *buf, const double2 *__restri
     }
 }
 
+#ifndef MM_DFT_FALLBACK  // 1: the O(N^2) direct DFT for non-power-of-two lines (A/B)
+#define MM_DFT_FALLBACK 0
+#endif
 // Exact DFT of TK lines of runtime length N (any N), via a scratch tile.
 template <int TK, bool INV>
 __device__ __forceinline__ void tile_dft(double2 *buf, double2 *scr, int N,
@@ -344,13 +347,112 @@ __device__ __forceinline__ void tile_dft(double2 *buf, double2 *scr, int N,
     __syncthreads();
 }
 
+// Mixed-radix Stockham FFT of TK lines of runtime length N (any N): one pass
+// per factor of N (4, 2, 3, 5, then any remaining prime), ping-pong between
+// buf and scr, result in buf.  Pass with radix R after the radices NS:
+// butterfly j < N/R of line c reads x[j + r N/R], twiddles by
+// W_{NS R}^{(j mod NS) r} (the length-N table: index (j mod NS) r N/(NS R)),
+// takes the R-point DFT and writes y[(j - j mod NS) R + j mod NS + r NS].
+// O(N sum of factors) instead of the O(N^2) direct DFT for the grids
+// pocketfft serves in the reference (grid.py:195-220: any n, e.g. the
+// 640 / 800 weak-scaling sizes of SURVEY 8(d) config 5).
+__device__ __forceinline__ int next_radix(int rem) {
+    if (rem % 4 == 0) return 4;
+    if (rem % 2 == 0) return 2;
+    if (rem % 3 == 0) return 3;
+    if (rem % 5 == 0) return 5;
+    for (int p = 7; p * p <= rem; p += 2)
+        if (rem % p == 0) return p;
+    return rem;
+}
+
+template <int TK, bool INV>
+__device__ __noinline__ void tile_fft_mixed(double2 *buf, double2 *scr, int N,
+                                            const double2 *__restrict__ tw) {
+    constexpr int LD = TK + 1;
+    double2 *src = buf, *dst = scr;
+    int NS = 1;
+    for (int rem = N; rem > 1;) {
+        const int R = next_radix(rem);
+        const int nb = N / R, tws = N / (NS * R), rs = N / R;
+        for (int w = threadIdx.x; w < nb * TK; w += blockDim.x) {
+            const int j = w / TK, c = w - j * TK;
+            const int jm = j % NS;
+            const int base = (j - jm) * R + jm;
+            if (R == 2 || R == 4) {
+                double2 v[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    if (r >= R) break;
+                    v[r] = src[(j + r * nb) * LD + c];
+                    if (r > 0 && NS > 1) {
+                        double2 t = __ldg(&tw[jm * r * tws]);
+                        if (INV) t.y = -t.y;
+                        v[r] = cmul(v[r], t);
+                    }
+                }
+                if (R == 2) {
+                    dst[base * LD + c] = cadd(v[0], v[1]);
+                    dst[(base + NS) * LD + c] = csub(v[0], v[1]);
+                } else {
+                    const double2 a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]);
+                    const double2 b0 = cadd(v[1], v[3]), b1 = csub(v[1], v[3]);
+                    // forward: x (-i); inverse: x (+i)
+                    const double2 b1r = INV ? make_double2(-b1.y, b1.x) : make_double2(b1.y, -b1.x);
+                    dst[base * LD + c] = cadd(a0, b0);
+                    dst[(base + NS) * LD + c] = cadd(a1, b1r);
+                    dst[(base + 2 * NS) * LD + c] = csub(a0, b0);
+                    dst[(base + 3 * NS) * LD + c] = csub(a1, b1r);
+                }
+            } else {
+                // generic R-point DFT (R odd prime); W_R^k = tw[k N / R]
+                for (int sidx = 0; sidx < R; ++sidx) {
+                    double2 acc = make_double2(0.0, 0.0);
+                    int k = 0;  // (r * sidx) mod R
+                    for (int r = 0; r < R; ++r) {
+                        double2 v = src[(j + r * nb) * LD + c];
+                        if (r > 0 && NS > 1) {
+                            double2 t = __ldg(&tw[jm * r * tws]);
+                            if (INV) t.y = -t.y;
+                            v = cmul(v, t);
+                        }
+                        double2 wr = __ldg(&tw[k * rs]);
+                        if (INV) wr.y = -wr.y;
+                        acc = cadd(acc, cmul(v, wr));
+                        k += sidx;
+                        if (k >= R) k -= R;
+                    }
+                    dst[(base + sidx * NS) * LD + c] = acc;
+                }
+            }
+        }
+        __syncthreads();
+        double2 *t = src;
+        src = dst;
+        dst = t;
+        NS *= R;
+        rem /= R;
+    }
+    if (src != buf) {
+        for (int w = threadIdx.x; w < N * TK; w += blockDim.x) {
+            const int k = w / TK, c = w % TK;
+            buf[k * LD + c] = src[k * LD + c];
+        }
+        __syncthreads();
+    }
+}
+
 template <int N1, int N2, int TK, bool INV, int NTH = TK * (N1 > N2 ? N1 : N2)>
 __device__ __forceinline__ void line_transform(double2 *buf, double2 *scr, int N,
                                                const double2 *__restrict__ tw) {
-    if constexpr (N1 == 0)
-        tile_dft<TK, INV>(buf, scr, N, tw);
-    else
+    if constexpr (N1 == 0) {
+        if (MM_DFT_FALLBACK)
+            tile_dft<TK, INV>(buf, scr, N, tw);
+        else
+            tile_fft_mixed<TK, INV>(buf, scr, N, tw);
+    } else {
         tile_fft<N1, N2, TK, INV, NTH>(buf, tw);
+    }
 }
 
 struct RowGeom {

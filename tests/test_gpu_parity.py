@@ -109,7 +109,10 @@ def test_projection(name):
 
 
 @pytest.mark.parametrize("dim,n", [(2, 5), (2, 7), (2, 16), (2, 64), (2, 128), (3, 6), (3, 9),
-                                   (3, 16), (3, 32), (3, 64)])
+                                   (3, 16), (3, 32), (3, 64),
+                                   # mixed-radix lines (tile_fft_mixed): 2^a 3^b 5^c and primes
+                                   (2, 22), (2, 26), (2, 96), (2, 160), (2, 250), (3, 14),
+                                   (3, 24), (3, 40), (3, 60), (3, 96)])
 def test_projection_matches_oracle(dim, n):
     rng = np.random.default_rng(100 + n)
     L = 0.5
@@ -501,3 +504,27 @@ def test_reassigned_moduli_reach_the_device():
         out.append((np.array(st.F), np.array(st.lam), [r[:5] for r in st.history]))
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
     assert out[0][2] == out[1][2]
+
+
+@pytest.mark.parametrize("n,K", [(24, 8), (40, 6)])
+def test_mixed_radix_grid_trajectory_matches_oracle(n, K):
+    """Non-power-of-two 3D grids run the row layout with mixed-radix line
+    FFTs (radices 4, 2, 3, 5): whole outer iterations against the oracle."""
+    grid, mu, kap = _laminate(3, n, 0)
+    bc = mm.MacroBC.strain(np.diag([0.95, 1.0, 1.0]))
+    m = mm.MooneyRivlin(mu, kap, dim=3, mu_rep=1.0)
+    params = mm.SolverParams(max_outer=K)
+    st = mm.solver.init_state(grid, m, bc, params)
+    F0 = np.array(st.F) + 1e-4 * np.random.default_rng(0).standard_normal(st.F.shape)
+    st.F = F0.copy()
+    st, _ = mm.solve(grid, m, bc, params, policy=mm.RatioToDual(0.3), state=st,
+                     raise_on_max=False)
+    om = oracle.MR(mu, kap, dim=3, mu_rep=1.0)
+    op = oracle.Params(max_outer=K)
+    ost = oracle.init_state(3, n, om, bc.strain_mask, bc.value, op)
+    ost.F = F0.copy()
+    ost, _ = oracle.solve(3, n, 0.5, om, bc.strain_mask, bc.value, op,
+                          policy=oracle.RatioToDual(0.3), state=ost, raise_on_max=False)
+    for k in ("F", "lam", "grad_u", "u_tilde"):
+        assert rel_l2(getattr(st, k), getattr(ost, k)) < 1e-10, k
+    assert st.total_sweeps == ost.total_sweeps

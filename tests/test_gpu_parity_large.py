@@ -156,11 +156,13 @@ def _numpy_pipeline(dim, n, L, T):
     return u
 
 
-@pytest.mark.parametrize("dim,n", [(3, 512), (2, 1024)])
+@pytest.mark.parametrize("dim,n", [(3, 512), (2, 1024), (2, 640), (2, 800), (3, 160)])
 def test_projection_row_layout_sizes_match_numpy(dim, n):
     """3D n = 512 runs the row layout (k_row_fwd, persistent k_colp<32,16>,
     k_col solve, k_row_inv_p<16,16>); 2D 1024^2 runs the N = 1024 column
-    FFT.  lam = 0 and rho = 1, so T = F (host memory: one tensor field)."""
+    FFT; 2D 640^2 / 800^2 and 3D 160^3 run the mixed-radix line FFTs at the
+    SURVEY config-5 weak-scaling lengths.  lam = 0 and rho = 1, so T = F
+    (host memory: one tensor field)."""
     rng = np.random.default_rng(900 + n)
     shape = (n,) * dim
     F = rng.standard_normal(shape + (dim, dim))
