@@ -124,7 +124,7 @@ def test_projection_matches_oracle(dim, n):
     pr = mm.helmholtz_project(mm.Grid(dim, n, L), F, lam, 2.5, mm.MacroBC(mask, value))
     assert rel_l2(pr.u_tilde, ot) < 1e-12
     assert rel_l2(pr.grad_u, og) < 1e-12
-    assert rel_l2(pr.u_mean, ou) < 1e-14
+    assert rel_l2(pr.u_mean, ou) < 1e-13  # device-order mean over up to 0.9M points
 
 
 def test_discrete_grad_div_match_oracle_stencils():
