@@ -124,7 +124,8 @@ int mm_abi_version(void);
  * which = MM_STRUCT_* below; -1 for an unknown id. */
 enum mm_struct_id {
     MM_STRUCT_LOCAL_STATS = 0, MM_STRUCT_UPDATE_STATS = 1, MM_STRUCT_STEP_PARAMS = 2,
-    MM_STRUCT_STEP_RESULT = 3, MM_STRUCT_PROFILE = 4, MM_STRUCT_LCE_PARAMS = 5
+    MM_STRUCT_STEP_RESULT = 3, MM_STRUCT_PROFILE = 4, MM_STRUCT_LCE_PARAMS = 5,
+    MM_STRUCT_SOLVE_PARAMS = 6, MM_STRUCT_SOLVE_RESULT = 7
 };
 int64_t mm_struct_size(int which);
 
@@ -254,6 +255,35 @@ int mm_residuals_and_step(mm_ctx *ctx, const mm_step_params *p, mm_step_result *
 int mm_update_and_sweep(mm_ctx *ctx, int material, double rho_next, double tol,
                         int64_t max_sweeps, double phi_scale, int want_points,
                         mm_local_stats *ls, mm_update_stats *us);
+
+/* solve()'s whole fused loop in the library (solver.py:305-339 with the
+ * fused schedule, solver.py:252-302 per iteration): the policy's metered
+ * local chunks, macro_gradient (projection.py:125-129), mm_residuals_and_step,
+ * the convergence test -- the same decisions in the Python loop's float
+ * order, without a Python round trip per iteration.  `step` carries the
+ * per-solve constants of mm_step_params (its u_mean / rho / r_l /
+ * outer_iter / last_allowed fields are ignored).  hist receives 4 doubles
+ * per completed iteration (r_p, r_d, r_l, rho after the update).  Returns
+ * MM_ERR_DIVERGED when the guard trips (the result is filled up to that
+ * iteration, whose history entry is not written). */
+enum mm_policy_kind { MM_POLICY_EXACT = 0, MM_POLICY_FRACTION = 1, MM_POLICY_RATIO = 2 };
+typedef struct {
+    mm_step_params step;
+    double bc_mask[9], bc_value[9];  /* MacroBC (strain_mask as 0/1, value), d*d used */
+    double rho, r_d_prev;            /* state.rho, state.r_d_prev on entry */
+    double lam_sum[9];               /* sum of lam over points on entry */
+    int64_t outer_iter, max_outer, max_local;
+    int policy;                      /* mm_policy_kind */
+    int64_t policy_chunk;
+    double fraction;                 /* FractionConverged.fraction */
+} mm_solve_params;
+typedef struct {
+    int64_t iterations, outer_iter, total_sweeps;
+    int converged, diverged;
+    double rho, r_d_prev, point_sweeps;
+    double lam_sum[9], u_mean[9];
+} mm_solve_result;
+int mm_solve_fused(mm_ctx *ctx, const mm_solve_params *p, mm_solve_result *r, double *hist);
 
 /* Slab decomposition: rank `rank` of `nranks` holds planes
  * [rank*n/nranks, (rank+1)*n/nranks) of a 3D n^3 grid (n divisible by

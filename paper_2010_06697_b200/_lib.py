@@ -31,6 +31,7 @@ FIELD_ANG, FIELD_CHART, FIELD_PINC, FIELD_N0, FIELD_FF, FIELD_PREV_ANG, FIELD_PR
 FIELD_PREV_PINC = 14
 
 MAT_MR, MAT_QUADRATIC, MAT_LCE, MAT_MR_DESCENT = range(4)
+POLICY_EXACT, POLICY_FRACTION, POLICY_RATIO = range(3)
 
 # every symbol include/mm_admm.h declares (checked by the CPU test suite)
 EXPORTS = (
@@ -44,7 +45,7 @@ EXPORTS = (
     "mm_equilibrium_residual", "mm_selftest_log", "mm_slab_set_peers", "mm_slab_ipc_handle",
     "mm_slab_open_peers", "mm_bloch_setup", "mm_bloch_start", "mm_bloch_iterate",
     "mm_bloch_mode", "mm_debug_lce_counters", "mm_residuals_and_step", "mm_slab_field",
-    "mm_slab_stream",
+    "mm_slab_stream", "mm_solve_fused",
 )
 
 SLAB_HALO_T, SLAB_FWD, SLAB_SOLVE, SLAB_INV = range(4)
@@ -85,6 +86,23 @@ class StepResultC(ctypes.Structure):
     _fields_ = [("r_p", ctypes.c_double), ("r_d", ctypes.c_double), ("rho_next", ctypes.c_double),
                 ("diverged", ctypes.c_int), ("done", ctypes.c_int), ("swept", ctypes.c_int),
                 ("sum_lam", ctypes.c_double * 9)]
+
+
+class SolveParamsC(ctypes.Structure):
+    _fields_ = [("step", StepParamsC), ("bc_mask", ctypes.c_double * 9),
+                ("bc_value", ctypes.c_double * 9), ("rho", ctypes.c_double),
+                ("r_d_prev", ctypes.c_double), ("lam_sum", ctypes.c_double * 9),
+                ("outer_iter", ctypes.c_int64), ("max_outer", ctypes.c_int64),
+                ("max_local", ctypes.c_int64), ("policy", ctypes.c_int),
+                ("policy_chunk", ctypes.c_int64), ("fraction", ctypes.c_double)]
+
+
+class SolveResultC(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int64), ("outer_iter", ctypes.c_int64),
+                ("total_sweeps", ctypes.c_int64), ("converged", ctypes.c_int),
+                ("diverged", ctypes.c_int), ("rho", ctypes.c_double),
+                ("r_d_prev", ctypes.c_double), ("point_sweeps", ctypes.c_double),
+                ("lam_sum", ctypes.c_double * 9), ("u_mean", ctypes.c_double * 9)]
 
 
 class ProfileC(ctypes.Structure):
@@ -226,6 +244,8 @@ def load_library():
             "mm_slab_field": ([P, I, PP, ctypes.POINTER(I64), ctypes.POINTER(I),
                                ctypes.POINTER(I)], I),
             "mm_slab_stream": ([P, PP], I),
+            "mm_solve_fused": ([P, ctypes.POINTER(SolveParamsC), ctypes.POINTER(SolveResultC),
+                                P], I),
             "mm_residuals_and_step": ([P, ctypes.POINTER(StepParamsC), ctypes.POINTER(StepResultC),
                                        ctypes.POINTER(LocalStatsC)], I),
         }
@@ -420,6 +440,18 @@ class Context:
         self.check(self.lib.mm_residuals_and_step(self.h, ctypes.byref(prm), ctypes.byref(res),
                                                   ctypes.byref(ls)))
         return res, ls
+
+    def solve_fused(self, prm, max_outer):
+        """mm_solve_fused: returns (result, history (iterations, 4), status);
+        a diverged run returns MM_ERR_DIVERGED with the result filled."""
+        res = SolveResultC()
+        hist = np.zeros((max(int(max_outer), 1), 4))
+        rc = self.lib.mm_solve_fused(self.h, ctypes.byref(prm), ctypes.byref(res), _ptr(hist))
+        if rc not in (MM_OK, MM_ERR_DIVERGED):
+            self.check(rc)
+        n = int(res.iterations) - (1 if res.diverged else 0)
+        msg = self.lib.mm_last_error(self.h).decode() if rc else ""
+        return res, hist[:n].copy(), rc, msg
 
     def update_multiplier(self):
         st = UpdateStatsC()

@@ -495,6 +495,8 @@ int64_t mm_struct_size(int which) {
         case MM_STRUCT_STEP_RESULT: return (int64_t)sizeof(mm_step_result);
         case MM_STRUCT_PROFILE: return (int64_t)sizeof(mm_profile);
         case MM_STRUCT_LCE_PARAMS: return (int64_t)sizeof(mm_lce_params);
+        case MM_STRUCT_SOLVE_PARAMS: return (int64_t)sizeof(mm_solve_params);
+        case MM_STRUCT_SOLVE_RESULT: return (int64_t)sizeof(mm_solve_result);
         default: return -1;
     }
 }
@@ -1188,6 +1190,109 @@ int mm_residuals_and_step(mm_ctx *ctx, const mm_step_params *p, mm_step_result *
     }
     memcpy(out->sum_lam, us.sum_lam, sizeof us.sum_lam);
     return MM_OK;
+}
+
+// solve()'s fused loop (solver.py _solve_fused, device-decided branch),
+// statement for statement in the Python loop's float order
+int mm_solve_fused(mm_ctx *ctx, const mm_solve_params *p, mm_solve_result *r, double *hist) {
+    if (!ctx || !p || !r || !hist) return MM_ERR_PARAM;
+    if (ctx->slab_mode || ctx->points_only)
+        return mm_fail(ctx, MM_ERR_CONFIG, "mm_solve_fused runs on a single-grid context");
+    memset(r, 0, sizeof *r);
+    const int d = ctx->dim, D = ctx->D;
+    const double npts = p->step.npts;
+    mm_step_params prm = p->step;
+    double rho = p->rho, r_d_prev = p->r_d_prev;
+    double lam_sum[9];
+    memcpy(lam_sum, p->lam_sum, sizeof lam_sum);
+    int64_t outer_iter = p->outer_iter, total_sweeps = 0;
+    double point_sweeps = 0.0;
+    bool have_pending = false;
+    mm_local_stats pending{}, stats{};
+    double u_mean[9] = {0};
+    int rc = MM_OK;
+    const int64_t pchunk = p->policy_chunk;
+    for (int64_t it = 0; it < p->max_outer; ++it) {
+        // LocalPolicy.target_tol (solver.py:128-199)
+        double tol_pt = prm.point_tol;
+        if (p->policy == MM_POLICY_RATIO) {
+            if (!isfinite(r_d_prev)) tol_pt = 1.0;
+            else {
+                const double b = p->step.ratio * r_d_prev;
+                tol_pt = (b > prm.point_tol) ? b : prm.point_tol;  // Python max(a, b)
+            }
+        }
+        int64_t sweeps_total = 0;
+        for (;;) {
+            const int64_t chunk = std::min(pchunk, p->max_local - sweeps_total);
+            if (have_pending) {
+                stats = pending;
+                have_pending = false;
+            } else {
+                // MooneyRivlin/_quadratic _device_local: tol = point_tol * mu_rep
+                if ((rc = mm_local_sweeps(ctx, prm.material, rho, tol_pt * prm.mu_rep, chunk,
+                                          prm.phi_scale, 0, &stats)))
+                    return rc;
+            }
+            sweeps_total += stats.sweeps;
+            point_sweeps += stats.sum_nsw;
+            const double frac = npts ? (double)stats.n_conv / npts : 1.0;
+            const bool pol_done = p->policy == MM_POLICY_FRACTION ? frac >= p->fraction
+                                                                  : frac >= 1.0;
+            if (pol_done || stats.sweeps < chunk || sweeps_total >= p->max_local) break;
+        }
+        total_sweeps += sweeps_total;
+        const double r_l = sqrt(stats.sum_res2 / npts) / prm.mu_rep;
+        // macro_gradient (projection.py:125-129)
+        for (int i = 0; i < 9; ++i) u_mean[i] = 0.0;
+        for (int i = 0; i < D; ++i) {
+            const double Fm = stats.sum_F[i] / npts;
+            const double Lm = lam_sum[i] / npts;
+            const double su = Fm - (Lm - p->bc_value[i]) / rho;
+            u_mean[i] = p->bc_mask[i] != 0.0 ? p->bc_value[i] : su;
+        }
+        memcpy(prm.u_mean, u_mean, sizeof u_mean);
+        prm.rho = rho;
+        prm.r_l = r_l;
+        prm.outer_iter = outer_iter + 1;
+        prm.last_allowed = it == p->max_outer - 1 ? 1 : 0;
+        mm_step_result res;
+        mm_local_stats ls;
+        if ((rc = mm_residuals_and_step(ctx, &prm, &res, &ls))) return rc;
+        outer_iter += 1;
+        r_d_prev = res.r_d;
+        memcpy(lam_sum, res.sum_lam, sizeof lam_sum);
+        r->iterations = it + 1;
+        if (res.diverged) {
+            r->diverged = 1;
+            rc = MM_ERR_DIVERGED;
+            mm_fail(ctx, MM_ERR_DIVERGED, "primal residual %.3e at outer iteration %lld",
+                    res.r_p, (long long)outer_iter);
+            break;
+        }
+        rho = res.rho_next;
+        if (res.swept) {
+            pending = ls;
+            have_pending = true;
+        }
+        hist[4 * it + 0] = res.r_p;
+        hist[4 * it + 1] = res.r_d;
+        hist[4 * it + 2] = r_l;
+        hist[4 * it + 3] = rho;
+        if (res.done) {
+            r->converged = 1;
+            break;
+        }
+    }
+    r->outer_iter = outer_iter;
+    r->total_sweeps = total_sweeps;
+    r->rho = rho;
+    r->r_d_prev = r_d_prev;
+    r->point_sweeps = point_sweeps;
+    memcpy(r->lam_sum, lam_sum, sizeof lam_sum);
+    memcpy(r->u_mean, u_mean, sizeof u_mean);
+    (void)d;
+    return rc;
 }
 
 int mm_project_update(mm_ctx *ctx, double rho, const double *u_mean, mm_update_stats *out) {

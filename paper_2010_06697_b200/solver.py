@@ -598,6 +598,8 @@ def _solve_fused(grid, model, bc, params, policy, state, r_l_tol):
         prm.material = mat
         prm.phi_scale = phi_scale
         prm.chunk = min(policy.chunk, params.max_local)
+    if device_step and os.environ.get("MM_C_LOOP", "1") != "0":
+        return _solve_fused_c(eng, grid, model, bc, params, policy, state, prm, mat, phi_scale)
     for it in range(params.max_outer):
         t_start = time.perf_counter()
         tol_pt = policy.target_tol(params, state.r_d_prev)
@@ -689,6 +691,58 @@ def _solve_fused(grid, model, bc, params, policy, state, r_l_tol):
             converged = True
             break
     return converged, resid
+
+
+def _solve_fused_c(eng, grid, model, bc, params, policy, state, prm, mat, phi_scale):
+    """The fused loop of _solve_fused run inside the library (mm_solve_fused):
+    the same policy metering, macro control, residuals, decisions and float
+    order as the Python loop above, no Python round trip per iteration
+    (bitwise identical; MM_C_LOOP=0 runs the Python loop).  Residuals.wall_ms
+    is the loop's average per iteration."""
+    d = grid.dim
+    sp = _lib.SolveParamsC()
+    sp.step = prm
+    mask = np.zeros(9)
+    val = np.zeros(9)
+    mask[: d * d] = np.asarray(bc.strain_mask, dtype=bool).reshape(-1)
+    val[: d * d] = np.asarray(bc.value, dtype=float).reshape(-1)
+    sp.bc_mask[:] = mask
+    sp.bc_value[:] = val
+    sp.rho = state.rho
+    sp.r_d_prev = float(state.r_d_prev)
+    lam = np.zeros(9)
+    if eng.lam_sum is None:
+        eng.lam_mean()
+    lam[: d * d] = np.asarray(eng.lam_sum, dtype=float).reshape(-1)
+    sp.lam_sum[:] = lam
+    sp.outer_iter = state.outer_iter
+    sp.max_outer = params.max_outer
+    sp.max_local = params.max_local
+    sp.policy = (_lib.POLICY_RATIO if isinstance(policy, RatioToDual) else
+                 _lib.POLICY_FRACTION if isinstance(policy, FractionConverged) else
+                 _lib.POLICY_EXACT)
+    sp.policy_chunk = policy.chunk
+    sp.fraction = getattr(policy, "fraction", 1.0)
+    t0 = time.perf_counter()
+    res, hist, rc, msg = eng.ctx.solve_fused(sp, params.max_outer)
+    wall = (time.perf_counter() - t0) * 1e3 / max(int(res.iterations), 1)
+    state._mark_device("F", "grad_u", "u_tilde", "lam")
+    base = state.outer_iter
+    for i, (r_p, r_d, r_l, rho) in enumerate(hist):
+        state.history.append(Residuals(base + i + 1, float(r_p), float(r_d), float(r_l),
+                                       float(rho), wall))
+    state.outer_iter = int(res.outer_iter)
+    state.total_sweeps += int(res.total_sweeps)
+    state.r_d_prev = float(res.r_d_prev)
+    state.rho = float(res.rho)
+    if res.iterations:
+        state.u_mean = np.array(res.u_mean[: d * d]).reshape(d, d)
+    eng.lam_sum = np.array(res.lam_sum[: d * d])
+    eng.point_sweeps += float(res.point_sweeps)
+    if rc == _lib.MM_ERR_DIVERGED:
+        raise DivergenceError(msg)
+    resid = state.history[-1] if len(hist) else None
+    return bool(res.converged), resid
 
 
 # ---------------------------------------------------------------------------

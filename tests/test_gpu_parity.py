@@ -466,17 +466,21 @@ def test_library_decision_step_matches_host_loop(dim, n, pol, monkeypatch):
               "fraction": mm.FractionConverged(0.9, 2)}[pol]
     params = mm.SolverParams(max_outer=400)
     out = {}
-    for flag in ("0", "1"):
-        monkeypatch.setenv("MM_HOST_DECIDE", flag)
+    # "0": the library loop (mm_solve_fused); "py": the Python loop over
+    # mm_residuals_and_step; "1": the host-decided loop
+    for flag in ("0", "py", "1"):
+        monkeypatch.setenv("MM_HOST_DECIDE", "1" if flag == "1" else "0")
+        monkeypatch.setenv("MM_C_LOOP", "0" if flag == "py" else "1")
         st = mm.solver.init_state(grid, m, bc, params)
         st.F = st.F + 1e-3 * np.random.default_rng(1).standard_normal(st.F.shape)
         st, conv = mm.solve(grid, m, bc, params, policy=policy, state=st, raise_on_max=False)
         out[flag] = (conv, [np.array(getattr(st, k)) for k in ("F", "lam", "grad_u", "u_tilde")],
                      [r[:5] for r in st.history], st.total_sweeps, st.rho)
-    a, b = out["0"], out["1"]
-    assert a[0] == b[0] and a[2] == b[2] and a[3] == b[3] and a[4] == b[4]
-    for x, y in zip(a[1], b[1]):
-        assert np.array_equal(x, y)
+    for other in ("py", "1"):
+        a, b = out["0"], out[other]
+        assert a[0] == b[0] and a[2] == b[2] and a[3] == b[3] and a[4] == b[4]
+        for x, y in zip(a[1], b[1]):
+            assert np.array_equal(x, y)
 
 
 def test_reassigned_moduli_reach_the_device():
