@@ -57,8 +57,22 @@ constexpr int LOCAL_THREADS = MM_LOCAL_THREADS;
 // log().
 // ---------------------------------------------------------------------------
 constexpr int LOGTAB_N = 128;
+#ifndef MM_LOGK_CONST  // 1: log_pos constants from the constant bank (c_logk)
+#define MM_LOGK_CONST 1
+#endif
+#if MM_LOGK_CONST
+#define MM_LOGK(i) c_logk[i]
+#else
+#define MM_LOGK(i) (((const double[8]){1.0 / 7.0, -1.0 / 6.0, 0.2, -0.25, 1.0 / 3.0, -0.5, \
+                                       0x1.62e42fefa3800p-1, 0x1.ef35793c76730p-45})[i])
+#endif
 __device__ double g_logtab[3 * LOGTAB_N];  // invc | log c (hi) | log c (lo)
 static bool g_logtab_ready[64];
+
+// polynomial / ln 2 constants as constant-bank operands of the DFMAs (as
+// double immediates each use was rematerialised by two UMOVs per evaluation)
+__constant__ double c_logk[8] = {1.0 / 7.0, -1.0 / 6.0, 0.2, -0.25, 1.0 / 3.0, -0.5,
+                                 0x1.62e42fefa3800p-1, 0x1.ef35793c76730p-45};
 
 __device__ __forceinline__ double log_pos(double x, const double *__restrict__ T) {
     const uint64_t ix = (uint64_t)__double_as_longlong(x);
@@ -68,17 +82,16 @@ __device__ __forceinline__ double log_pos(double x, const double *__restrict__ T
     const double kd = (double)((int64_t)tmp >> 52);
     const double z = __longlong_as_double((long long)(ix - (tmp & 0xfff0000000000000ULL)));
     const double r = fma(z, T[i], -1.0);
-    const double ln2_hi = 0x1.62e42fefa3800p-1, ln2_lo = 0x1.ef35793c76730p-45;
-    const double w = fma(kd, ln2_hi, T[LOGTAB_N + i]);
+    const double w = fma(kd, MM_LOGK(6), T[LOGTAB_N + i]);
     const double hi = w + r;
     const double lo = (w - hi) + r;
     const double r2 = r * r;
-    double p = fma(r, 1.0 / 7.0, -1.0 / 6.0);
-    p = fma(r, p, 0.2);
-    p = fma(r, p, -0.25);
-    p = fma(r, p, 1.0 / 3.0);
-    p = fma(r, p, -0.5);
-    return hi + (fma(kd, ln2_lo, T[2 * LOGTAB_N + i]) + fma(r2, p, lo));
+    double p = fma(r, MM_LOGK(0), MM_LOGK(1));
+    p = fma(r, p, MM_LOGK(2));
+    p = fma(r, p, MM_LOGK(3));
+    p = fma(r, p, MM_LOGK(4));
+    p = fma(r, p, MM_LOGK(5));
+    return hi + (fma(kd, MM_LOGK(7), T[2 * LOGTAB_N + i]) + fma(r2, p, lo));
 }
 
 static int ensure_logtab(mm_ctx *ctx) {
