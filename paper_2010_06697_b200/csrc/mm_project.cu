@@ -1238,6 +1238,126 @@ k_plane(double2 *__restrict__ spec, PlaneGeom g, const double2 *__restrict__ tw)
 }
 
 // ---------------------------------------------------------------------------
+// Plane pass, half-warp per line (n = 256, MM_PLANE_HW).  The same three
+// passes per (c, k2) plane and cluster barriers as k_plane, but each line is
+// owned by 16 consecutive lanes that load it (cp.async, double-buffered per
+// line slot), transform it (256 = 16 x 16: two radix-16 Stockham stages in
+// registers, exchanged through the slot's shared buffer) and store it with
+// warp-level synchronisation only: no block-wide barrier inside a pass, so
+// every half-warp streams its lines independently (k_plane's tile FFT was
+// bound by __syncthreads and shared-memory latency: 12 warps/SM, barrier
+// stalls 24 %).  Element i = 16 a + b of a line sits at slot 16 a + (b ^ a):
+// the stage-1 transpose (y[16 q + r] for fixed r across lanes q) and the
+// natural-order reads / writes (x[q + 16 r]) are both conflict-free.
+// ---------------------------------------------------------------------------
+#ifndef MM_PLANE_HW
+#define MM_PLANE_HW 1
+#endif
+#ifndef MM_PLANE_HW_NT
+#define MM_PLANE_HW_NT 128
+#endif
+#ifndef MM_PLANE_HW_MINB
+#define MM_PLANE_HW_MINB 3
+#endif
+
+__device__ __forceinline__ int hw_slot(int a, int b) { return 16 * a + (b ^ a); }
+
+// 256-point FFT of the line in `buf` (this half-warp's slot), lane q of 16
+__device__ __forceinline__ void hw_fft256(double2 *buf, int q, const double2 *__restrict__ tw,
+                                          bool inv) {
+    double2 v[16];
+    // stage 1 (radix 16, NS = 1): x[q + 16 r] -> y[16 q + r]
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = buf[hw_slot(r, q)];
+    __syncwarp();
+    fft_reg_rt<16>(v, inv);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) buf[hw_slot(q, r)] = v[r];
+    __syncwarp();
+    // stage 2 (radix 16, NS = 16): twiddle W_256^{q r}, x[q + 16 r] -> y[q + 16 r]
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = buf[hw_slot(r, q)];
+#pragma unroll
+    for (int r = 1; r < 16; ++r) {
+        double2 w = __ldg(&tw[q * r]);
+        if (inv) w.y = -w.y;
+        v[r] = cmul(v[r], w);
+    }
+    fft_reg_rt<16>(v, inv);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) buf[hw_slot(r, q)] = v[r];
+    __syncwarp();
+}
+
+template <int KIND, int NSLOT, int LPC>
+__device__ __forceinline__ void hw_pass(double2 *__restrict__ pl, double2 *bufs, int r0, int slot,
+                                        int q, const PlaneGeom &g, int k2,
+                                        const double2 *__restrict__ tw) {
+    constexpr int N = 256, NL = LPC / NSLOT;  // lines per slot in this pass
+    auto elem = [&](int t, int n) -> int64_t {
+        if constexpr (KIND == PL_COL_SOLVE) return (int64_t)n * N + t;
+        else return (int64_t)t * N + n;
+    };
+    auto issue = [&](int t, double2 *dst) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) cp_async16(&dst[hw_slot(k, q)], &pl[elem(t, 16 * k + q)], 16);
+        cp_async_commit();
+    };
+    issue(r0 + slot, bufs);
+#pragma unroll 1
+    for (int i = 0; i < NL; ++i) {
+        const int t = r0 + slot + i * NSLOT;
+        double2 *buf = bufs + (i & 1) * N;
+        if (i + 1 < NL) issue(t + NSLOT, bufs + ((i + 1) & 1) * N);
+        else cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
+        hw_fft256(buf, q, tw, KIND == PL_ROW_INV);
+        if constexpr (KIND == PL_COL_SOLVE) {
+            // u_hat = -d_hat / |g|^2 on live modes (k_col<COL_SOLVE>'s expression
+            // and summation order); the line is column i1 = t of plane k2
+            const double s1 = __ldg(&g.sym[N + t]);
+            const double sl = __ldg(&g.sym[2 * N + k2]);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const int n = 16 * k + q;
+                double gsq = __ldg(&g.sym[n]);
+                gsq = gsq + s1;
+                gsq = gsq + sl;
+                const double inv = (gsq > g.thresh) ? 1.0 / gsq : 0.0;
+                const int sidx = hw_slot(k, q);
+                buf[sidx] = cscale(buf[sidx], -inv * g.scale);
+            }
+            __syncwarp();
+            hw_fft256(buf, q, tw, true);
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) pl[elem(t, 16 * k + q)] = buf[hw_slot(k, q)];
+        __syncwarp();  // the buffer is refilled by the issue two lines on
+    }
+    cp_async_wait<0>();
+}
+
+template <int NTH, int CS>
+__global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(NTH, MM_PLANE_HW_MINB)
+k_plane_hw(double2 *__restrict__ spec, PlaneGeom g, const double2 *__restrict__ tw) {
+    constexpr int N = 256, NSLOT = NTH / 16, LPC = N / CS;
+    static_assert(LPC % NSLOT == 0, "lines per CTA divide among the slots");
+    extern __shared__ double2 smem_c[];
+    const int plane = blockIdx.x / CS;  // c * nh + k2
+    const int r = blockIdx.x % CS;      // rank in the cluster
+    const int k2 = plane % g.nh;
+    const int slot = threadIdx.x >> 4, q = threadIdx.x & 15;
+    double2 *bufs = smem_c + slot * 2 * N;
+    double2 *pl = spec + (int64_t)plane * N * N;
+    hw_pass<PL_ROW_FWD, NSLOT, LPC>(pl, bufs, r * LPC, slot, q, g, k2, tw);
+    cluster_barrier();
+    hw_pass<PL_COL_SOLVE, NSLOT, LPC>(pl, bufs, r * LPC, slot, q, g, k2, tw);
+    cluster_barrier();
+    hw_pass<PL_ROW_INV, NSLOT, LPC>(pl, bufs, r * LPC, slot, q, g, k2, tw);
+}
+
+// ---------------------------------------------------------------------------
 // F: gradient of u_tilde, multiplier ascent and residual sums
 // slots: 0 sum dG^2, 1 sum misfit^2, 2.. sum lam (D)
 // ---------------------------------------------------------------------------
@@ -1740,7 +1860,18 @@ int run_plane(mm_ctx *ctx, double scale) {
         case 32: return run_plane_n<8, 4>(ctx, g);
         case 64: return run_plane_n<8, 8>(ctx, g);
         case 128: return run_plane_n<16, 8>(ctx, g);
-        case 256: return run_plane_n<16, 16>(ctx, g);
+        case 256:
+            if (MM_PLANE_HW) {
+                constexpr int NTH = MM_PLANE_HW_NT, CS = 8;
+                const size_t smem = sizeof(double2) * 2 * 256 * (NTH / 16);
+                auto kern = k_plane_hw<NTH, CS>;
+                int rc = launch_smem(ctx, kern, dim3(1), NTH, smem);
+                if (rc) return rc;
+                kern<<<CS * ctx->dim * g.nh, NTH, smem, ctx->stream>>>(ctx->spec, g, ctx->tw_full);
+                MM_LAUNCH_CHECK(ctx);
+                return MM_OK;
+            }
+            return run_plane_n<16, 16>(ctx, g);
         default: return mm_fail(ctx, MM_ERR_CONFIG, "plane FFT needs n in 16..256 (pow2)");
     }
 }
