@@ -1250,8 +1250,8 @@ k_plane(double2 *__restrict__ spec, PlaneGeom g, const double2 *__restrict__ tw)
 // the stage-1 transpose (y[16 q + r] for fixed r across lanes q) and the
 // natural-order reads / writes (x[q + 16 r]) are both conflict-free.
 // ---------------------------------------------------------------------------
-#ifndef MM_PLANE_HW
-#define MM_PLANE_HW 1
+#ifndef MM_PLANE_HW  // measured 0.697 (k_plane) -> 0.743 ms at 256^3: the column pass loses
+#define MM_PLANE_HW 0  // coalescing with one line per half-warp; off
 #endif
 #ifndef MM_PLANE_HW_NT
 #define MM_PLANE_HW_NT 128
