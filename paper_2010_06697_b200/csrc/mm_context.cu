@@ -801,6 +801,8 @@ void mm_destroy(mm_ctx *ctx) {
                       ctx->halo_in_hi, ctx->halo_out_lo, ctx->halo_out_hi, ctx->sym, ctx->partials, ctx->red_out,
                       ctx->res, ctx->tstate, ctx->stage, ctx->Pbuf, ctx->Tbuf};
     for (double *p : ptrs) mm_free(ctx, p);
+    void *lce_bufs[] = {ctx->lce_fsq0, ctx->lce_list[0], ctx->lce_list[1], ctx->lce_cnt};
+    for (void *p : lce_bufs) mm_free(ctx, p);
     void *others[] = {ctx->spec, ctx->tw_full, ctx->tw_half, ctx->tw_r2c, ctx->red_count,
                       ctx->nsw, ctx->ok, ctx->freestate, ctx->peer_recv, ctx->peer_send};
     for (void *p : others) mm_free(ctx, p);

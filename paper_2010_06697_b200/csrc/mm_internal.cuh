@@ -114,6 +114,11 @@ struct mm_ctx {
     // so that axis-0 neighbours are plain offsets and the halo exchange
     // writes straight into them.  Ut / Ut2 / dirbuf point at plane 0.
     int64_t uM = 0, dM = 0;
+    // Newton-compacted 3D LCE schedule (mm_lce.cu): |F|^2 at call start,
+    // two deferred-point lists and three rotating counters
+    double *lce_fsq0 = nullptr;
+    int *lce_list[2] = {nullptr, nullptr};
+    int *lce_cnt = nullptr;
     double *Ut_base = nullptr, *Ut2_base = nullptr, *dir_base = nullptr;
     // peer-memory transposes: device tables of every rank's RECV / SEND buffer
     double2 **peer_recv = nullptr, **peer_send = nullptr;

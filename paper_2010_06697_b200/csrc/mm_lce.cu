@@ -464,7 +464,30 @@ __device__ unsigned long long g_lce_cnt[8];
 #define LCE_CNT(i) ((void)0)
 #endif
 
+// Newton-compacted schedule (LceSplit.mode != 0).  A policy chunk runs as
+// rounds: round 0 (mode 1) walks every point through its cheap multiplier-
+// only sweeps and stops it at its first Newton step, which it defers
+// (state stored, sweep count one back, index appended to list_out); round
+// k >= 1 (mode 2) takes the deferred points, re-evaluates the deferring
+// sweep (same state, same bits, same decision), performs that Newton step,
+// continues with cheap sweeps and defers again at the next Newton step.
+// Every lane of a warp therefore executes exactly one Newton step per
+// round, instead of the warp running the Newton code whenever any of its
+// points needs it (8 of 32 lanes active per instruction on polydomain
+// inputs).  The per-point sequence of sweeps is the plain loop's; the batch
+// sums come from k_lce3_reduce over the per-point results.
+struct LceSplit {
+    int mode;                      // 0: plain loop; 1: round 0; 2: round >= 1
+    const int *list_in;            // mode 2: points of this round
+    const int *count_in;
+    int *list_out, *count_out;     // deferred points (appended)
+    int *count_clear;              // the counter the next round appends to
+    int32_t *nsw_io;               // sweeps of this call so far (split: always)
+    double *fsq0_io;               // |F|^2 at the start of the call (tN0)
+};
+
 // slots: 0 sum res^2, 1 n_ok, 2 max nsw, 3..11 sum F
+template <int MODE>  // == LceSplit.mode, a compile-time constant
 __global__ void __launch_bounds__(LCE3_THREADS)
 k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ chart,
         double *__restrict__ pinc, const double *__restrict__ Gg, const double *__restrict__ Lg,
@@ -472,7 +495,7 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
         const double *__restrict__ Fk, const double *__restrict__ angk,
         const double *__restrict__ chartk, int64_t M, LcePar P, double *__restrict__ res_out,
         int32_t *__restrict__ nsw_out, uint8_t *__restrict__ ok_out, double *partials,
-        double *red_out, unsigned int *count) {
+        double *red_out, unsigned int *count, LceSplit SP) {
     extern __shared__ double smA[];  // 132 * LCE3_THREADS
     __shared__ double smem[32 * 13];
     double *S = smA + threadIdx.x;
@@ -486,8 +509,11 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
 #if MM_LCE_STATS
     unsigned long long cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
-         p += (int64_t)gridDim.x * blockDim.x) {
+    if (MODE && blockIdx.x == 0 && threadIdx.x == 0) *SP.count_clear = 0;
+    const int64_t npoints = MODE == 2 ? (int64_t)*SP.count_in : M;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < npoints;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = MODE == 2 ? (int64_t)SP.list_in[idx] : idx;
         double Fl[9], E[9];
 #pragma unroll
         for (int i = 0; i < 9; ++i) {
@@ -509,14 +535,20 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
         }
         double ph = ang[p], th = ang[M + p], pp = pinc[p];
         double fsq0 = 0.0;
+        if (MODE == 2) {
+            fsq0 = SP.fsq0_io[p];
+        } else {
 #pragma unroll
-        for (int i = 0; i < 9; ++i) fsq0 += Fl[i] * Fl[i];
+            for (int i = 0; i < 9; ++i) fsq0 += Fl[i] * Fl[i];
+        }
         const double tF0 = 1.0 / (rho + 2.0 * mur + 2.0 * mual + 3.0 * gam + visF);
         const double tN0 = 1.0 / (P.mu * (2.0 * P.r1d + 2.0 * P.al) * fmax(fsq0, 1.0) + visn + 1e-30);
         const double base = mur + rho + visF;
-        int64_t nsw = 0;
+        int64_t nsw = MODE == 2 ? (int64_t)SP.nsw_io[p] : 0;
         double res = 0.0;
         bool converged = false;
+        bool deferred = false;
+        int newton_budget = MODE == 1 ? 0 : (MODE == 2 ? 1 : 0x7fffffff);
         // Sweeps that only ascend the nested det multiplier (the polydomain
         // stall regime) are cheap; Newton sweeps are ~20x dearer.  Each lane
         // first runs through its cheap sweeps (inner loop) and the warp then
@@ -525,7 +557,7 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
         // divergent Newton per sweep in which only the few lanes that need
         // it are active.  Every lane performs exactly the same sequence of
         // sweeps as the plain loop.
-        int64_t it = 0;
+        int64_t it = nsw;  // the loop keeps it == nsw at the top of every sweep
         while (it < P.max_sweeps + 1) {
             double n[3], sp, cp, st, ct, u[3], cc, J, dJ, pr, cof[9], gFl[9], gF2, gn[3];
             double m1[3], mth[3], g1, g2, gnn, sp2;
@@ -640,6 +672,14 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
             if ((threadIdx.x & 31) == __ffs(__activemask()) - 1) cnt[7] += 32;
 #endif
             if (!newton) break;
+            if (newton_budget == 0) {
+                // defer this Newton step to the next round (split schedule): the
+                // sweep is re-evaluated there, so its count is taken back
+                deferred = true;
+                nsw -= 1;
+                break;
+            }
+            --newton_budget;
             ++it;
             LCE_CNT(1);
             const double phi0 = phiJ3(Fl, n, n0l, P, pp, D, ffl, nkl);
@@ -834,6 +874,23 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
         ang[p] = ph;
         ang[M + p] = th;
         pinc[p] = pp;
+        if (MODE) {
+            SP.nsw_io[p] = (int32_t)nsw;
+            if (MODE == 1) SP.fsq0_io[p] = fsq0;
+            if (deferred) {
+                // warp-aggregated append of the deferred points
+                const unsigned m = __activemask();
+                const int lane = threadIdx.x & 31, lead = __ffs(m) - 1;
+                int base = 0;
+                if (lane == lead) base = atomicAdd(SP.count_out, __popc(m));
+                base = __shfl_sync(m, base, lead);
+                SP.list_out[base + __popc(m & ((1u << lane) - 1u))] = (int)p;
+                continue;
+            }
+            res_out[p] = res;
+            ok_out[p] = converged ? 1 : 0;
+            continue;
+        }
         if (res_out) {
             res_out[p] = res;
             nsw_out[p] = (int32_t)nsw;
@@ -851,6 +908,35 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
     for (int i = 0; i < 8; ++i)
         if (cnt[i]) atomicAdd(&g_lce_cnt[i], cnt[i]);
 #endif
+    if (MODE) return;  // split schedule: k_lce3_reduce sums the per-point results
+    int ops[13];
+#pragma unroll
+    for (int k = 0; k < 13; ++k) ops[k] = RED_SUM;
+    ops[2] = RED_MAX;
+    block_reduce<13>(acc, ops, smem);
+    grid_finalize<13>(acc, ops, partials, red_out, count, smem);
+}
+
+// batch sums of a split-schedule chunk from the per-point results (slots as
+// k_lce3d's: sum res^2, n_ok, max nsw, sum F (9), sum nsw)
+__global__ void __launch_bounds__(256)
+k_lce3_reduce(const double *__restrict__ Fg, const double *__restrict__ res,
+              const uint8_t *__restrict__ ok, const int32_t *__restrict__ nsw, int64_t M,
+              double *partials, double *red_out, unsigned int *count) {
+    __shared__ double smem[32 * 13];
+    double acc[13];
+#pragma unroll
+    for (int k = 0; k < 13; ++k) acc[k] = 0.0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const double r = res[p];
+        acc[0] += r * r;
+        acc[1] += ok[p] ? 1.0 : 0.0;
+        acc[2] = fmax(acc[2], (double)nsw[p]);
+#pragma unroll
+        for (int i = 0; i < 9; ++i) acc[3 + i] += Fg[i * M + p];
+        acc[12] += (double)nsw[p];
+    }
     int ops[13];
 #pragma unroll
     for (int k = 0; k < 13; ++k) ops[k] = RED_SUM;
@@ -1040,16 +1126,69 @@ int mm_run_lce(mm_ctx *ctx, double rho, double tol, int64_t max_sweeps, int want
         if ((rc = mm_ensure_partials(ctx, blocks))) return rc;
         const size_t smem = sizeof(double) * 132 * LCE3_THREADS;
         if (smem > 48 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(k_lce3d, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)smem);
-            if (e != cudaSuccess) return mm_fail(ctx, MM_ERR_CUDA, "%s", cudaGetErrorString(e));
+            for (auto kern : {k_lce3d<0>, k_lce3d<1>, k_lce3d<2>}) {
+                cudaError_t e = cudaFuncSetAttribute(
+                    kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (e != cudaSuccess)
+                    return mm_fail(ctx, MM_ERR_CUDA, "%s", cudaGetErrorString(e));
+            }
         }
-        StageScope ss(ctx, MM_STAGE_LOCAL);
-        k_lce3d<<<blocks, threads, smem, ctx->stream>>>(
-            ctx->F, ctx->ang, ctx->chart, ctx->pinc, ctx->G, ctx->Lam, ctx->n0, ctx->ff, Fk, angk,
-            viscous ? ctx->prevChart : nullptr, M, P, want_points ? ctx->res : nullptr,
-            want_points ? ctx->nsw : nullptr, want_points ? ctx->ok : nullptr, ctx->partials,
-            ctx->red_out, ctx->red_count);
+        const char *split_env = getenv("MM_LCE_SPLIT_MIN");  // per call (tests A/B it)
+        const int64_t split_min = split_env ? atoll(split_env) : (int64_t)1 << 18;
+        const bool split = M >= split_min && max_sweeps <= 256;
+        const double *chk = viscous ? ctx->prevChart : nullptr;
+        if (!split) {
+            StageScope ss(ctx, MM_STAGE_LOCAL);
+            k_lce3d<0><<<blocks, threads, smem, ctx->stream>>>(
+                ctx->F, ctx->ang, ctx->chart, ctx->pinc, ctx->G, ctx->Lam, ctx->n0, ctx->ff, Fk,
+                angk, chk, M, P, want_points ? ctx->res : nullptr,
+                want_points ? ctx->nsw : nullptr, want_points ? ctx->ok : nullptr, ctx->partials,
+                ctx->red_out, ctx->red_count, LceSplit{});
+        } else {
+            if ((rc = mm_ensure_points(ctx))) return rc;
+            if (!ctx->lce_fsq0 &&
+                (rc = mm_alloc(ctx, (void **)&ctx->lce_fsq0, sizeof(double) * M)))
+                return rc;
+            for (int b = 0; b < 2; ++b)
+                if (!ctx->lce_list[b] &&
+                    (rc = mm_alloc(ctx, (void **)&ctx->lce_list[b], sizeof(int) * M)))
+                    return rc;
+            if (!ctx->lce_cnt && (rc = mm_alloc(ctx, (void **)&ctx->lce_cnt, sizeof(int) * 3)))
+                return rc;
+            MM_CUDA(ctx, cudaMemsetAsync(ctx->lce_cnt, 0, sizeof(int) * 3, ctx->stream));
+            StageScope ss(ctx, MM_STAGE_LOCAL, (int)max_sweeps + 2);
+            // round k reads counter k % 3 / list k % 2, appends to counter (k + 1) % 3 /
+            // list (k + 1) % 2 and clears counter (k + 2) % 3; a round finds at most
+            // one Newton step per point, so max_sweeps rounds after round 0 finish
+            // every point (the empty late rounds exit at once)
+            for (int64_t k = 0; k <= max_sweeps; ++k) {
+                LceSplit sp;
+                sp.mode = k == 0 ? 1 : 2;
+                sp.list_in = ctx->lce_list[k % 2];
+                sp.count_in = ctx->lce_cnt + k % 3;
+                sp.list_out = ctx->lce_list[(k + 1) % 2];
+                sp.count_out = ctx->lce_cnt + (k + 1) % 3;
+                sp.count_clear = ctx->lce_cnt + (k + 2) % 3;
+                sp.nsw_io = ctx->nsw;
+                sp.fsq0_io = ctx->lce_fsq0;
+                if (k == 0)
+                    k_lce3d<1><<<blocks, threads, smem, ctx->stream>>>(
+                        ctx->F, ctx->ang, ctx->chart, ctx->pinc, ctx->G, ctx->Lam, ctx->n0,
+                        ctx->ff, Fk, angk, chk, M, P, ctx->res, ctx->nsw, ctx->ok, ctx->partials,
+                        ctx->red_out, ctx->red_count, sp);
+                else
+                    k_lce3d<2><<<blocks, threads, smem, ctx->stream>>>(
+                        ctx->F, ctx->ang, ctx->chart, ctx->pinc, ctx->G, ctx->Lam, ctx->n0,
+                        ctx->ff, Fk, angk, chk, M, P, ctx->res, ctx->nsw, ctx->ok, ctx->partials,
+                        ctx->red_out, ctx->red_count, sp);
+                MM_LAUNCH_CHECK(ctx);
+            }
+            const int rb = (int)std::min<int64_t>((M + 255) / 256, 148 * 8);
+            if ((rc = mm_ensure_partials(ctx, rb))) return rc;
+            k_lce3_reduce<<<rb, 256, 0, ctx->stream>>>(ctx->F, ctx->res, ctx->ok, ctx->nsw, M,
+                                                     ctx->partials, ctx->red_out,
+                                                     ctx->red_count);
+        }
     }
     MM_LAUNCH_CHECK(ctx);
     double r[MM_MAX_PARTIALS];

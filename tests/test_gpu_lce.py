@@ -171,3 +171,35 @@ def test_lce_viscous_time_step_matches_oracle():
     for k in ("F", "lam", "grad_u"):
         assert rel_l2(getattr(st, k), getattr(ost, k)) < 1e-10, k
     assert st.total_sweeps == ost.total_sweeps
+
+
+@pytest.mark.parametrize("chunk", [5, 25])
+def test_lce3d_newton_compacted_schedule_is_the_plain_loop(chunk, monkeypatch):
+    """The Newton-compacted rounds (MM_LCE_SPLIT_MIN=0 forces them) perform
+    every point's sweeps exactly as the single-launch loop: fields, angles,
+    chart, p_inc, per-point residuals, sweep counts and flags bit for bit;
+    the batch sums (reduced afterwards in another order) to roundoff."""
+    rng = np.random.default_rng(21)
+    npts = 3000
+    n0 = rng.standard_normal((npts, 3))
+    n0 /= np.linalg.norm(n0, axis=1, keepdims=True)
+    F0 = np.tile(np.eye(3), (npts, 1, 1)) + 1e-2 * rng.standard_normal((npts, 3, 3))
+    G = np.tile(np.eye(3), (npts, 1, 1)) + 1e-2 * rng.standard_normal((npts, 3, 3))
+    lam = 1e-2 * rng.standard_normal((npts, 3, 3))
+    ff = 1e-3 * rng.standard_normal((npts, 3))
+    out = {}
+    for split in ("0", "1000000000"):
+        monkeypatch.setenv("MM_LCE_SPLIT_MIN", split)
+        m = mm.LiquidCrystalElastomer(mu=1.0, r=2.0, alpha=0.1, frank_kappa=1e-4, n0=n0, dim=3)
+        internal = m.init_internal(npts)
+        F = F0.copy()
+        st = m.local_sweeps(F, internal, G, lam, 1.0, 0.0, None, None, {"frank_force": ff},
+                            chunk, 1e-6)
+        res, nsw, ok = m._pts_ctx.download_points()
+        out[split] = (F, internal, st, res, nsw, ok)
+    a, b = out["0"], out["1000000000"]
+    assert np.array_equal(a[0], b[0])
+    for k in a[1]:
+        assert np.array_equal(a[1][k], b[1][k]), k
+    assert np.array_equal(a[3], b[3]) and np.array_equal(a[4], b[4]) and np.array_equal(a[5], b[5])
+    assert a[2].sweeps == b[2].sweeps and a[2].converged_frac == b[2].converged_frac
