@@ -483,12 +483,19 @@ struct LceSplit {
     int *list_out, *count_out;     // deferred points (appended)
     int *count_clear;              // the counter the next round appends to
     int32_t *nsw_io;               // sweeps of this call so far (split: always)
+    int budget;                    // Newton steps a round-k >= 1 point takes (1)
     double *fsq0_io;               // |F|^2 at the start of the call (tN0)
 };
 
+// resident 64-thread blocks per SM asked of the lean round-0 kernel (no
+// elimination workspace, so only registers bound its occupancy)
+#ifndef MM_LCE_LEAN_MINB
+#define MM_LCE_LEAN_MINB 8
+#endif
+
 // slots: 0 sum res^2, 1 n_ok, 2 max nsw, 3..11 sum F
 template <int MODE>  // == LceSplit.mode, a compile-time constant
-__global__ void __launch_bounds__(LCE3_THREADS)
+__global__ void __launch_bounds__(LCE3_THREADS, MODE == 1 ? MM_LCE_LEAN_MINB : 1)
 k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ chart,
         double *__restrict__ pinc, const double *__restrict__ Gg, const double *__restrict__ Lg,
         const double *__restrict__ n0, const double *__restrict__ ffg,
@@ -548,7 +555,10 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
         double res = 0.0;
         bool converged = false;
         bool deferred = false;
-        int newton_budget = MODE == 1 ? 0 : (MODE == 2 ? 1 : 0x7fffffff);
+        // a runtime value for round k >= 1 (SP.budget = 1): a compile-time 1
+        // lets the compiler peel the first Newton step into a second copy of
+        // the step (1.8 KB of spills instead of 0.65)
+        int newton_budget = MODE == 1 ? 0 : (MODE == 2 ? SP.budget : 0x7fffffff);
         // Sweeps that only ascend the nested det multiplier (the polydomain
         // stall regime) are cheap; Newton sweeps are ~20x dearer.  Each lane
         // first runs through its cheap sweeps (inner loop) and the warp then
@@ -1171,8 +1181,9 @@ int mm_run_lce(mm_ctx *ctx, double rho, double tol, int64_t max_sweeps, int want
                 sp.count_clear = ctx->lce_cnt + (k + 2) % 3;
                 sp.nsw_io = ctx->nsw;
                 sp.fsq0_io = ctx->lce_fsq0;
-                if (k == 0)
-                    k_lce3d<1><<<blocks, threads, smem, ctx->stream>>>(
+                sp.budget = 1;
+                if (k == 0)  // round 0 has no Newton step: no elimination workspace
+                    k_lce3d<1><<<lce_blocks(M, threads), threads, 0, ctx->stream>>>(
                         ctx->F, ctx->ang, ctx->chart, ctx->pinc, ctx->G, ctx->Lam, ctx->n0,
                         ctx->ff, Fk, angk, chk, M, P, ctx->res, ctx->nsw, ctx->ok, ctx->partials,
                         ctx->red_out, ctx->red_count, sp);
