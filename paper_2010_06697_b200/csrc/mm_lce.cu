@@ -495,7 +495,7 @@ struct LceSplit {
 
 // slots: 0 sum res^2, 1 n_ok, 2 max nsw, 3..11 sum F
 template <int MODE>  // == LceSplit.mode, a compile-time constant
-__global__ void __launch_bounds__(LCE3_THREADS, MODE == 1 ? MM_LCE_LEAN_MINB : 1)
+__global__ void __launch_bounds__(LCE3_THREADS, (MODE == 1 || MODE == 4) ? MM_LCE_LEAN_MINB : 1)
 k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ chart,
         double *__restrict__ pinc, const double *__restrict__ Gg, const double *__restrict__ Lg,
         const double *__restrict__ n0, const double *__restrict__ ffg,
@@ -516,11 +516,13 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
 #if MM_LCE_STATS
     unsigned long long cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
-    if (MODE && blockIdx.x == 0 && threadIdx.x == 0) *SP.count_clear = 0;
-    const int64_t npoints = MODE == 2 ? (int64_t)*SP.count_in : M;
+    // modes 2, 3, 4 walk a list; 3 (Newton step only) appends nothing
+    constexpr bool LIST = MODE >= 2;
+    if (MODE && MODE != 3 && blockIdx.x == 0 && threadIdx.x == 0) *SP.count_clear = 0;
+    const int64_t npoints = LIST ? (int64_t)*SP.count_in : M;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < npoints;
          idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t p = MODE == 2 ? (int64_t)SP.list_in[idx] : idx;
+        const int64_t p = LIST ? (int64_t)SP.list_in[idx] : idx;
         double Fl[9], E[9];
 #pragma unroll
         for (int i = 0; i < 9; ++i) {
@@ -542,7 +544,7 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
         }
         double ph = ang[p], th = ang[M + p], pp = pinc[p];
         double fsq0 = 0.0;
-        if (MODE == 2) {
+        if (LIST) {
             fsq0 = SP.fsq0_io[p];
         } else {
 #pragma unroll
@@ -551,14 +553,15 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
         const double tF0 = 1.0 / (rho + 2.0 * mur + 2.0 * mual + 3.0 * gam + visF);
         const double tN0 = 1.0 / (P.mu * (2.0 * P.r1d + 2.0 * P.al) * fmax(fsq0, 1.0) + visn + 1e-30);
         const double base = mur + rho + visF;
-        int64_t nsw = MODE == 2 ? (int64_t)SP.nsw_io[p] : 0;
+        int64_t nsw = LIST ? (int64_t)SP.nsw_io[p] : 0;
         double res = 0.0;
         bool converged = false;
         bool deferred = false;
         // a runtime value for round k >= 1 (SP.budget = 1): a compile-time 1
         // lets the compiler peel the first Newton step into a second copy of
         // the step (1.8 KB of spills instead of 0.65)
-        int newton_budget = MODE == 1 ? 0 : (MODE == 2 ? SP.budget : 0x7fffffff);
+        int newton_budget = (MODE == 1 || MODE == 4) ? 0
+                            : (MODE == 2 || MODE == 3) ? SP.budget : 0x7fffffff;
         // Sweeps that only ascend the nested det multiplier (the polydomain
         // stall regime) are cheap; Newton sweeps are ~20x dearer.  Each lane
         // first runs through its cheap sweeps (inner loop) and the warp then
@@ -875,6 +878,7 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
                 }
                 if (pass == 1) did = true;
             }
+            if constexpr (MODE == 3) break;  // Newton step only: the lean round continues
         }
 #pragma unroll
         for (int i = 0; i < 9; ++i) {
@@ -887,6 +891,7 @@ k_lce3d(double *__restrict__ Fg, double *__restrict__ ang, double *__restrict__ 
         if (MODE) {
             SP.nsw_io[p] = (int32_t)nsw;
             if (MODE == 1) SP.fsq0_io[p] = fsq0;
+            if (MODE == 3) continue;  // mid-chunk state: the lean round (mode 4) takes it on
             if (deferred) {
                 // warp-aggregated append of the deferred points
                 const unsigned m = __activemask();
@@ -1136,7 +1141,7 @@ int mm_run_lce(mm_ctx *ctx, double rho, double tol, int64_t max_sweeps, int want
         if ((rc = mm_ensure_partials(ctx, blocks))) return rc;
         const size_t smem = sizeof(double) * 132 * LCE3_THREADS;
         if (smem > 48 * 1024) {
-            for (auto kern : {k_lce3d<0>, k_lce3d<1>, k_lce3d<2>}) {
+            for (auto kern : {k_lce3d<0>, k_lce3d<2>, k_lce3d<3>}) {
                 cudaError_t e = cudaFuncSetAttribute(
                     kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 if (e != cudaSuccess)
@@ -1171,6 +1176,8 @@ int mm_run_lce(mm_ctx *ctx, double rho, double tol, int64_t max_sweeps, int want
             // list (k + 1) % 2 and clears counter (k + 2) % 3; a round finds at most
             // one Newton step per point, so max_sweeps rounds after round 0 finish
             // every point (the empty late rounds exit at once)
+            const char *kind_env = getenv("MM_LCE_SPLIT_KIND");
+            const int kind = kind_env ? atoi(kind_env) : 3;  // 2: Newton + lean in one kernel
             for (int64_t k = 0; k <= max_sweeps; ++k) {
                 LceSplit sp;
                 sp.mode = k == 0 ? 1 : 2;
@@ -1187,11 +1194,24 @@ int mm_run_lce(mm_ctx *ctx, double rho, double tol, int64_t max_sweeps, int want
                         ctx->F, ctx->ang, ctx->chart, ctx->pinc, ctx->G, ctx->Lam, ctx->n0,
                         ctx->ff, Fk, angk, chk, M, P, ctx->res, ctx->nsw, ctx->ok, ctx->partials,
                         ctx->red_out, ctx->red_count, sp);
-                else
+                else if (kind == 2)
                     k_lce3d<2><<<blocks, threads, smem, ctx->stream>>>(
                         ctx->F, ctx->ang, ctx->chart, ctx->pinc, ctx->G, ctx->Lam, ctx->n0,
                         ctx->ff, Fk, angk, chk, M, P, ctx->res, ctx->nsw, ctx->ok, ctx->partials,
                         ctx->red_out, ctx->red_count, sp);
+                else {
+                    // the Newton step of every deferred point at 6 warps/SM (elimination
+                    // workspace), then its cheap sweeps without the workspace at 16
+                    k_lce3d<3><<<blocks, threads, smem, ctx->stream>>>(
+                        ctx->F, ctx->ang, ctx->chart, ctx->pinc, ctx->G, ctx->Lam, ctx->n0,
+                        ctx->ff, Fk, angk, chk, M, P, ctx->res, ctx->nsw, ctx->ok, ctx->partials,
+                        ctx->red_out, ctx->red_count, sp);
+                    MM_LAUNCH_CHECK(ctx);
+                    k_lce3d<4><<<lce_blocks(M, threads), threads, 0, ctx->stream>>>(
+                        ctx->F, ctx->ang, ctx->chart, ctx->pinc, ctx->G, ctx->Lam, ctx->n0,
+                        ctx->ff, Fk, angk, chk, M, P, ctx->res, ctx->nsw, ctx->ok, ctx->partials,
+                        ctx->red_out, ctx->red_count, sp);
+                }
                 MM_LAUNCH_CHECK(ctx);
             }
             const int rb = (int)std::min<int64_t>((M + 255) / 256, 148 * 8);

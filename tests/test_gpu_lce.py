@@ -173,8 +173,8 @@ def test_lce_viscous_time_step_matches_oracle():
     assert st.total_sweeps == ost.total_sweeps
 
 
-@pytest.mark.parametrize("chunk", [5, 25])
-def test_lce3d_newton_compacted_schedule_is_the_plain_loop(chunk, monkeypatch):
+@pytest.mark.parametrize("chunk,kind", [(5, "3"), (25, "3"), (25, "2")])
+def test_lce3d_newton_compacted_schedule_is_the_plain_loop(chunk, kind, monkeypatch):
     """The Newton-compacted rounds (MM_LCE_SPLIT_MIN=0 forces them) perform
     every point's sweeps exactly as the single-launch loop: fields, angles,
     chart, p_inc, per-point residuals, sweep counts and flags bit for bit;
@@ -188,6 +188,7 @@ def test_lce3d_newton_compacted_schedule_is_the_plain_loop(chunk, monkeypatch):
     lam = 1e-2 * rng.standard_normal((npts, 3, 3))
     ff = 1e-3 * rng.standard_normal((npts, 3))
     out = {}
+    monkeypatch.setenv("MM_LCE_SPLIT_KIND", kind)
     for split in ("0", "1000000000"):
         monkeypatch.setenv("MM_LCE_SPLIT_MIN", split)
         m = mm.LiquidCrystalElastomer(mu=1.0, r=2.0, alpha=0.1, frank_kappa=1e-4, n0=n0, dim=3)
