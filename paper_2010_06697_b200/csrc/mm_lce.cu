@@ -1177,7 +1177,9 @@ int mm_run_lce(mm_ctx *ctx, double rho, double tol, int64_t max_sweeps, int want
             // one Newton step per point, so max_sweeps rounds after round 0 finish
             // every point (the empty late rounds exit at once)
             const char *kind_env = getenv("MM_LCE_SPLIT_KIND");
-            const int kind = kind_env ? atoi(kind_env) : 3;  // 2: Newton + lean in one kernel
+            // 2 (default): the Newton step and the next cheap sweeps in one kernel; 3: a
+            // Newton-only kernel + a lean one (measured 10.38 vs 10.50 s at 256^3)
+            const int kind = kind_env ? atoi(kind_env) : 2;
             for (int64_t k = 0; k <= max_sweeps; ++k) {
                 LceSplit sp;
                 sp.mode = k == 0 ? 1 : 2;
