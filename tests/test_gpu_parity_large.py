@@ -201,14 +201,15 @@ def _ulp(a):
     return np.nextafter(a, np.inf)
 
 
-def test_lce_config3_subset_one_polydomain_iteration():
-    """Config 3 material on a 32^3 polydomain director field, one outer
+@pytest.mark.parametrize("n", [32, 64])
+def test_lce_config3_subset_one_polydomain_iteration(n):
+    """Config 3 material on a 32^3 and 64^3 polydomain director field, one outer
     iteration at max_local 5 (below the roundoff-amplification horizon of
     non-converging Newton points), against the oracle.  Bar:
     1e-10, or within 3x the oracle's own drift when its initial F moves by
     one ulp (the Newton steps of points far from convergence amplify
-    roundoff, and CUDA's sin/cos differ from glibc's by an ulp)."""
-    n = 32
+    roundoff, and CUDA's sin/cos differ from glibc's by an ulp).  At 64^3
+    (262144 points) the local step runs the Newton-compacted rounds."""
     grid, n0, kw = _lce_problem(n)
     m = mm.LiquidCrystalElastomer(**kw)
     om = oracle.LCE(**kw)
@@ -234,7 +235,7 @@ def test_lce_config3_subset_one_polydomain_iteration():
     pairs += [(k, st.internal[k], ost.internal[k], oenv.internal[k]) for k in ("angles", "chart")]
     for k, a, b, c in pairs:
         e, env = rel_l2(a, b), rel_l2(c, b)
-        print(f"LCE 32^3 one iteration {k}: ours-vs-oracle {e:.3e}, oracle 1-ulp drift {env:.3e}")
+        print(f"LCE {n}^3 one iteration {k}: ours-vs-oracle {e:.3e}, oracle 1-ulp drift {env:.3e}")
         assert e < max(1e-10, 3.0 * env), k
 
 
