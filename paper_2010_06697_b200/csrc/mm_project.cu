@@ -597,31 +597,25 @@ k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho
             const int x0 = 2 * m, x1 = 2 * m + 1;
             const int xm = (x0 == 0) ? n - 1 : x0 - 1;
             const int xp = (x1 + 1 == n) ? 0 : x1 + 1;
-            // the point pair (x0, x1 = x0 + 1) of a slot is 16-byte aligned
-            // (x0 even, rows start at multiples of n): one LDG.128 per pair
-            auto ld2 = [](const double *a, int64_t o) {
-                return __ldg(reinterpret_cast<const double2 *>(a + o));
-            };
 #pragma unroll
             for (int c = 0; c < DIM; ++c) {
                 const int64_t cz = (int64_t)(c * DIM) * M;                  // T_c0 (axis 0)
                 const int64_t cy = (int64_t)(c * DIM + 1) * M;              // T_c1 (axis 1, 3D)
                 const int64_t cx = (int64_t)(c * DIM + DIM - 1) * M + nb.self;  // contiguous
-                const double2 z2 = make_double2(0.0, 0.0);
                 const double fxm = __ldg(&F[cx + xm]), lxm = HAS_L ? __ldg(&L[cx + xm]) : 0.0;
-                const double2 fx = ld2(F, cx + x0), lx = HAS_L ? ld2(L, cx + x0) : z2;
-                const double fx0 = fx.x, lx0 = lx.x, fx1 = fx.y, lx1 = lx.y;
+                const double fx0 = __ldg(&F[cx + x0]), lx0 = HAS_L ? __ldg(&L[cx + x0]) : 0.0;
+                const double fx1 = __ldg(&F[cx + x1]), lx1 = HAS_L ? __ldg(&L[cx + x1]) : 0.0;
                 const double fxp = __ldg(&F[cx + xp]), lxp = HAS_L ? __ldg(&L[cx + xp]) : 0.0;
-                const double2 fzp = ld2(F, cz + nb.zp + x0), lzp = HAS_L ? ld2(L, cz + nb.zp + x0) : z2;
-                const double2 fzm = ld2(F, cz + nb.zm + x0), lzm = HAS_L ? ld2(L, cz + nb.zm + x0) : z2;
-                const double fzp0 = fzp.x, lzp0 = lzp.x, fzp1 = fzp.y, lzp1 = lzp.y;
-                const double fzm0 = fzm.x, lzm0 = lzm.x, fzm1 = fzm.y, lzm1 = lzm.y;
+                const double fzp0 = __ldg(&F[cz + nb.zp + x0]), lzp0 = HAS_L ? __ldg(&L[cz + nb.zp + x0]) : 0.0;
+                const double fzp1 = __ldg(&F[cz + nb.zp + x1]), lzp1 = HAS_L ? __ldg(&L[cz + nb.zp + x1]) : 0.0;
+                const double fzm0 = __ldg(&F[cz + nb.zm + x0]), lzm0 = HAS_L ? __ldg(&L[cz + nb.zm + x0]) : 0.0;
+                const double fzm1 = __ldg(&F[cz + nb.zm + x1]), lzm1 = HAS_L ? __ldg(&L[cz + nb.zm + x1]) : 0.0;
                 double y0 = 0.0, y1 = 0.0;
                 if (DIM == 3) {
-                    const double2 fyp = ld2(F, cy + nb.yp + x0), lyp = HAS_L ? ld2(L, cy + nb.yp + x0) : z2;
-                    const double2 fym = ld2(F, cy + nb.ym + x0), lym = HAS_L ? ld2(L, cy + nb.ym + x0) : z2;
-                    const double fyp0 = fyp.x, lyp0 = lyp.x, fyp1 = fyp.y, lyp1 = lyp.y;
-                    const double fym0 = fym.x, lym0 = lym.x, fym1 = fym.y, lym1 = lym.y;
+                    const double fyp0 = __ldg(&F[cy + nb.yp + x0]), lyp0 = HAS_L ? __ldg(&L[cy + nb.yp + x0]) : 0.0;
+                    const double fyp1 = __ldg(&F[cy + nb.yp + x1]), lyp1 = HAS_L ? __ldg(&L[cy + nb.yp + x1]) : 0.0;
+                    const double fym0 = __ldg(&F[cy + nb.ym + x0]), lym0 = HAS_L ? __ldg(&L[cy + nb.ym + x0]) : 0.0;
+                    const double fym1 = __ldg(&F[cy + nb.ym + x1]), lym1 = HAS_L ? __ldg(&L[cy + nb.ym + x1]) : 0.0;
                     y0 = (fyp0 - lyp0 * irho) - (fym0 - lym0 * irho);
                     y1 = (fyp1 - lyp1 * irho) - (fym1 - lym1 * irho);
                 }
