@@ -52,7 +52,7 @@ def main():
     n = int(sys.argv[4]) if len(sys.argv) > 4 else 256
     alg = bench.stage_bytes(n)
     rows = raw_rows(rep)
-    lines = [f"# ncu summary, grid {n}^3, config-2 laminate (bench.py --steps 3 --warmup 3)", "",
+    lines = [f"# ncu summary, grid {n}^3, config-2 laminate (bench.py --steps 8 --warmup 3; launch list --steps 3)", "",
              "Full capture (`--set full --clock-control none`), one launch per stage kernel:", "",
              "| kernel | stage | us | DRAM read MB | DRAM write MB | traffic / alg. bytes | DRAM % "
              "| SM % | warps active % | FP64 pipe % | regs |",
