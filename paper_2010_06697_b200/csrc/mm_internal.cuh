@@ -1,6 +1,8 @@
 // Internal definitions shared by the CUDA translation units of libmm_admm.
 #pragma once
 
+#include <cuda.h>          // CUtensorMap (TMA descriptors; encoded through the runtime's driver entry point)
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -116,6 +118,11 @@ struct mm_ctx {
     int64_t uM = 0, dM = 0;
     // Newton-compacted 3D LCE schedule (mm_lce.cu): |F|^2 at call start,
     // two deferred-point lists and three rotating counters
+    // TMA descriptor of the plane-layout spectrum (mm_project.cu plane_col_tma)
+    CUtensorMap tmap{};
+    bool tmap_ok = false;
+    const void *tmap_src = nullptr;
+    int tmap_n = 0;
     double *lce_fsq0 = nullptr;
     int *lce_list[2] = {nullptr, nullptr};
     int *lce_cnt = nullptr;

@@ -233,9 +233,9 @@ __device__ __forceinline__ void fft_reg_rt(double2 (&v)[R], bool inv) {
 // shared-memory round trip and two barriers fewer per transform, 168
 // registers, half the threads per tile; the plane pass default: 0.805 ->
 // 0.714 ms at 256^3).
-template <int N, int TK, int R, int NS, int PPT = 8>
+template <int N, int TK, int R, int NS, int PPT = 8, int LDX = TK + 1>
 __device__ __forceinline__ void stockham_pass(double2 *buf, const double2 *__restrict__ tw, bool inv) {
-    constexpr int LD = TK + 1, NB = PPT / R, JS = N / PPT;
+    constexpr int LD = LDX, NB = PPT / R, JS = N / PPT;
     const int c = threadIdx.x % TK, q = threadIdx.x / TK;
     double2 v[NB][R];
     // MM_TW_PROD (R = 16, one butterfly per thread): the twiddles W^{jm r}
@@ -291,13 +291,14 @@ __device__ __forceinline__ void stockham_pass(double2 *buf, const double2 *__res
 }
 
 // radix plan: N = 8 * 8 * 4 (256), 8 * 4 * 4 (128), 8 * 8 (64), 8 * 4 (32), 4 * 4 (16)
-template <int N, int TK, int PPT = 8>
+template <int N, int TK, int PPT = 8, int LDX = TK + 1>
 __device__ __forceinline__ void tile_fft_s(double2 *buf, const double2 *__restrict__ tw, bool inv) {
     static_assert(N >= 16 && N <= 256 && (N & (N - 1)) == 0, "N in 16..256, power of two");
+    static_assert(PPT == 16 || LDX == TK + 1, "a dense (TMA) tile layout needs PPT = 16");
     if constexpr (PPT == 16) {
         // 16 points per thread: radix-16 first pass, then the remaining factor
-        stockham_pass<N, TK, 16, 1, 16>(buf, tw, inv);
-        if constexpr (N > 16) stockham_pass<N, TK, N / 16, 16, 16>(buf, tw, inv);
+        stockham_pass<N, TK, 16, 1, 16, LDX>(buf, tw, inv);
+        if constexpr (N > 16) stockham_pass<N, TK, N / 16, 16, 16, LDX>(buf, tw, inv);
     } else if constexpr (N == 256) {
         stockham_pass<N, TK, 8, 1>(buf, tw, inv);
         stockham_pass<N, TK, 8, 8>(buf, tw, inv);
@@ -1219,20 +1220,154 @@ __device__ __forceinline__ void plane_pass(double2 *__restrict__ pl, double2 *sm
     cp_async_wait<0>();
 }
 
+// ---- TMA (cp.async.bulk.tensor) + mbarrier helpers -------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+// bounded wait on an mbarrier phase: a descriptor error would otherwise hang
+// the GPU; 2^24 probes is ~a second, far beyond any tile
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t ok = 0;
+    for (uint32_t it = 0; !ok; ++it) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (it > (1u << 24)) __trap();
+    }
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                            int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, const void *src, int x, int y,
+                                             int z) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(map),
+                 "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// Pass 2 of the plane (FFT along axis 0, solve, inverse) with TMA: a tile of
+// TK columns x N rows is one cp.async.bulk.tensor load into a dense
+// [row][column] shared-memory tile (the line-interleaved layout the Stockham
+// FFT wants, no padding needed: 8 consecutive 16-byte elements fill the 32
+// banks), completion on an mbarrier (expect_tx); the result goes back with a
+// TMA store.  Double-buffered: thread 0 issues tile t+1's load while the
+// CTA transforms tile t, after the previous store from that buffer has read
+// its shared memory.
+template <int N1, int N2, int TK>
+__device__ __forceinline__ void plane_col_tma(const CUtensorMap *map, int plane, double2 *smem,
+                                              uint64_t *bars, int t0, int t1,
+                                              const PlaneGeom &g, int k2,
+                                              const double2 *__restrict__ tw) {
+    using C = PlaneCfg<N1, N2, TK>;
+    constexpr int N = C::N, NT = C::NT, IT = C::IT, LD = TK;
+    constexpr uint32_t BYTES = (uint32_t)(N * TK * sizeof(double2));
+    const int tx = threadIdx.x;
+    double2 *buf[2] = {smem, smem + N * (TK + 1)};  // 128-byte aligned offsets
+    if (tx == 0 && t0 < t1) {
+        mbar_expect_tx(&bars[0], BYTES);
+        tma_load_3d(buf[0], map, &bars[0], 2 * t0 * TK, 0, plane);
+    }
+    uint32_t phase[2] = {0u, 0u};
+#pragma unroll 1
+    for (int t = t0, i = 0; t < t1; ++t, ++i) {
+        const int b = i & 1;
+        if (tx == 0 && t + 1 < t1) {
+            bulk_wait_read0();  // the store of tile t-1 has read buffer 1-b
+            mbar_expect_tx(&bars[1 - b], BYTES);
+            tma_load_3d(buf[1 - b], map, &bars[1 - b], 2 * (t + 1) * TK, 0, plane);
+        }
+        double s0v[IT];
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int w = it * NT + tx;
+            s0v[it] = w < N * TK ? __ldg(&g.sym[w / TK]) : 0.0;
+        }
+        const double s1v = __ldg(&g.sym[N + t * TK + tx % TK]);
+        mbar_wait(&bars[b], phase[b]);
+        phase[b] ^= 1u;
+        double2 *bf = buf[b];
+        tile_fft_s<N, TK, C::PPT, LD>(bf, tw, false);
+        const double sl = __ldg(&g.sym[2 * N + k2]);
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int w = it * NT + tx;
+            if (w < N * TK) {
+                const int kl = w / TK, c = w % TK;
+                double gsq = s0v[it];
+                gsq = gsq + s1v;
+                gsq = gsq + sl;
+                const double inv = (gsq > g.thresh) ? 1.0 / gsq : 0.0;
+                bf[kl * LD + c] = cscale(bf[kl * LD + c], -inv * g.scale);
+            }
+        }
+        __syncthreads();
+        tile_fft_s<N, TK, C::PPT, LD>(bf, tw, true);
+        fence_proxy_async();  // this thread's shared-memory writes -> the async proxy
+        __syncthreads();
+        if (tx == 0) {
+            tma_store_3d(map, bf, 2 * t * TK, 0, plane);
+            bulk_commit();
+        }
+    }
+    if (tx == 0) bulk_wait0();  // the stores are performed before the cluster barrier
+    __syncthreads();
+}
+
 template <int N1, int N2, int TK, int CS>
 __global__ void __cluster_dims__(CS, 1, 1)
     __launch_bounds__(PlaneCfg<N1, N2, TK>::NT, PlaneCfg<N1, N2, TK>::MINB)
-k_plane(double2 *__restrict__ spec, PlaneGeom g, const double2 *__restrict__ tw) {
+k_plane(double2 *__restrict__ spec, PlaneGeom g, const double2 *__restrict__ tw,
+        const __grid_constant__ CUtensorMap tmap, int use_tma) {
     constexpr int N = N1 * N2;
     constexpr int PER = N / TK / CS;  // tiles per CTA per pass
-    extern __shared__ double2 smem_c[];
+    extern __shared__ __align__(128) double2 smem_c[];
     const int plane = blockIdx.x / CS;  // c * nh + k2
     const int r = blockIdx.x % CS;      // rank in the cluster
     const int k2 = plane % g.nh;
     double2 *pl = spec + (int64_t)plane * N * N;
     plane_pass<N1, N2, TK, PL_ROW_FWD>(pl, smem_c, r * PER, (r + 1) * PER, g, k2, tw);
     cluster_barrier();
-    plane_pass<N1, N2, TK, PL_COL_SOLVE>(pl, smem_c, r * PER, (r + 1) * PER, g, k2, tw);
+    if constexpr (PlaneCfg<N1, N2, TK>::PPT == 16) {
+        if (use_tma) {
+            __shared__ __align__(8) uint64_t bars[2];
+            if (threadIdx.x == 0) {
+                mbar_init(&bars[0], 1);
+                mbar_init(&bars[1], 1);
+                asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+            }
+            __syncthreads();
+            plane_col_tma<N1, N2, TK>(&tmap, plane, smem_c, bars, r * PER, (r + 1) * PER, g, k2,
+                                      tw);
+        } else {
+            plane_pass<N1, N2, TK, PL_COL_SOLVE>(pl, smem_c, r * PER, (r + 1) * PER, g, k2, tw);
+        }
+    } else {
+        plane_pass<N1, N2, TK, PL_COL_SOLVE>(pl, smem_c, r * PER, (r + 1) * PER, g, k2, tw);
+    }
     cluster_barrier();
     plane_pass<N1, N2, TK, PL_ROW_INV>(pl, smem_c, r * PER, (r + 1) * PER, g, k2, tw);
 }
@@ -1343,7 +1478,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(NTH, MM_PLANE_HW_MI
 k_plane_hw(double2 *__restrict__ spec, PlaneGeom g, const double2 *__restrict__ tw) {
     constexpr int N = 256, NSLOT = NTH / 16, LPC = N / CS;
     static_assert(LPC % NSLOT == 0, "lines per CTA divide among the slots");
-    extern __shared__ double2 smem_c[];
+    extern __shared__ __align__(128) double2 smem_c[];
     const int plane = blockIdx.x / CS;  // c * nh + k2
     const int r = blockIdx.x % CS;      // rank in the cluster
     const int k2 = plane % g.nh;
@@ -1790,6 +1925,43 @@ int run_col(mm_ctx *ctx, const ColGeom &g, int n_outer) {
     }
 }
 
+#ifndef MM_PLANE_TMA  // pass 2 of the plane FFT through TMA + mbarrier (plane_col_tma)
+#define MM_PLANE_TMA 1
+#endif
+
+// Tensor map of the plane-layout spectrum for plane_col_tma: doubles, dims
+// {2N (re/im along axis 1), N (axis 0), planes}, box {2 TK, N, 1}.  Encoded
+// once per context through the driver entry point (no libcuda link).
+int mm_plane_tensor_map(mm_ctx *ctx, int N, int TK) {
+    if (ctx->tmap_ok && ctx->tmap_src == ctx->spec && ctx->tmap_n == N) return MM_OK;
+    ctx->tmap_ok = false;
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn) {
+            cudaGetLastError();
+            return MM_OK;  // no TMA: plane_pass's cp.async path
+        }
+        encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    const cuuint64_t dims[3] = {(cuuint64_t)2 * N, (cuuint64_t)N,
+                                (cuuint64_t)ctx->dim * (cuuint64_t)ctx->nh};
+    const cuuint64_t strides[2] = {(cuuint64_t)N * 16, (cuuint64_t)N * N * 16};
+    const cuuint32_t box[3] = {(cuuint32_t)(2 * TK), (cuuint32_t)N, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode(&ctx->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, ctx->spec, dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return mm_fail(ctx, MM_ERR_CUDA, "cuTensorMapEncodeTiled: %d", (int)r);
+    ctx->tmap_ok = true;
+    ctx->tmap_src = ctx->spec;
+    ctx->tmap_n = N;
+    return MM_OK;
+}
+
 template <int N1, int N2, int TK, int CS>
 int run_plane_t(mm_ctx *ctx, const PlaneGeom &g) {
     using C = PlaneCfg<N1, N2, TK>;
@@ -1803,7 +1975,12 @@ int run_plane_t(mm_ctx *ctx, const PlaneGeom &g) {
             return mm_fail(ctx, MM_ERR_CUDA, "cluster size %d: %s", CS, cudaGetErrorString(e));
     }
     const int blocks = CS * ctx->dim * g.nh;
-    kern<<<blocks, C::NT, smem, ctx->stream>>>(ctx->spec, g, ctx->tw_full);
+    int use_tma = 0;
+    if (C::PPT == 16 && MM_PLANE_TMA) {
+        if ((rc = mm_plane_tensor_map(ctx, C::N, TK))) return rc;
+        use_tma = ctx->tmap_ok ? 1 : 0;
+    }
+    kern<<<blocks, C::NT, smem, ctx->stream>>>(ctx->spec, g, ctx->tw_full, ctx->tmap, use_tma);
     MM_LAUNCH_CHECK(ctx);
     return MM_OK;
 }
