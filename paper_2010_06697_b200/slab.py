@@ -174,7 +174,7 @@ class TorchComm:
                     b.copy_(a)
             return
         self._host_ready(list(to_lower) + list(to_upper))
-        stage = not self.stream_ordered and to_lower and to_lower[0].is_cuda
+        stage = bool(not self.stream_ordered and to_lower and to_lower[0].is_cuda)
         send_lo = [a.cpu() if stage else a.contiguous() for a in to_lower]
         send_hi = [a.cpu() if stage else a.contiguous() for a in to_upper]
         rx_hi = [torch.empty_like(s) for s in send_lo] if stage else list(from_upper)
@@ -245,11 +245,13 @@ class TorchComm:
         if self.P == 1:
             return v.copy()
         if self.stream_ordered:
-            t = torch.as_tensor(v).to(torch.device("cuda", self.device))
-            parts = [torch.empty_like(t) for _ in range(self.P)]
+            # every step on the library stream: the upload, the gather and the
+            # read-back are ordered with each other and with the library's work
             with self._stream():
+                t = torch.as_tensor(v).to(torch.device("cuda", self.device))
+                parts = [torch.empty_like(t) for _ in range(self.P)]
                 self.dist.all_gather(parts, t)
-            arr = np.stack([p.cpu().numpy() for p in parts])
+                arr = np.stack([p.cpu().numpy() for p in parts])
         else:
             t = torch.as_tensor(v)
             parts = [torch.empty_like(t) for _ in range(self.P)]
