@@ -160,6 +160,13 @@ class TorchComm:
             if self._sync is not None:
                 self._sync()
 
+    def _host_done(self, tensors):
+        """A host-side exchange wrote device buffers on torch's stream: finish
+        it before the library stream reads them."""
+        if not self.stream_ordered and any(getattr(t, "is_cuda", False) for t in tensors):
+            import torch
+            torch.cuda.synchronize(self.device)
+
     def neighbor_exchange(self, to_lower, to_upper, from_upper, from_lower):
         """to_lower[i] -> the lower neighbour's from_upper[i]; to_upper[i] ->
         the upper neighbour's from_lower[i] (periodic ring of ranks)."""
@@ -167,11 +174,13 @@ class TorchComm:
         dist = self.dist
         lo, hi = (self.rank - 1) % self.P, (self.rank + 1) % self.P
         if self.P == 1:
+            self._host_ready(list(to_lower) + list(to_upper))
             with self._stream():
                 for a, b in zip(to_lower, from_upper):
                     b.copy_(a)
                 for a, b in zip(to_upper, from_lower):
                     b.copy_(a)
+            self._host_done(list(from_upper) + list(from_lower))
             return
         self._host_ready(list(to_lower) + list(to_upper))
         stage = bool(not self.stream_ordered and to_lower and to_lower[0].is_cuda)
@@ -198,8 +207,10 @@ class TorchComm:
         recv comes from rank s."""
         import torch
         if self.P == 1:
+            self._host_ready([send])
             with self._stream():
                 recv.copy_(send)
+            self._host_done([recv])
             return
         self._host_ready([send])
         if not self.stream_ordered and send.is_cuda:
