@@ -119,8 +119,8 @@ struct mm_ctx {
     // Newton-compacted 3D LCE schedule (mm_lce.cu): |F|^2 at call start,
     // two deferred-point lists and three rotating counters
     // TMA descriptor of the plane-layout spectrum (mm_project.cu plane_col_tma)
-    CUtensorMap tmap{};
-    bool tmap_ok = false;
+    CUtensorMap tmap{}, rmap{};
+    bool tmap_ok = false, rmap_ok = false;
     const void *tmap_src = nullptr;
     int tmap_n = 0;
     double *lce_fsq0 = nullptr;

@@ -1260,6 +1260,20 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, const void 
                  "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
                  : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                            int x, int y, int z, int w) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap *map, const void *src, int x, int y,
+                                             int z, int w) {
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];\n" ::"l"(map),
+                 "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(src))
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() {
     asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
@@ -1279,8 +1293,8 @@ __device__ __forceinline__ void fence_proxy_async() {
 // its shared memory.
 template <int N1, int N2, int TK>
 __device__ __forceinline__ void plane_col_tma(const CUtensorMap *map, int plane, double2 *smem,
-                                              uint64_t *bars, int t0, int t1,
-                                              const PlaneGeom &g, int k2,
+                                              uint64_t *bars, uint32_t (&phase)[2], int t0,
+                                              int t1, const PlaneGeom &g, int k2,
                                               const double2 *__restrict__ tw) {
     using C = PlaneCfg<N1, N2, TK>;
     constexpr int N = C::N, NT = C::NT, IT = C::IT, LD = TK;
@@ -1288,10 +1302,10 @@ __device__ __forceinline__ void plane_col_tma(const CUtensorMap *map, int plane,
     const int tx = threadIdx.x;
     double2 *buf[2] = {smem, smem + N * (TK + 1)};  // 128-byte aligned offsets
     if (tx == 0 && t0 < t1) {
+        bulk_wait_read0();
         mbar_expect_tx(&bars[0], BYTES);
         tma_load_3d(buf[0], map, &bars[0], 2 * t0 * TK, 0, plane);
     }
-    uint32_t phase[2] = {0u, 0u};
 #pragma unroll 1
     for (int t = t0, i = 0; t < t1; ++t, ++i) {
         const int b = i & 1;
@@ -1337,11 +1351,86 @@ __device__ __forceinline__ void plane_col_tma(const CUtensorMap *map, int plane,
     __syncthreads();
 }
 
+// 256-point FFT of the lines of a dense line-major tile (element n of line c
+// at buf[c * 256 + n], the TMA layout of a row tile): 16 lanes per line, two
+// radix-16 stages in registers; stage 1 writes an XOR-swizzled transpose
+// (slot 16 a + (b ^ a)), stage 2 reads it and writes natural order back, so
+// every exchange is conflict-free and synchronised within the warp only.
+__device__ __forceinline__ int lm_swz(int a, int b) { return 16 * a + (b ^ a); }
+
+__device__ __forceinline__ void tile_fft_lm256(double2 *buf, const double2 *__restrict__ tw,
+                                               bool inv) {
+    const int c = threadIdx.x >> 4, q = threadIdx.x & 15;
+    double2 *L = buf + c * 256;
+    double2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = L[q + 16 * r];
+    __syncwarp();
+    fft_reg_rt<16>(v, inv);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) L[lm_swz(q, r)] = v[r];
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = L[lm_swz(r, q)];
+    __syncwarp();
+#pragma unroll
+    for (int r = 1; r < 16; ++r) {
+        double2 w = __ldg(&tw[q * r]);
+        if (inv) w.y = -w.y;
+        v[r] = cmul(v[r], w);
+    }
+    fft_reg_rt<16>(v, inv);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) L[q + 16 * r] = v[r];
+    __syncwarp();
+}
+
+// Passes 1 and 3 of the plane (FFT along axis 1) with TMA, n = 256: a tile
+// of TK rows is one 4D cp.async.bulk.tensor load (rows are contiguous: box
+// {256 doubles, 2 halves, TK rows, 1 plane}) into a dense line-major tile,
+// transformed by tile_fft_lm256, stored back by TMA; double-buffered as
+// plane_col_tma.
+template <int TK>
+__device__ __forceinline__ void plane_row_tma(const CUtensorMap *map, int plane, double2 *smem,
+                                              uint64_t *bars, uint32_t (&phase)[2], int t0,
+                                              int t1, const double2 *__restrict__ tw, bool inv) {
+    constexpr int N = 256;
+    constexpr uint32_t BYTES = (uint32_t)(N * TK * sizeof(double2));
+    const int tx = threadIdx.x;
+    double2 *buf[2] = {smem, smem + N * (TK + 1)};
+    if (tx == 0 && t0 < t1) {
+        bulk_wait_read0();
+        mbar_expect_tx(&bars[0], BYTES);
+        tma_load_4d(buf[0], map, &bars[0], 0, 0, t0 * TK, plane);
+    }
+#pragma unroll 1
+    for (int t = t0, i = 0; t < t1; ++t, ++i) {
+        const int b = i & 1;
+        if (tx == 0 && t + 1 < t1) {
+            bulk_wait_read0();
+            mbar_expect_tx(&bars[1 - b], BYTES);
+            tma_load_4d(buf[1 - b], map, &bars[1 - b], 0, 0, (t + 1) * TK, plane);
+        }
+        mbar_wait(&bars[b], phase[b]);
+        phase[b] ^= 1u;
+        tile_fft_lm256(buf[b], tw, inv);
+        fence_proxy_async();
+        __syncthreads();
+        if (tx == 0) {
+            tma_store_4d(map, buf[b], 0, 0, t * TK, plane);
+            bulk_commit();
+        }
+    }
+    if (tx == 0) bulk_wait0();
+    __syncthreads();
+}
+
 template <int N1, int N2, int TK, int CS>
 __global__ void __cluster_dims__(CS, 1, 1)
     __launch_bounds__(PlaneCfg<N1, N2, TK>::NT, PlaneCfg<N1, N2, TK>::MINB)
 k_plane(double2 *__restrict__ spec, PlaneGeom g, const double2 *__restrict__ tw,
-        const __grid_constant__ CUtensorMap tmap, int use_tma) {
+        const __grid_constant__ CUtensorMap tmap, int use_tma,
+        const __grid_constant__ CUtensorMap rmap) {
     constexpr int N = N1 * N2;
     constexpr int PER = N / TK / CS;  // tiles per CTA per pass
     extern __shared__ __align__(128) double2 smem_c[];
@@ -1349,19 +1438,29 @@ k_plane(double2 *__restrict__ spec, PlaneGeom g, const double2 *__restrict__ tw,
     const int r = blockIdx.x % CS;      // rank in the cluster
     const int k2 = plane % g.nh;
     double2 *pl = spec + (int64_t)plane * N * N;
-    plane_pass<N1, N2, TK, PL_ROW_FWD>(pl, smem_c, r * PER, (r + 1) * PER, g, k2, tw);
+    // use_tma: 1 = the column pass through TMA, 2 = the row passes too
+    // (n = 256, 8-row tiles, 128 threads: 16 lanes per row)
+    constexpr bool ROWTMA = N1 * N2 == 256 && TK == 8 && PlaneCfg<N1, N2, TK>::NT == 128;
+    constexpr bool COLTMA = PlaneCfg<N1, N2, TK>::PPT == 16;
+    __shared__ __align__(8) uint64_t bars[2];
+    uint32_t phase[2] = {0u, 0u};
+    if ((COLTMA || ROWTMA) && use_tma) {
+        if (threadIdx.x == 0) {
+            mbar_init(&bars[0], 1);
+            mbar_init(&bars[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+    }
+    if (ROWTMA && use_tma == 2)
+        plane_row_tma<TK>(&rmap, plane, smem_c, bars, phase, r * PER, (r + 1) * PER, tw, false);
+    else
+        plane_pass<N1, N2, TK, PL_ROW_FWD>(pl, smem_c, r * PER, (r + 1) * PER, g, k2, tw);
     cluster_barrier();
-    if constexpr (PlaneCfg<N1, N2, TK>::PPT == 16) {
+    if constexpr (COLTMA) {
         if (use_tma) {
-            __shared__ __align__(8) uint64_t bars[2];
-            if (threadIdx.x == 0) {
-                mbar_init(&bars[0], 1);
-                mbar_init(&bars[1], 1);
-                asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-            }
-            __syncthreads();
-            plane_col_tma<N1, N2, TK>(&tmap, plane, smem_c, bars, r * PER, (r + 1) * PER, g, k2,
-                                      tw);
+            plane_col_tma<N1, N2, TK>(&tmap, plane, smem_c, bars, phase, r * PER, (r + 1) * PER,
+                                      g, k2, tw);
         } else {
             plane_pass<N1, N2, TK, PL_COL_SOLVE>(pl, smem_c, r * PER, (r + 1) * PER, g, k2, tw);
         }
@@ -1369,7 +1468,10 @@ k_plane(double2 *__restrict__ spec, PlaneGeom g, const double2 *__restrict__ tw,
         plane_pass<N1, N2, TK, PL_COL_SOLVE>(pl, smem_c, r * PER, (r + 1) * PER, g, k2, tw);
     }
     cluster_barrier();
-    plane_pass<N1, N2, TK, PL_ROW_INV>(pl, smem_c, r * PER, (r + 1) * PER, g, k2, tw);
+    if (ROWTMA && use_tma == 2)
+        plane_row_tma<TK>(&rmap, plane, smem_c, bars, phase, r * PER, (r + 1) * PER, tw, true);
+    else
+        plane_pass<N1, N2, TK, PL_ROW_INV>(pl, smem_c, r * PER, (r + 1) * PER, g, k2, tw);
 }
 
 // ---------------------------------------------------------------------------
@@ -1925,8 +2027,8 @@ int run_col(mm_ctx *ctx, const ColGeom &g, int n_outer) {
     }
 }
 
-#ifndef MM_PLANE_TMA  // pass 2 of the plane FFT through TMA + mbarrier (plane_col_tma)
-#define MM_PLANE_TMA 1
+#ifndef MM_PLANE_TMA  // 1: pass 2 of the plane FFT through TMA + mbarrier (plane_col_tma);
+#define MM_PLANE_TMA 2  // 2: passes 1 and 3 too at n = 256 (plane_row_tma)
 #endif
 
 // Tensor map of the plane-layout spectrum for plane_col_tma: doubles, dims
@@ -1956,6 +2058,21 @@ int mm_plane_tensor_map(mm_ctx *ctx, int N, int TK) {
                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return mm_fail(ctx, MM_ERR_CUDA, "cuTensorMapEncodeTiled: %d", (int)r);
+    // row tiles (passes 1 and 3, n = 256): doubles {256 (half a row), 2 halves,
+    // N rows, planes}, box {256, 2, TK, 1}: TK whole rows, dense
+    ctx->rmap_ok = false;
+    if (N == 256) {
+        const cuuint64_t rd[4] = {256, 2, (cuuint64_t)N, dims[2]};
+        const cuuint64_t rs[3] = {256 * 8, (cuuint64_t)N * 16, (cuuint64_t)N * N * 16};
+        const cuuint32_t rb[4] = {256, 2, (cuuint32_t)TK, 1};
+        const cuuint32_t re[4] = {1, 1, 1, 1};
+        r = encode(&ctx->rmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ctx->spec, rd, rs, rb, re,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            return mm_fail(ctx, MM_ERR_CUDA, "cuTensorMapEncodeTiled (rows): %d", (int)r);
+        ctx->rmap_ok = true;
+    }
     ctx->tmap_ok = true;
     ctx->tmap_src = ctx->spec;
     ctx->tmap_n = N;
@@ -1979,8 +2096,12 @@ int run_plane_t(mm_ctx *ctx, const PlaneGeom &g) {
     if (C::PPT == 16 && MM_PLANE_TMA) {
         if ((rc = mm_plane_tensor_map(ctx, C::N, TK))) return rc;
         use_tma = ctx->tmap_ok ? 1 : 0;
+        if (use_tma && MM_PLANE_TMA >= 2 && C::N == 256 && TK == 8 && C::NT == 128 &&
+            ctx->rmap_ok)
+            use_tma = 2;
     }
-    kern<<<blocks, C::NT, smem, ctx->stream>>>(ctx->spec, g, ctx->tw_full, ctx->tmap, use_tma);
+    kern<<<blocks, C::NT, smem, ctx->stream>>>(ctx->spec, g, ctx->tw_full, ctx->tmap, use_tma,
+                                               ctx->rmap);
     MM_LAUNCH_CHECK(ctx);
     return MM_OK;
 }
