@@ -1283,6 +1283,66 @@ __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
+// Column tiles (pass 2, n = 256) through TMA with the hardware 128-byte
+// swizzle: element n of column c of an 8-column tile sits at complex slot
+// n * 8 + (c ^ (n & 7)).  16 lanes own one column; the in-warp radix-16 x 16
+// FFT keeps its intermediate at row rho(i) = i ^ ((i >> 4) & 7), which makes
+// both the transposed write (y[16 q + r]) and the strided read (x[q + 16 r])
+// hit eight distinct 16-byte bank groups.  The forward transform's output is
+// in natural order in registers, so the solve and the first stage of the
+// inverse run without a shared-memory round trip.
+__device__ __forceinline__ int csw(int row, int c) { return row * 8 + (c ^ (row & 7)); }
+__device__ __forceinline__ int crho(int i) { return i ^ ((i >> 4) & 7); }
+
+__device__ __forceinline__ void col_fft_solve_256(double2 *buf, const double2 *__restrict__ tw,
+                                                  const PlaneGeom &g, int col, int k2) {
+    const int c = threadIdx.x >> 4, q = threadIdx.x & 15;
+    double2 v[16];
+    const double s1 = __ldg(&g.sym[256 + col]);
+    const double sl = __ldg(&g.sym[2 * 256 + k2]);
+    // forward, stage 1: x[q + 16 r] -> y[16 q + r]
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = buf[csw(q + 16 * r, c)];
+    __syncwarp();
+    fft_reg_rt<16>(v, false);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) buf[csw(crho(16 * q + r), c)] = v[r];
+    __syncwarp();
+    // forward, stage 2: twiddle W^{q r}, natural order out (element q + 16 r)
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = buf[csw(crho(q + 16 * r), c)];
+#pragma unroll
+    for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], __ldg(&tw[q * r]));
+    fft_reg_rt<16>(v, false);
+    // solve (k_col<COL_SOLVE>'s expression and summation order) on element q + 16 r
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        double gsq = __ldg(&g.sym[q + 16 * r]);
+        gsq = gsq + s1;
+        gsq = gsq + sl;
+        const double inv = (gsq > g.thresh) ? 1.0 / gsq : 0.0;
+        v[r] = cscale(v[r], -inv * g.scale);
+    }
+    // inverse, stage 1 straight from registers: x[q + 16 r] = v[r]
+    fft_reg_rt<16>(v, true);
+    __syncwarp();  // every lane is done reading the forward intermediate
+#pragma unroll
+    for (int r = 0; r < 16; ++r) buf[csw(crho(16 * q + r), c)] = v[r];
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = buf[csw(crho(q + 16 * r), c)];
+#pragma unroll
+    for (int r = 1; r < 16; ++r) {
+        const double2 w = __ldg(&tw[q * r]);
+        v[r] = cmul(v[r], make_double2(w.x, -w.y));
+    }
+    fft_reg_rt<16>(v, true);
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) buf[csw(q + 16 * r, c)] = v[r];
+    __syncwarp();
+}
+
 // Pass 2 of the plane (FFT along axis 0, solve, inverse) with TMA: a tile of
 // TK columns x N rows is one cp.async.bulk.tensor load into a dense
 // [row][column] shared-memory tile (the line-interleaved layout the Stockham
@@ -1291,13 +1351,55 @@ __device__ __forceinline__ void fence_proxy_async() {
 // TMA store.  Double-buffered: thread 0 issues tile t+1's load while the
 // CTA transforms tile t, after the previous store from that buffer has read
 // its shared memory.
+// plane_col_tma's double-buffered TMA loop around col_fft_solve_256
+__device__ __forceinline__ void plane_col_swz(const CUtensorMap *map, int plane, double2 *smem,
+                                              uint64_t *bars, uint32_t (&phase)[2], int t0,
+                                              int t1, const PlaneGeom &g, int k2,
+                                              const double2 *__restrict__ tw) {
+    constexpr int N = 256, TK = 8;
+    constexpr uint32_t BYTES = (uint32_t)(N * TK * sizeof(double2));
+    const int tx = threadIdx.x;
+    double2 *buf[2] = {smem, smem + N * (TK + 1)};  // 1024-byte aligned offsets
+    if (tx == 0 && t0 < t1) {
+        bulk_wait_read0();
+        mbar_expect_tx(&bars[0], BYTES);
+        tma_load_3d(buf[0], map, &bars[0], 2 * t0 * TK, 0, plane);
+    }
+#pragma unroll 1
+    for (int t = t0, i = 0; t < t1; ++t, ++i) {
+        const int b = i & 1;
+        if (tx == 0 && t + 1 < t1) {
+            bulk_wait_read0();
+            mbar_expect_tx(&bars[1 - b], BYTES);
+            tma_load_3d(buf[1 - b], map, &bars[1 - b], 2 * (t + 1) * TK, 0, plane);
+        }
+        mbar_wait(&bars[b], phase[b]);
+        phase[b] ^= 1u;
+        col_fft_solve_256(buf[b], tw, g, t * TK + (tx >> 4), k2);
+        fence_proxy_async();
+        __syncthreads();
+        if (tx == 0) {
+            tma_store_3d(map, buf[b], 2 * t * TK, 0, plane);
+            bulk_commit();
+        }
+    }
+    if (tx == 0) bulk_wait0();
+    __syncthreads();
+}
+
 template <int N1, int N2, int TK>
 __device__ __forceinline__ void plane_col_tma(const CUtensorMap *map, int plane, double2 *smem,
                                               uint64_t *bars, uint32_t (&phase)[2], int t0,
                                               int t1, const PlaneGeom &g, int k2,
-                                              const double2 *__restrict__ tw) {
+                                              const double2 *__restrict__ tw, bool swz) {
     using C = PlaneCfg<N1, N2, TK>;
     constexpr int N = C::N, NT = C::NT, IT = C::IT, LD = TK;
+    if constexpr (N == 256 && TK == 8 && NT == 128) {
+        if (swz) {  // 16 lanes per column on the swizzled tile, no block barrier
+            plane_col_swz(map, plane, smem, bars, phase, t0, t1, g, k2, tw);
+            return;
+        }
+    }
     constexpr uint32_t BYTES = (uint32_t)(N * TK * sizeof(double2));
     const int tx = threadIdx.x;
     double2 *buf[2] = {smem, smem + N * (TK + 1)};  // 128-byte aligned offsets
@@ -1433,12 +1535,13 @@ k_plane(double2 *__restrict__ spec, PlaneGeom g, const double2 *__restrict__ tw,
         const __grid_constant__ CUtensorMap rmap) {
     constexpr int N = N1 * N2;
     constexpr int PER = N / TK / CS;  // tiles per CTA per pass
-    extern __shared__ __align__(128) double2 smem_c[];
+    extern __shared__ __align__(1024) double2 smem_c[];  // 128-byte swizzled TMA tiles
     const int plane = blockIdx.x / CS;  // c * nh + k2
     const int r = blockIdx.x % CS;      // rank in the cluster
     const int k2 = plane % g.nh;
     double2 *pl = spec + (int64_t)plane * N * N;
-    // use_tma: 1 = the column pass through TMA, 2 = the row passes too
+    // use_tma: 1 = the column pass through TMA, 2 = the row passes too,
+    // 3 = and the column pass on swizzled tiles
     // (n = 256, 8-row tiles, 128 threads: 16 lanes per row)
     constexpr bool ROWTMA = N1 * N2 == 256 && TK == 8 && PlaneCfg<N1, N2, TK>::NT == 128;
     constexpr bool COLTMA = PlaneCfg<N1, N2, TK>::PPT == 16;
@@ -1452,7 +1555,7 @@ k_plane(double2 *__restrict__ spec, PlaneGeom g, const double2 *__restrict__ tw,
         }
         __syncthreads();
     }
-    if (ROWTMA && use_tma == 2)
+    if (ROWTMA && use_tma >= 2)
         plane_row_tma<TK>(&rmap, plane, smem_c, bars, phase, r * PER, (r + 1) * PER, tw, false);
     else
         plane_pass<N1, N2, TK, PL_ROW_FWD>(pl, smem_c, r * PER, (r + 1) * PER, g, k2, tw);
@@ -1460,7 +1563,7 @@ k_plane(double2 *__restrict__ spec, PlaneGeom g, const double2 *__restrict__ tw,
     if constexpr (COLTMA) {
         if (use_tma) {
             plane_col_tma<N1, N2, TK>(&tmap, plane, smem_c, bars, phase, r * PER, (r + 1) * PER,
-                                      g, k2, tw);
+                                      g, k2, tw, use_tma == 3);
         } else {
             plane_pass<N1, N2, TK, PL_COL_SOLVE>(pl, smem_c, r * PER, (r + 1) * PER, g, k2, tw);
         }
@@ -1468,7 +1571,7 @@ k_plane(double2 *__restrict__ spec, PlaneGeom g, const double2 *__restrict__ tw,
         plane_pass<N1, N2, TK, PL_COL_SOLVE>(pl, smem_c, r * PER, (r + 1) * PER, g, k2, tw);
     }
     cluster_barrier();
-    if (ROWTMA && use_tma == 2)
+    if (ROWTMA && use_tma >= 2)
         plane_row_tma<TK>(&rmap, plane, smem_c, bars, phase, r * PER, (r + 1) * PER, tw, true);
     else
         plane_pass<N1, N2, TK, PL_ROW_INV>(pl, smem_c, r * PER, (r + 1) * PER, g, k2, tw);
@@ -1580,7 +1683,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(NTH, MM_PLANE_HW_MI
 k_plane_hw(double2 *__restrict__ spec, PlaneGeom g, const double2 *__restrict__ tw) {
     constexpr int N = 256, NSLOT = NTH / 16, LPC = N / CS;
     static_assert(LPC % NSLOT == 0, "lines per CTA divide among the slots");
-    extern __shared__ __align__(128) double2 smem_c[];
+    extern __shared__ __align__(1024) double2 smem_c[];  // 128-byte swizzled TMA tiles
     const int plane = blockIdx.x / CS;  // c * nh + k2
     const int r = blockIdx.x % CS;      // rank in the cluster
     const int k2 = plane % g.nh;
@@ -2030,12 +2133,16 @@ int run_col(mm_ctx *ctx, const ColGeom &g, int n_outer) {
 #ifndef MM_PLANE_TMA  // 1: pass 2 of the plane FFT through TMA + mbarrier (plane_col_tma);
 #define MM_PLANE_TMA 2  // 2: passes 1 and 3 too at n = 256 (plane_row_tma)
 #endif
+#ifndef MM_PLANE_COLSWZ
+#define MM_PLANE_COLSWZ 0  // 1: n = 256 column pass on 128-byte swizzled tiles (plane_col_swz; measured slower)
+#endif
 
 // Tensor map of the plane-layout spectrum for plane_col_tma: doubles, dims
 // {2N (re/im along axis 1), N (axis 0), planes}, box {2 TK, N, 1}.  Encoded
 // once per context through the driver entry point (no libcuda link).
-int mm_plane_tensor_map(mm_ctx *ctx, int N, int TK) {
-    if (ctx->tmap_ok && ctx->tmap_src == ctx->spec && ctx->tmap_n == N) return MM_OK;
+int mm_plane_tensor_map(mm_ctx *ctx, int N, int TK, bool swz) {
+    // the cache key includes the swizzle: tmap_n = N, negated for the swizzled map
+    if (ctx->tmap_ok && ctx->tmap_src == ctx->spec && ctx->tmap_n == (swz ? -N : N)) return MM_OK;
     ctx->tmap_ok = false;
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
@@ -2054,8 +2161,11 @@ int mm_plane_tensor_map(mm_ctx *ctx, int N, int TK) {
     const cuuint64_t strides[2] = {(cuuint64_t)N * 16, (cuuint64_t)N * N * 16};
     const cuuint32_t box[3] = {(cuuint32_t)(2 * TK), (cuuint32_t)N, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
+    // swz (n = 256, TK = 8, 128 threads, MM_PLANE_TMA >= 2): the column tiles
+    // use the 128-byte swizzle that col_fft_solve_256 indexes
     CUresult r = encode(&ctx->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, ctx->spec, dims, strides,
-                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return mm_fail(ctx, MM_ERR_CUDA, "cuTensorMapEncodeTiled: %d", (int)r);
     // row tiles (passes 1 and 3, n = 256): doubles {256 (half a row), 2 halves,
@@ -2075,7 +2185,7 @@ int mm_plane_tensor_map(mm_ctx *ctx, int N, int TK) {
     }
     ctx->tmap_ok = true;
     ctx->tmap_src = ctx->spec;
-    ctx->tmap_n = N;
+    ctx->tmap_n = swz ? -N : N;
     return MM_OK;
 }
 
@@ -2094,11 +2204,14 @@ int run_plane_t(mm_ctx *ctx, const PlaneGeom &g) {
     const int blocks = CS * ctx->dim * g.nh;
     int use_tma = 0;
     if (C::PPT == 16 && MM_PLANE_TMA) {
-        if ((rc = mm_plane_tensor_map(ctx, C::N, TK))) return rc;
+        // use_tma == 3 <=> the column map is swizzled (plane_col_swz)
+        const bool swz =
+            MM_PLANE_TMA >= 2 && MM_PLANE_COLSWZ && C::N == 256 && TK == 8 && C::NT == 128;
+        if ((rc = mm_plane_tensor_map(ctx, C::N, TK, swz))) return rc;
         use_tma = ctx->tmap_ok ? 1 : 0;
         if (use_tma && MM_PLANE_TMA >= 2 && C::N == 256 && TK == 8 && C::NT == 128 &&
             ctx->rmap_ok)
-            use_tma = 2;
+            use_tma = swz ? 3 : 2;
     }
     kern<<<blocks, C::NT, smem, ctx->stream>>>(ctx->spec, g, ctx->tw_full, ctx->tmap, use_tma,
                                                ctx->rmap);
