@@ -2205,8 +2205,10 @@ int run_plane_t(mm_ctx *ctx, const PlaneGeom &g) {
     int use_tma = 0;
     if (C::PPT == 16 && MM_PLANE_TMA) {
         // use_tma == 3 <=> the column map is swizzled (plane_col_swz)
-        const bool swz =
-            MM_PLANE_TMA >= 2 && MM_PLANE_COLSWZ && C::N == 256 && TK == 8 && C::NT == 128;
+        // MM_PLANE_COLSWZ in the environment overrides the build default (per call: tests)
+        const char *cs_env = getenv("MM_PLANE_COLSWZ");
+        const bool colswz = cs_env && *cs_env ? atoi(cs_env) != 0 : MM_PLANE_COLSWZ != 0;
+        const bool swz = MM_PLANE_TMA >= 2 && colswz && C::N == 256 && TK == 8 && C::NT == 128;
         if ((rc = mm_plane_tensor_map(ctx, C::N, TK, swz))) return rc;
         use_tma = ctx->tmap_ok ? 1 : 0;
         if (use_tma && MM_PLANE_TMA >= 2 && C::N == 256 && TK == 8 && C::NT == 128 &&
