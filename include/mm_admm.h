@@ -375,9 +375,11 @@ enum mm_option {
     MM_OPT_T_FIELD = 2,
     MM_OPT_PLANE_FFT = 3,
     MM_OPT_ROWINV_PIPE = 4, /* default 1: persistent double-buffered C2R rows (plane layout) */
-    MM_OPT_SPECULATE = 5    /* default 1: mm_update_and_sweep queues the next projection's
+    MM_OPT_SPECULATE = 5,   /* default 1: mm_update_and_sweep queues the next projection's
                              * A / column passes / E behind the fused pass; mm_project_residuals
                              * uses them if no other call intervened and rho matches */
+    MM_OPT_ROWFWD_WARP = 6  /* default 1: n = 256 R2C rows with one warp per 4-row task
+                             * (k_row_fwd_w), same four-step as the block-tiled kernel */
 };
 int mm_set_option(mm_ctx *ctx, int option, int64_t value);
 

@@ -1333,6 +1333,7 @@ int mm_set_option(mm_ctx *ctx, int option, int64_t value) {
         case MM_OPT_PLANE_FFT: ctx->opt_plane = value != 0; return MM_OK;
         case MM_OPT_ROWINV_PIPE: ctx->opt_rowinv_p = value != 0; return MM_OK;
         case MM_OPT_SPECULATE: ctx->opt_speculate = value != 0; return MM_OK;
+        case MM_OPT_ROWFWD_WARP: ctx->opt_rowfwd_w = value != 0; return MM_OK;
         default: return mm_fail(ctx, MM_ERR_PARAM, "unknown option %d", option);
     }
 }

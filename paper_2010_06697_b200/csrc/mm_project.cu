@@ -50,6 +50,12 @@ namespace {
 #ifndef MM_ROWFWD_REGS
 #define MM_ROWFWD_REGS 96
 #endif
+#ifndef MM_ROWFWD_W
+#define MM_ROWFWD_W 1  // n = 256: the warp-per-task R2C rows (k_row_fwd_w)
+#endif
+#ifndef MM_ROWFWD_W_MINB
+#define MM_ROWFWD_W_MINB 4  // 128 registers: 0.369 ms at 256^3 (5: 0.399, 6: 0.574, tiled kernel 0.459)
+#endif
 __constant__ double2 c_w32[32];  // exp(-2 pi i k / 32)
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -686,6 +692,102 @@ k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho
             spec[((int64_t)c * nh + k) * g.nrows + row] = X;
         else
             spec[((int64_t)c * g.nrows + row) * g.P + k] = X;
+    }
+}
+
+// A for n = 256 (3D, T field, single GPU): one warp per task of 4
+// consecutive rows x one component, 8 lanes per row, no block barrier.  Lane
+// q of a row holds slots m = q + 8 s (s < 16) of the packed row
+// z[m] = d[2m] + i d[2m+1]: its loads are 128-byte row segments (T_c2 of the
+// row, T_c0 of the axis-0 neighbour rows, T_c1 of the axis-1 neighbour
+// rows), the stencil arithmetic is k_row_fwd's, and the 128-point transform
+// is tile_fft<16, 8>'s four-step in the same order (16-point FFTs over s,
+// twiddles W^{q k1}, an XOR-swizzled exchange through the warp's own shared
+// memory, 8-point FFTs), so the spectrum is k_row_fwd's.  The split and the
+// stores read the natural-order row back from shared memory: 64-byte runs
+// (4 rows of one (c, k)) in the plane layout, 128-byte runs in the row
+// layout.
+constexpr int RFW_WARPS = 4;
+__global__ void __launch_bounds__(32 * RFW_WARPS, MM_ROWFWD_W_MINB)
+k_row_fwd_w(const double *__restrict__ T, double2 *__restrict__ spec, RowGeom g,
+            const double2 *__restrict__ tw, const double2 *__restrict__ tw_r2c) {
+    constexpr int n = 256, N = 128, nh = 129;
+    __shared__ double2 sm[RFW_WARPS][4][N];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t task = (int64_t)blockIdx.x * RFW_WARPS + warp;
+    if (task >= 3 * (g.nrows / 4)) return;
+    const int c = (int)(task % 3);
+    const int64_t row0 = (task / 3) * 4;
+    const int j = lane >> 3, q = lane & 7;
+    const int64_t row = row0 + j;
+    const int64_t M = g.M;
+    const RowNbr nb = row_nbrs(g, (int)row);
+    const double *Tz = T + (int64_t)(c * 3) * M;
+    const double *Ty = T + (int64_t)(c * 3 + 1) * M;
+    const double *Tx = T + (int64_t)(c * 3 + 2) * M + nb.self;
+    double2 v[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const int m = q + 8 * s;
+        const int x0 = 2 * m;
+        const int xm = (x0 == 0) ? n - 1 : x0 - 1;
+        const int xp = (x0 + 2 == n) ? 0 : x0 + 2;
+        const double2 fx = __ldg(reinterpret_cast<const double2 *>(Tx + x0));
+        const double fxm = __ldg(Tx + xm), fxp = __ldg(Tx + xp);
+        const double2 zp = __ldg(reinterpret_cast<const double2 *>(Tz + nb.zp + x0));
+        const double2 zm = __ldg(reinterpret_cast<const double2 *>(Tz + nb.zm + x0));
+        const double2 yp = __ldg(reinterpret_cast<const double2 *>(Ty + nb.yp + x0));
+        const double2 ym = __ldg(reinterpret_cast<const double2 *>(Ty + nb.ym + x0));
+        const double y0 = yp.x - ym.x, y1 = yp.y - ym.y;
+        v[s].x = (zp.x - zm.x) + y0 + (fx.y - fxm);
+        v[s].y = (zp.y - zm.y) + y1 + (fxp - fx.x);
+        if ((s & 3) == 3) asm volatile("" ::: "memory");  // loads in batches of 4 slots
+    }
+    // step 1 (tile_fft<16, 8>): n2 = q, 16 points x[8 n1 + q]
+    fft_reg<16, false>(v);
+    if (q != 0) {
+#pragma unroll
+        for (int k1 = 1; k1 < 16; ++k1) v[k1] = cmul(v[k1], __ldg(&tw[q * k1]));
+    }
+    double2 *L = sm[warp][j];
+    // element (k1, n2) of the exchange at k1 * 8 + (n2 ^ (k1 & 7))
+#pragma unroll
+    for (int k1 = 0; k1 < 16; ++k1) L[k1 * 8 + (q ^ (k1 & 7))] = v[k1];
+    __syncwarp();
+    // step 2: columns k1 = q and q + 8, 8 points each -> X[k1 + 16 k2]
+    double2 u[2][8];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int k1 = q + 8 * h;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) u[h][t] = L[k1 * 8 + (t ^ (k1 & 7))];
+        fft_reg<8, false>(u[h]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) L[q + 8 * h + 16 * k2] = u[h][k2];
+    __syncwarp();
+    // split (k_row_fwd's expression) and store
+    const double2 *W = sm[warp][0];
+    const int rj = g.plane ? (lane & 3) : (lane >> 3);
+    const int kk = g.plane ? (lane >> 2) : (lane & 7);
+    const int kst = g.plane ? 8 : 8;
+    const double2 *Lr = W + rj * N;
+    const int64_t orow = row0 + rj;
+#pragma unroll 3
+    for (int k = kk; k < nh; k += kst) {
+        const double2 Zk = Lr[k == N ? 0 : k];
+        const double2 Zc = cconj(Lr[k == 0 ? 0 : N - k]);
+        const double2 E = cscale(cadd(Zk, Zc), 0.5);
+        const double2 Od = csub(Zk, Zc);
+        const double2 WO = cmul(__ldg(&tw_r2c[k]), Od);
+        const double2 X = make_double2(E.x + 0.5 * WO.y, E.y - 0.5 * WO.x);
+        if (g.plane)
+            spec[((int64_t)c * nh + k) * g.nrows + orow] = X;
+        else
+            spec[((int64_t)c * g.nrows + orow) * g.P + k] = X;
     }
 }
 
@@ -2001,6 +2103,16 @@ int run_rows_t(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double
     const size_t smem = sizeof(double2) * (size_t)(g.N + 1) * (C::TK + 1) * (N1 ? 1 : 2);
     dim3 grid((unsigned)((g.nrows + ROWS - 1) / ROWS));
     if (fwd) {
+        if constexpr (N1 == 16 && N2 == 8 && DIM == 3) {
+            if (fsrc && MM_ROWFWD_W && g.packed && !g.hhi && g.nrows % 4 == 0 && ctx->opt_rowfwd_w) {
+                const int64_t tasks = 3 * (g.nrows / 4);
+                const unsigned blocks = (unsigned)((tasks + RFW_WARPS - 1) / RFW_WARPS);
+                k_row_fwd_w<<<blocks, 32 * RFW_WARPS, 0, ctx->stream>>>(fsrc, ctx->spec, g, tw_line,
+                                                                       ctx->tw_r2c);
+                MM_LAUNCH_CHECK(ctx);
+                return MM_OK;
+            }
+        }
         if (fsrc) {
             // divergence of the given field alone (T supplied, or a stress field)
             auto kern = k_row_fwd<N1, N2, DIM, ROWS, false>;

@@ -384,6 +384,38 @@ def test_plane_fft_matches_row_layout(n, monkeypatch):
     np.testing.assert_allclose(out["1"][3][1:], out["0"][3][1:], rtol=1e-11)
 
 
+def test_row_fwd_warp_kernel_matches_tiled():
+    """n = 256: the warp-per-task R2C rows (k_row_fwd_w, MM_OPT_ROWFWD_WARP)
+    perform tile_fft<16, 8>'s four-step and k_row_fwd's stencil and split in
+    the same order; whole outer iterations agree with the block-tiled kernel
+    to roundoff (the compiler may contract complex products differently),
+    sweep counts exactly."""
+    import os
+    grid, mu, kap = _laminate(3, 256, 0)
+    bc = mm.MacroBC.strain(np.diag([0.95, 1.0, 1.0]))
+    m = mm.MooneyRivlin(mu, kap, dim=3, mu_rep=1.0)
+    params = mm.SolverParams(max_outer=3)
+    out = {}
+    for flag in ("1", "0"):
+        os.environ["MM_ROWFWD_WARP"] = flag
+        try:
+            st = mm.solver.init_state(grid, m, bc, params)
+            st.F = st.F + 1e-4 * np.random.default_rng(0).standard_normal(st.F.shape)
+            st, _ = mm.solve(grid, m, bc, params, policy=mm.RatioToDual(0.3), state=st,
+                             raise_on_max=False)
+        finally:
+            del os.environ["MM_ROWFWD_WARP"]
+        out[flag] = ([np.array(getattr(st, k)) for k in ("F", "lam", "grad_u", "u_tilde")],
+                     st.history[-1][:5], st.total_sweeps)
+        del st
+    bitwise = all(np.array_equal(a, b) for a, b in zip(out["1"][0], out["0"][0]))
+    print("row_fwd warp vs tiled bitwise:", bitwise)
+    for a, b in zip(out["1"][0], out["0"][0]):
+        assert rel_l2(a, b) < 1e-13
+    assert out["1"][2] == out["0"][2]
+    np.testing.assert_allclose(out["1"][1][1:], out["0"][1][1:], rtol=1e-11)
+
+
 def test_plane_column_swizzle_variant():
     """n = 256: the column pass on 128-byte swizzled TMA tiles with the
     in-warp FFT (MM_PLANE_COLSWZ=1, csrc/mm_project.cu col_fft_solve_256)
