@@ -378,8 +378,9 @@ enum mm_option {
     MM_OPT_SPECULATE = 5,   /* default 1: mm_update_and_sweep queues the next projection's
                              * A / column passes / E behind the fused pass; mm_project_residuals
                              * uses them if no other call intervened and rho matches */
-    MM_OPT_ROWFWD_WARP = 6  /* default 1: n = 256 R2C rows with one warp per 4-row task
-                             * (k_row_fwd_w), same four-step as the block-tiled kernel */
+    MM_OPT_ROWFWD_WARP = 6  /* default 1: single-GPU n = 256 R2C rows with one warp per
+                             * 4-row task (k_row_fwd_w): the block-tiled kernel's four-step
+                             * in the same order (bitwise equal) */
 };
 int mm_set_option(mm_ctx *ctx, int option, int64_t value);
 

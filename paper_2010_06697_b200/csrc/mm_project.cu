@@ -695,6 +695,17 @@ k_row_fwd(const double *__restrict__ F, const double *__restrict__ L, double rho
     }
 }
 
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc, int src_bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc),
+                 "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND));
+}
+
 // A for n = 256 (3D, T field, single GPU): one warp per task of 4
 // consecutive rows x one component, 8 lanes per row, no block barrier.  Lane
 // q of a row holds slots m = q + 8 s (s < 16) of the packed row
@@ -1035,16 +1046,6 @@ k_col(double2 *__restrict__ spec, ColGeom g, const double2 *__restrict__ tw) {
 // one shared buffer, the cp.async (LDGSTS) copies of tile t+gridDim.x land in
 // the other, so global loads are always in flight (the plain variant above is
 // load-latency bound: ncu long_scoreboard stalls dominate).
-__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc, int src_bytes) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc),
-                 "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int NPEND>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND));
-}
 
 struct TileMap {
     int ntk, n_outer;  // column tiles per line set, outer lines
@@ -2104,7 +2105,8 @@ int run_rows_t(mm_ctx *ctx, bool fwd, double rho, const RowGeom &g, const double
     dim3 grid((unsigned)((g.nrows + ROWS - 1) / ROWS));
     if (fwd) {
         if constexpr (N1 == 16 && N2 == 8 && DIM == 3) {
-            if (fsrc && MM_ROWFWD_W && g.packed && !g.hhi && g.nrows % 4 == 0 && ctx->opt_rowfwd_w) {
+            if (fsrc && MM_ROWFWD_W && g.packed && !g.hhi && !ctx->slab_mode && g.nrows % 4 == 0 &&
+                ctx->opt_rowfwd_w) {
                 const int64_t tasks = 3 * (g.nrows / 4);
                 const unsigned blocks = (unsigned)((tasks + RFW_WARPS - 1) / RFW_WARPS);
                 k_row_fwd_w<<<blocks, 32 * RFW_WARPS, 0, ctx->stream>>>(fsrc, ctx->spec, g, tw_line,
