@@ -91,9 +91,22 @@ int mm_ensure_partials(mm_ctx *ctx, int64_t nblocks) {
     return MM_OK;
 }
 
+// The reduction result slot: single-grid and point-set contexts map it from
+// pinned host memory, so the last block of a reducing kernel writes the sums
+// straight to the host (no copy launch, no copy on the GPU timeline); slab
+// contexts keep it in device memory.
+static int alloc_red_out(mm_ctx *ctx) {
+    MM_CUDA(ctx, cudaHostAlloc((void **)&ctx->host_out, sizeof(double) * MM_MAX_PARTIALS,
+                               cudaHostAllocMapped));
+    MM_CUDA(ctx, cudaHostGetDevicePointer((void **)&ctx->red_out, ctx->host_out, 0));
+    ctx->red_mapped = true;
+    return MM_OK;
+}
+
 int mm_fetch_reduction(mm_ctx *ctx, int K, double *out) {
-    MM_CUDA(ctx, cudaMemcpyAsync(ctx->host_out, ctx->red_out, sizeof(double) * K,
-                                 cudaMemcpyDeviceToHost, ctx->stream));
+    if (!ctx->red_mapped)
+        MM_CUDA(ctx, cudaMemcpyAsync(ctx->host_out, ctx->red_out, sizeof(double) * K,
+                                     cudaMemcpyDeviceToHost, ctx->stream));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     memcpy(out, ctx->host_out, sizeof(double) * K);
     mm_drain_timings(ctx);
@@ -541,10 +554,9 @@ int mm_create(int dim, int n, double length, int device, mm_ctx **out) {
     TRY(mm_alloc(ctx, (void **)&ctx->Ut, sizeof(double) * dim * M));
     TRY(mm_alloc(ctx, (void **)&ctx->spec, sizeof(double2) * dim * ctx->nrows * ctx->P));
     TRY(mm_alloc(ctx, (void **)&ctx->sym, sizeof(double) * dim * n));
-    TRY(mm_alloc(ctx, (void **)&ctx->red_out, sizeof(double) * MM_MAX_PARTIALS));
+    TRY(alloc_red_out(ctx));
     TRY(mm_alloc(ctx, (void **)&ctx->red_count, sizeof(unsigned int) * 4));
     MM_CUDA(ctx, cudaMemset(ctx->red_count, 0, sizeof(unsigned int) * 4));
-    MM_CUDA(ctx, cudaMallocHost((void **)&ctx->host_out, sizeof(double) * MM_MAX_PARTIALS));
     MM_CUDA(ctx, cudaMemsetAsync(ctx->F, 0, sizeof(double) * ctx->D * M, ctx->stream));
     MM_CUDA(ctx, cudaMemsetAsync(ctx->G, 0, sizeof(double) * ctx->D * M, ctx->stream));
     MM_CUDA(ctx, cudaMemsetAsync(ctx->Lam, 0, sizeof(double) * ctx->D * M, ctx->stream));
@@ -777,10 +789,9 @@ int mm_create_points(int dim, int64_t npts, int device, mm_ctx **out) {
     if ((rc = mm_alloc(ctx, (void **)&ctx->F, sizeof(double) * ctx->D * M))) return rc;
     if ((rc = mm_alloc(ctx, (void **)&ctx->G, sizeof(double) * ctx->D * M))) return rc;
     if ((rc = mm_alloc(ctx, (void **)&ctx->Lam, sizeof(double) * ctx->D * M))) return rc;
-    if ((rc = mm_alloc(ctx, (void **)&ctx->red_out, sizeof(double) * MM_MAX_PARTIALS))) return rc;
+    if ((rc = alloc_red_out(ctx))) return rc;
     if ((rc = mm_alloc(ctx, (void **)&ctx->red_count, sizeof(unsigned int) * 4))) return rc;
     MM_CUDA(ctx, cudaMemset(ctx->red_count, 0, sizeof(unsigned int) * 4));
-    MM_CUDA(ctx, cudaMallocHost((void **)&ctx->host_out, sizeof(double) * MM_MAX_PARTIALS));
     if ((rc = mm_ensure_partials(ctx, 4096))) return rc;
     return MM_OK;
 }
@@ -795,6 +806,7 @@ void mm_destroy(mm_ctx *ctx) {
     if (ctx->Ut_base) ctx->Ut = ctx->Ut_base;
     if (ctx->Ut2_base) ctx->Ut2 = ctx->Ut2_base;
     if (ctx->dir_base) ctx->dirbuf = ctx->dir_base;
+    if (ctx->red_mapped) ctx->red_out = nullptr;  // host_out's device alias
     double *ptrs[] = {ctx->F, ctx->G, ctx->Lam, ctx->Ut, ctx->prevF, ctx->modA, ctx->modB,
                       ctx->ang, ctx->chart, ctx->pinc, ctx->n0, ctx->ff, ctx->prevAng,
                       ctx->prevChart, ctx->prevPinc, ctx->dirbuf, ctx->Ut2, ctx->halo_in_lo,

@@ -83,6 +83,7 @@ struct mm_ctx {
     bool opt_plane = true;        // MM_OPT_PLANE_FFT
     bool opt_rowinv_p = true;     // MM_OPT_ROWINV_PIPE
     bool opt_rowfwd_w = true;     // MM_OPT_ROWFWD_WARP
+    bool red_mapped = false;      // red_out is host_out's device alias (mapped pinned memory)
     bool opt_speculate = true;    // MM_OPT_SPECULATE
     // speculative projection front (A, column passes, E of the next
     // iteration launched by mm_update_and_sweep behind the fused pass): valid

@@ -1105,8 +1105,9 @@ int mm_run_update(mm_ctx *ctx, int material, double rho_next, double tol, int64_
     ctx->front_valid = false;
     if (spec) {
         if (!ctx->ev_red) MM_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_red, cudaEventDisableTiming));
-        MM_CUDA(ctx, cudaMemcpyAsync(ctx->host_out, ctx->red_out, sizeof(double) * K,
-                                     cudaMemcpyDeviceToHost, ctx->stream));
+        if (!ctx->red_mapped)
+            MM_CUDA(ctx, cudaMemcpyAsync(ctx->host_out, ctx->red_out, sizeof(double) * K,
+                                         cudaMemcpyDeviceToHost, ctx->stream));
         MM_CUDA(ctx, cudaEventRecord(ctx->ev_red, ctx->stream));
         double *u_new = nullptr;
         if ((rc = mm_run_project_front(ctx, rho_next, 2, &u_new))) return rc;
