@@ -25,9 +25,53 @@ def run(mod, n=64):
     return study, dt
 
 
+def breakdown():
+    """Time inside the library loop (mm_solve_fused) vs the rest of the study."""
+    import time as _t
+    from paper_2010_06697_b200 import _lib
+    acc = {"t": 0.0, "calls": 0, "iters": 0}
+    orig = _lib.Context.solve_fused
+
+    def timed(self, sp, max_outer):
+        t0 = _t.perf_counter()
+        out = orig(self, sp, max_outer)
+        acc["t"] += _t.perf_counter() - t0
+        acc["calls"] += 1
+        acc["iters"] += out[0].iterations
+        return out
+
+    from paper_2010_06697_b200 import _engine
+    eacc = {"t": 0.0}
+    eorig = _engine.Engine.__init__
+
+    def etimed(self, *a, **k):
+        t0 = _t.perf_counter()
+        eorig(self, *a, **k)
+        eacc["t"] += _t.perf_counter() - t0
+
+    _lib.Context.solve_fused = timed
+    _engine.Engine.__init__ = etimed
+    try:
+        run(mm)
+        for k in acc:
+            acc[k] = 0
+        eacc["t"] = 0.0
+        study, dt = run(mm)
+    finally:
+        _lib.Context.solve_fused = orig
+        _engine.Engine.__init__ = eorig
+    print(f"study {dt*1e3:.1f} ms; engine creation {eacc['t']*1e3:.1f} ms; inside mm_solve_fused "
+          f"{acc['t']*1e3:.1f} ms over {acc['calls']} calls, {acc['iters']} iterations = "
+          f"{acc['t']/max(acc['iters'],1)*1e6:.1f} us per iteration")
+
+
 if __name__ == "__main__":
+    if "--breakdown" in sys.argv:
+        breakdown()
+        sys.exit(0)
     run(mm)  # warm-up (context, JIT-free)
     study, dt = run(mm)
     it = study.state.outer_iter
     print(f"device: {len(study.records)} load steps, {it} outer iterations in {dt * 1e3:.1f} ms "
           f"= {dt / it * 1e6:.1f} us per outer iteration ({64 * 64 * it / dt:.3e} voxel-iter/s)")
+
