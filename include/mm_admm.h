@@ -378,9 +378,12 @@ enum mm_option {
     MM_OPT_SPECULATE = 5,   /* default 1: mm_update_and_sweep queues the next projection's
                              * A / column passes / E behind the fused pass; mm_project_residuals
                              * uses them if no other call intervened and rho matches */
-    MM_OPT_ROWFWD_WARP = 6  /* default 1: single-GPU n = 256 R2C rows with one warp per
+    MM_OPT_ROWFWD_WARP = 6, /* default 1: single-GPU n = 256 R2C rows with one warp per
                              * 4-row task (k_row_fwd_w): the block-tiled kernel's four-step
                              * in the same order (bitwise equal) */
+    MM_OPT_PIPELINE = 7     /* default 1: mm_residuals_and_step queues K1, the decision (on
+                             * the device) and the next fused pass back to back; the host
+                             * takes the same decision and checks it (bitwise equal loop) */
 };
 int mm_set_option(mm_ctx *ctx, int option, int64_t value);
 

@@ -56,6 +56,7 @@ class Engine:
         self.ctx.set_option(4, int(os.environ.get("MM_ROWINV_PIPE", "1")))
         self.ctx.set_option(5, int(os.environ.get("MM_SPECULATE", "1")))
         self.ctx.set_option(6, int(os.environ.get("MM_ROWFWD_WARP", "1")))
+        self.ctx.set_option(7, int(os.environ.get("MM_PIPELINE", "1")))
         self.model = None          # model whose parameters are on the device
         self.model_version = None
         self.lam_sum = None        # device-side sum of lam (None: recompute)

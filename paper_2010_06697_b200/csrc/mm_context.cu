@@ -134,8 +134,9 @@ static bool park_recycled(mm_ctx *ctx) {
 }
 
 static int alloc_red_out(mm_ctx *ctx) {
+    // three slots: reductions, K1's sums of a pipelined step, k_decide's copy
     if (!ctx->host_out)
-        MM_CUDA(ctx, cudaHostAlloc((void **)&ctx->host_out, sizeof(double) * MM_MAX_PARTIALS,
+        MM_CUDA(ctx, cudaHostAlloc((void **)&ctx->host_out, sizeof(double) * 3 * MM_MAX_PARTIALS,
                                    cudaHostAllocMapped));
     MM_CUDA(ctx, cudaHostGetDevicePointer((void **)&ctx->red_out, ctx->host_out, 0));
     ctx->red_mapped = true;
@@ -854,7 +855,8 @@ void mm_destroy(mm_ctx *ctx) {
                       ctx->halo_in_hi, ctx->halo_out_lo, ctx->halo_out_hi, ctx->sym, ctx->partials, ctx->red_out,
                       ctx->res, ctx->tstate, ctx->stage, ctx->Pbuf, ctx->Tbuf};
     for (double *p : ptrs) mm_free(ctx, p);
-    void *lce_bufs[] = {ctx->lce_fsq0, ctx->lce_list[0], ctx->lce_list[1], ctx->lce_cnt};
+    void *lce_bufs[] = {ctx->lce_fsq0, ctx->lce_list[0], ctx->lce_list[1], ctx->lce_cnt,
+                        ctx->dstep};
     for (void *p : lce_bufs) mm_free(ctx, p);
     void *others[] = {ctx->spec, ctx->tw_full, ctx->tw_half, ctx->tw_r2c, ctx->red_count,
                       ctx->nsw, ctx->ok, ctx->freestate, ctx->peer_recv, ctx->peer_send};
@@ -864,6 +866,7 @@ void mm_destroy(mm_ctx *ctx) {
     if (ctx->recvbuf) cudaFree(ctx->recvbuf);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->ev_red) cudaEventDestroy(ctx->ev_red);
+    if (ctx->ev_k1) cudaEventDestroy(ctx->ev_k1);
     if (ctx->xfer_ev[0]) cudaEventDestroy(ctx->xfer_ev[0]);
     if (ctx->xfer_ev[1]) cudaEventDestroy(ctx->xfer_ev[1]);
     if (park_recycled(ctx)) {
@@ -1199,10 +1202,103 @@ int mm_update_and_sweep(mm_ctx *ctx, int material, double rho_next, double tol,
     return mm_run_update(ctx, material, rho_next, tol, max_sweeps, phi_scale, want_points, ls, us);
 }
 
+// One pipelined step: K1 (whose last block also takes the decision,
+// decide_step), the fused pass (parameters from the device) and the
+// speculative front are queued back to back; the host then
+// reads K1's sums, takes the same decision, checks it against the device's
+// and finishes.  The GPU never waits for the host between K1 and the fused
+// pass.
+static int residuals_and_step_pipelined(mm_ctx *ctx, const mm_step_params *p,
+                                        mm_step_result *out, mm_local_stats *ls) {
+    int rc = mm_flush_pending(ctx);
+    if (rc) return rc;
+    if (!ctx->dstep && (rc = mm_alloc(ctx, (void **)&ctx->dstep, sizeof(DevStep)))) return rc;
+    if (!ctx->ev_k1) MM_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_k1, cudaEventDisableTiming));
+    double *k1 = ctx->red_out + MM_MAX_PARTIALS;
+    double *dcopy = ctx->red_out + 2 * MM_MAX_PARTIALS;
+    ctx->k1_dst = k1;
+    ctx->k1_decide.on = 1;
+    ctx->k1_decide.p = *p;
+    ctx->k1_decide.ds = ctx->dstep;
+    ctx->k1_decide.copy = dcopy;
+    rc = mm_run_project(ctx, p->rho, p->u_mean, 2, nullptr);
+    ctx->k1_dst = nullptr;
+    ctx->k1_decide.on = 0;
+    if (rc) return rc;
+    MM_CUDA(ctx, cudaEventRecord(ctx->ev_k1, ctx->stream));
+    ctx->gen++;  // (mm_update_and_sweep's) the front below is this call's
+    if ((rc = mm_run_update_pipe(ctx, p->material, p->rho, p->chunk, p->phi_scale))) return rc;
+    MM_CUDA(ctx, cudaEventSynchronize(ctx->ev_k1));
+    const double *hk1 = ctx->host_out + MM_MAX_PARTIALS;
+    const double r_d = p->rho * sqrt(hk1[0] / p->npts) / p->mu_rep;
+    const double r_p = sqrt(hk1[1] / p->npts);
+    out->r_d = r_d;
+    out->r_p = r_p;
+    double rho = p->rho;
+    bool swept = false;
+    double tol = 0.0;
+    if (!isfinite(r_p) || r_p > p->divergence_limit) {
+        out->diverged = 1;
+    } else {
+        if (p->adapt && p->outer_iter > 1) {
+            if (r_p > p->tau_adapt * r_d) {
+                rho *= p->kappa_adapt;
+            } else if (r_d > p->tau_adapt * r_p) {
+                const double a = rho / p->kappa_adapt;
+                rho = (p->rho_floor > a) ? p->rho_floor : a;
+            }
+        }
+        out->done = (r_p <= p->r_p_tol && r_d <= p->r_d_tol && p->r_l <= p->r_l_tol) ? 1 : 0;
+        if (!out->done) {
+            tol = p->point_tol;
+            if (p->ratio_policy) {
+                if (!isfinite(r_d)) tol = 1.0;
+                else {
+                    const double b = p->ratio * r_d;
+                    tol = (b > p->point_tol) ? b : p->point_tol;
+                }
+            }
+            tol *= p->mu_rep;
+            swept = true;
+        }
+    }
+    out->rho_next = out->diverged ? p->rho : rho;
+    mm_update_stats us;
+    memset(&us, 0, sizeof us);
+    if ((rc = mm_run_update_pipe_finish(ctx, swept, rho, ls, &us))) return rc;
+    // the fused pass ran with the device's decision: it must be this one
+    const double *hc = ctx->host_out + 2 * MM_MAX_PARTIALS;
+    const bool same = (hc[0] != 0.0) == !swept &&
+                      (!swept || (hc[1] == rho && hc[2] == tol)) &&
+                      (out->diverged || hc[1] == rho);
+    if (!same)
+        return mm_fail(ctx, MM_ERR_CONFIG,
+                       "pipelined step: device decision (skip %g, rho %.17g, tol %.17g) differs "
+                       "from the host's (skip %d, rho %.17g, tol %.17g)",
+                       hc[0], hc[1], hc[2], swept ? 0 : 1, rho, tol);
+    if (swept) {
+        out->swept = 1;
+    } else if ((rc = mm_update_multiplier(ctx, &us))) {
+        return rc;
+    }
+    memcpy(out->sum_lam, us.sum_lam, sizeof us.sum_lam);
+    return MM_OK;
+}
+
 // the decisions of solver.py's fused loop, in the Python loop's float order
 int mm_residuals_and_step(mm_ctx *ctx, const mm_step_params *p, mm_step_result *out,
                           mm_local_stats *ls) {
     if (!ctx || !p || !out || !ls) return MM_ERR_PARAM;
+    if (ctx->opt_pipeline && ctx->red_mapped && !ctx->slab_mode && !ctx->points_only &&
+        !p->last_allowed && ctx->have_sym && ctx->modA && p->chunk <= 64 &&
+        (p->material == MM_MAT_MR || p->material == MM_MAT_MR_DESCENT ||
+         p->material == MM_MAT_QUADRATIC) &&
+        p->rho > 0.0 && isfinite(p->rho)) {
+        memset(out, 0, sizeof *out);
+        memset(ls, 0, sizeof *ls);
+        MM_CUDA(ctx, cudaSetDevice(ctx->device));
+        return residuals_and_step_pipelined(ctx, p, out, ls);
+    }
     int rc = mm_project_residuals(ctx, p->rho, p->u_mean, &ctx->step_us);
     if (rc) return rc;
     const mm_update_stats &up = ctx->step_us;
@@ -1391,6 +1487,7 @@ int mm_set_option(mm_ctx *ctx, int option, int64_t value) {
         case MM_OPT_ROWINV_PIPE: ctx->opt_rowinv_p = value != 0; return MM_OK;
         case MM_OPT_SPECULATE: ctx->opt_speculate = value != 0; return MM_OK;
         case MM_OPT_ROWFWD_WARP: ctx->opt_rowfwd_w = value != 0; return MM_OK;
+        case MM_OPT_PIPELINE: ctx->opt_pipeline = value != 0; return MM_OK;
         default: return mm_fail(ctx, MM_ERR_PARAM, "unknown option %d", option);
     }
 }

@@ -17,6 +17,22 @@
 
 struct mm_bloch_state;
 
+// the next fused pass's parameters as the device decided them (k_decide)
+struct DevStep {
+    int skip;  // converged / diverged: the fused pass returns at once
+    int pad;
+    double rho_next, tol, tol_gs;
+};
+
+// mm_residuals_and_step's decision (a pipelined step), taken by the thread
+// that finalises K1's sums (decide_step below)
+struct DecideArgs {
+    int on;
+    mm_step_params p;
+    DevStep *ds;   // the next fused pass's parameters
+    double *copy;  // mapped: skip, rho_next, tol for the host's check
+};
+
 struct mm_ctx {
     int dim = 0, n = 0;
     double L = 0.0, h = 0.0;
@@ -84,6 +100,14 @@ struct mm_ctx {
     bool opt_rowinv_p = true;     // MM_OPT_ROWINV_PIPE
     bool opt_rowfwd_w = true;     // MM_OPT_ROWFWD_WARP
     bool red_mapped = false;      // red_out is host_out's device alias (mapped pinned memory)
+    // pipelined loop step (mm_residuals_and_step): K1 sums into a second
+    // mapped slot, the decision taken on the device (k_decide -> dstep) so the
+    // fused pass is queued behind K1 without a host round trip
+    bool opt_pipeline = true;     // MM_OPT_PIPELINE
+    double *k1_dst = nullptr;     // where K1's sums go (nullptr: red_out)
+    struct DevStep *dstep = nullptr;
+    struct DecideArgs k1_decide{};  // passed to K1 (on = 0: no decision)
+    cudaEvent_t ev_k1 = nullptr;
     bool opt_speculate = true;    // MM_OPT_SPECULATE
     // speculative projection front (A, column passes, E of the next
     // iteration launched by mm_update_and_sweep behind the fused pass): valid
@@ -212,8 +236,9 @@ __device__ __forceinline__ void block_reduce(double (&vals)[K], const int (&ops)
 // folds a contiguous range of blocks in order, then block_reduce combines the
 // threads in a fixed order => deterministic run to run.
 template <int K>
-__device__ void grid_finalize(const double (&vals)[K], const int (&ops)[K], double *partials,
-                              double *out, unsigned int *count, double *smem) {
+__device__ bool grid_finalize(const double (&vals)[K], const int (&ops)[K], double *partials,
+                              double *out, unsigned int *count, double *smem,
+                              double *final_vals = nullptr) {
     __shared__ bool is_last;
     const int nb = gridDim.x * gridDim.y * gridDim.z;
     const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
@@ -225,7 +250,7 @@ __device__ void grid_finalize(const double (&vals)[K], const int (&ops)[K], doub
         is_last = (t == (unsigned int)(nb - 1));
     }
     __syncthreads();
-    if (!is_last) return;
+    if (!is_last) return false;
     __threadfence();
     const int nt = blockDim.x;
     const int per = (nb + nt - 1) / nt;
@@ -244,7 +269,65 @@ __device__ void grid_finalize(const double (&vals)[K], const int (&ops)[K], doub
 #pragma unroll
         for (int k = 0; k < K; ++k) out[k] = acc[k];
         *count = 0u;
+        if (final_vals) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) final_vals[k] = acc[k];
+        }
+        return true;
     }
+    return false;
+}
+
+// decide_step: statement for statement the host's code, with no sums of
+// products, so no contraction can make the two differ
+__device__ inline double gs_threshold_dev(double tol) {  // gs_threshold (mm_local.cu)
+    if (tol != tol) return tol;
+    if (tol < 0.0) return -INFINITY;
+    if (tol == 0.0 || isinf(tol)) return tol;
+    double x = tol * tol;
+    while (x > 0.0 && sqrt(x) > tol) x = nextafter(x, 0.0);
+    while (sqrt(nextafter(x, INFINITY)) <= tol) x = nextafter(x, INFINITY);
+    return x;
+}
+
+__device__ inline void decide_step(double sum_dG2, double sum_mis2, const DecideArgs &a) {
+    const mm_step_params &p = a.p;
+    const double r_d = p.rho * sqrt(sum_dG2 / p.npts) / p.mu_rep;
+    const double r_p = sqrt(sum_mis2 / p.npts);
+    DevStep d{};
+    double rho = p.rho;
+    if (!isfinite(r_p) || r_p > p.divergence_limit) {
+        d.skip = 1;
+    } else {
+        if (p.adapt && p.outer_iter > 1) {
+            if (r_p > p.tau_adapt * r_d) {
+                rho *= p.kappa_adapt;
+            } else if (r_d > p.tau_adapt * r_p) {
+                const double q = rho / p.kappa_adapt;
+                rho = (p.rho_floor > q) ? p.rho_floor : q;
+            }
+        }
+        const bool done = r_p <= p.r_p_tol && r_d <= p.r_d_tol && p.r_l <= p.r_l_tol;
+        if (done) {
+            d.skip = 1;
+        } else {
+            double tol = p.point_tol;
+            if (p.ratio_policy) {
+                if (!isfinite(r_d)) tol = 1.0;
+                else {
+                    const double b = p.ratio * r_d;
+                    tol = (b > p.point_tol) ? b : p.point_tol;
+                }
+            }
+            d.tol = tol * p.mu_rep;
+            d.tol_gs = gs_threshold_dev(d.tol);
+        }
+    }
+    d.rho_next = rho;
+    *a.ds = d;
+    a.copy[0] = d.skip;
+    a.copy[1] = d.rho_next;
+    a.copy[2] = d.tol;
 }
 
 // periodic neighbour offsets of point p (< 2^31) along each axis; lgn = log2 n
@@ -393,5 +476,9 @@ int mm_slab_alloc_director(mm_ctx *ctx);
 int mm_materialize_G(mm_ctx *ctx);
 int mm_ensure_points(mm_ctx *ctx);
 int mm_flush_pending(mm_ctx *ctx);
+int mm_run_update_pipe(mm_ctx *ctx, int material, double rho_placeholder, int64_t max_sweeps,
+                       double phi_scale);
+int mm_run_update_pipe_finish(mm_ctx *ctx, bool swept, double rho_next, mm_local_stats *ls,
+                              mm_update_stats *us);
 int mm_run_update(mm_ctx *ctx, int material, double rho_next, double tol, int64_t max_sweeps,
                   double phi_scale, int want_points, mm_local_stats *ls, mm_update_stats *us);

@@ -634,8 +634,14 @@ k_update_local(double *__restrict__ F, double *__restrict__ Lam, double *__restr
                const double *__restrict__ modA, const double *__restrict__ modB, int64_t M,
                double rho_k, double rho, double tol, double tol_gs, double phi_scale, int chunk,
                double *__restrict__ res_out, int32_t *__restrict__ nsw_out, double *partials,
-               double *red_out, unsigned int *count) {
+               double *red_out, unsigned int *count, const DevStep *__restrict__ ds) {
     constexpr int K = 5 + 2 * D;  // ..., last slot: sum of per-point sweeps
+    if (ds) {  // pipelined step: parameters decided on the device
+        if (ds->skip) return;  // every block, before any side effect
+        rho = ds->rho_next;
+        tol = ds->tol;
+        tol_gs = ds->tol_gs;
+    }
     // MM_B_SMEM: B = lam + rho G and lam_{k+1} (for the T store) live in
     // per-thread shared-memory columns across the sweeps; the block
     // reduction's scratch reuses that space after the loop
@@ -1034,7 +1040,7 @@ constexpr bool kFusedStoresG = false;
 
 template <int MAT, int D, int ALGO, bool SWEEP>
 static int launch_update_local(mm_ctx *ctx, double rho_next, double tol, double phi_scale,
-                               int chunk, bool want_points) {
+                               int chunk, bool want_points, const DevStep *ds = nullptr) {
     const int blocks = local_blocks(ctx->M);
     int rc = mm_ensure_partials(ctx, blocks);
     if (rc) return rc;
@@ -1052,11 +1058,11 @@ static int launch_update_local(mm_ctx *ctx, double rho_next, double tol, double 
     k_update_local<MAT, D, ALGO, SWEEP><<<blocks, LOCAL_THREADS, 0, ctx->stream>>>(
         ctx->F, ctx->Lam, kFusedStoresG ? ctx->G : nullptr, Tout, mm_gsrc(ctx), ctx->modA, MAT == MAT_MR ? ctx->modB : ctx->modA, ctx->M,
         ctx->pending_rho, rho_next, tol, gs_threshold(tol), phi_scale, chunk, want_points ? ctx->res : nullptr,
-        want_points ? ctx->nsw : nullptr, ctx->partials, ctx->red_out, ctx->red_count);
+        want_points ? ctx->nsw : nullptr, ctx->partials, ctx->red_out, ctx->red_count, ds);
     MM_LAUNCH_CHECK(ctx);
     if (Tout) {
         ctx->T_valid = true;
-        ctx->T_rho = rho_next;
+        ctx->T_rho = rho_next;  // pipelined: a placeholder until the decision is read
     }
     return MM_OK;
 }
@@ -1128,6 +1134,74 @@ int mm_run_update(mm_ctx *ctx, int material, double rho_next, double tol, int64_
         ls->sum_nsw = r[K - 1];
         if (want_points) MM_CUDA(ctx, cudaMemsetAsync(ctx->ok, 0, ctx->M, ctx->stream));
     }
+    return MM_OK;
+}
+
+// Pipelined step (mm_residuals_and_step): the pending ascent fused with the
+// next first local chunk, with rho_next / tol read from ctx->dstep (k_decide,
+// queued behind K1), then the speculative projection front; nothing waits.
+// mm_run_update_pipe_finish takes the host's (identical) decision: swept ->
+// the pass ran (its sums are read), else it returned at once, the ascent is
+// still pending and the front is void.
+int mm_run_update_pipe(mm_ctx *ctx, int material, double rho_placeholder, int64_t max_sweeps,
+                       double phi_scale) {
+    int rc;
+    if (!ctx->lam_pending)
+        return mm_fail(ctx, MM_ERR_CONFIG, "no multiplier update pending (call mm_project_residuals)");
+    if (max_sweeps > 64) return mm_fail(ctx, MM_ERR_CONFIG, "fused local chunk limited to 64 sweeps");
+    const DevStep *ds = ctx->dstep;
+    const double r = rho_placeholder;
+    if (material == MM_MAT_MR_DESCENT || (material == MM_MAT_MR && ctx->dim == 3))
+        rc = ctx->dim == 2 ? launch_update_local<MAT_MR, 4, 0, true>(ctx, r, 0.0, phi_scale, (int)max_sweeps, false, ds)
+                           : launch_update_local<MAT_MR, 9, 0, true>(ctx, r, 0.0, phi_scale, (int)max_sweeps, false, ds);
+    else if (material == MM_MAT_MR)
+        rc = launch_update_local<MAT_MR, 4, 1, true>(ctx, r, 0.0, phi_scale, (int)max_sweeps, false, ds);
+    else if (material == MM_MAT_QUADRATIC)
+        rc = ctx->dim == 2 ? launch_update_local<MAT_QUAD, 4, 0, true>(ctx, r, 0.0, phi_scale, (int)max_sweeps, false, ds)
+                           : launch_update_local<MAT_QUAD, 9, 0, true>(ctx, r, 0.0, phi_scale, (int)max_sweeps, false, ds);
+    else
+        return mm_fail(ctx, MM_ERR_CONFIG, "material %d has no fused local chunk", material);
+    if (rc) return rc;
+    if (!ctx->ev_red) MM_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_red, cudaEventDisableTiming));
+    MM_CUDA(ctx, cudaEventRecord(ctx->ev_red, ctx->stream));
+    ctx->front_valid = false;
+    if (ctx->opt_speculate && ctx->have_sym && ctx->T_valid && ctx->T_rho == rho_placeholder) {
+        double *u_new = nullptr;
+        if ((rc = mm_run_project_front(ctx, rho_placeholder, 2, &u_new))) return rc;
+        ctx->front_valid = true;  // confirmed (or voided) by the finish
+    }
+    return MM_OK;
+}
+
+int mm_run_update_pipe_finish(mm_ctx *ctx, bool swept, double rho_next, mm_local_stats *ls,
+                              mm_update_stats *us) {
+    MM_CUDA(ctx, cudaEventSynchronize(ctx->ev_red));
+    if (!swept) {
+        ctx->T_valid = false;
+        ctx->front_valid = false;
+        return MM_OK;
+    }
+    const int D = ctx->D;
+    ctx->lam_pending = false;
+    if (kFusedStoresG) {
+        ctx->g_implicit = false;
+        ctx->g_buf_valid = true;
+    }
+    if (ctx->T_valid) ctx->T_rho = rho_next;
+    if (ctx->front_valid) {
+        ctx->front_rho = rho_next;
+        ctx->front_gen = ctx->gen;
+    }
+    const int K = 5 + 2 * D;
+    double r[MM_MAX_PARTIALS];
+    memcpy(r, ctx->host_out, sizeof(double) * K);
+    for (int i = 0; i < 9; ++i) us->sum_lam[i] = i < D ? r[4 + D + i] : 0.0;
+    ls->sum_res2 = r[0];
+    ls->n_conv = (int64_t)r[1];
+    ls->sweeps = ctx->M ? (int64_t)r[2] : 0;
+    for (int i = 0; i < 9; ++i) ls->sum_F[i] = i < D ? r[4 + i] : 0.0;
+    ls->sum_nsw = r[K - 1];
+    mm_drain_timings(ctx);
     return MM_OK;
 }
 

@@ -1823,7 +1823,7 @@ __global__ void __launch_bounds__(256)
 k_grad(const double *__restrict__ Ut, const double *__restrict__ Uold, double *__restrict__ G,
        const double *__restrict__ F, double *__restrict__ Lam, int n, int lgn, int64_t M,
        double inv2h, double rho, Mean9 um, Mean9 um_old, double *partials, double *red_out,
-       unsigned int *count, int64_t uM, int wrap0) {
+       unsigned int *count, int64_t uM, int wrap0, const DecideArgs dec) {
     constexpr int D = DIM * DIM;
     constexpr int K = 2 + D;
     __shared__ double smem[32 * K];
@@ -1894,7 +1894,9 @@ k_grad(const double *__restrict__ Ut, const double *__restrict__ Uold, double *_
 #pragma unroll
         for (int k = 0; k < K; ++k) ops[k] = RED_SUM;
         block_reduce<K>(acc, ops, smem);
-        grid_finalize<K>(acc, ops, partials, red_out, count, smem);
+        double fin[K];
+        if (grid_finalize<K>(acc, ops, partials, red_out, count, smem, fin) && dec.on)
+            decide_step(fin[0], fin[1], dec);
     }
 }
 
@@ -1933,7 +1935,8 @@ __device__ __forceinline__ void ring_cell(int r, int x0, int y0, int n, int &off
 __global__ void __launch_bounds__(RT_X * RT_Y, 2)
 k_res_march(const double *__restrict__ Un, const double *__restrict__ Uo,
             const double *__restrict__ F, int n, int64_t M, double inv2h, Mean9 um, Mean9 umo,
-            double *partials, double *red_out, unsigned int *count, int64_t uM, int wrap0) {
+            double *partials, double *red_out, unsigned int *count, int64_t uM, int wrap0,
+            const DecideArgs dec) {
     __shared__ double sm[2][3][RT_Y + 2][RT_X + 2];
     __shared__ double red_sm[32 * 2];
     // 1D block (block_reduce / grid_finalize index threads by threadIdx.x)
@@ -2028,7 +2031,9 @@ k_res_march(const double *__restrict__ Un, const double *__restrict__ Uo,
     }
     const int ops[2] = {RED_SUM, RED_SUM};
     block_reduce<2>(acc, ops, red_sm);
-    grid_finalize<2>(acc, ops, partials, red_out, count, red_sm);
+    double fin[2];
+    if (grid_finalize<2>(acc, ops, partials, red_out, count, red_sm, fin) && dec.on)
+        decide_step(fin[0], fin[1], dec);
 }
 
 // stencil divergence of F into Ut: (div F)_i = sum_j (F_ij(x+e_j) - F_ij(x-e_j)) / (2h)
@@ -2521,12 +2526,15 @@ int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
                      : update == 2 ? (ctx->g_implicit ? GRAD_RES_IMPL : GRAD_RES_EXPL)
                      : !ctx->opt_implicit_g ? GRAD_EXPLW
                      : (ctx->g_implicit ? GRAD_IMPL : GRAD_EXPL);
+    double *rout = ctx->k1_dst ? ctx->k1_dst : ctx->red_out;  // pipelined step: second slot
+    DecideArgs dec = ctx->k1_decide;
+    if (update != 2) dec.on = 0;
 #define LAUNCH(DIM, MODE)                                                                       \
     k_grad<DIM, MODE><<<blocks, threads, 0, ctx->stream>>>(u_new, ctx->Ut, ctx->G, ctx->F,       \
                                                            ctx->Lam, n, lgn, ctx->M, inv2h, rho, \
-                                                           um, umo, ctx->partials, ctx->red_out, \
+                                                           um, umo, ctx->partials, rout,         \
                                                            ctx->red_count, ctx->uM,              \
-                                                           ctx->slab_mode ? 0 : 1)
+                                                           ctx->slab_mode ? 0 : 1, dec)
     const int nplanes = ctx->slab_mode ? ctx->slab_nl : n;
     const bool march = d == 3 && mode == GRAD_RES_IMPL && n % RT_X == 0 && n % RT_Y == 0 &&
                        nplanes % RT_ZC == 0 && ctx->opt_march;
@@ -2535,8 +2543,8 @@ int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
         dim3 grid(n / RT_X, n / RT_Y, nplanes / RT_ZC);
         if ((rc = mm_ensure_partials(ctx, (int64_t)grid.x * grid.y * grid.z))) return rc;
         k_res_march<<<grid, RT_X * RT_Y, 0, ctx->stream>>>(
-            u_new, ctx->Ut, ctx->F, n, ctx->M, inv2h, um, umo, ctx->partials, ctx->red_out,
-            ctx->red_count, ctx->uM, ctx->slab_mode ? 0 : 1);
+            u_new, ctx->Ut, ctx->F, n, ctx->M, inv2h, um, umo, ctx->partials, rout,
+            ctx->red_count, ctx->uM, ctx->slab_mode ? 0 : 1, dec);
     } else {
         StageScope ss(ctx, MM_STAGE_GRAD);
         if (d == 2) {
@@ -2578,6 +2586,7 @@ int mm_run_project(mm_ctx *ctx, double rho, const double *u_mean, int update,
         ctx->lam_pending = true;  // lam += rho (grad_u - F) deferred (mm_run_update)
         ctx->pending_rho = rho;
     }
+    if (!out) return MM_OK;  // pipelined step: the sums are read later (k1_dst)
     double r[MM_MAX_PARTIALS];
     const int K = 2 + ctx->D;
     if ((rc = mm_fetch_reduction(ctx, K, r))) return rc;
@@ -2673,11 +2682,11 @@ int mm_materialize_G(mm_ctx *ctx) {
         if (ctx->dim == 2)
             k_grad<2, GRAD_WRITE><<<blocks, threads, 0, ctx->stream>>>(
                 ctx->Ut, ctx->Ut, ctx->G, ctx->F, ctx->Lam, ctx->n, lgn, ctx->M, inv2h, 0.0, um,
-                umo, nullptr, nullptr, nullptr, ctx->uM, ctx->slab_mode ? 0 : 1);
+                umo, nullptr, nullptr, nullptr, ctx->uM, ctx->slab_mode ? 0 : 1, DecideArgs{});
         else
             k_grad<3, GRAD_WRITE><<<blocks, threads, 0, ctx->stream>>>(
                 ctx->Ut, ctx->Ut, ctx->G, ctx->F, ctx->Lam, ctx->n, lgn, ctx->M, inv2h, 0.0, um,
-                umo, nullptr, nullptr, nullptr, ctx->uM, ctx->slab_mode ? 0 : 1);
+                umo, nullptr, nullptr, nullptr, ctx->uM, ctx->slab_mode ? 0 : 1, DecideArgs{});
     }
     MM_LAUNCH_CHECK(ctx);
     ctx->g_buf_valid = true;
@@ -2695,11 +2704,11 @@ int mm_run_stencil(mm_ctx *ctx, int op) {
         if (ctx->dim == 2)
             k_grad<2, GRAD_WRITE><<<blocks, threads, 0, ctx->stream>>>(
                 ctx->Ut, ctx->Ut, ctx->G, ctx->F, ctx->Lam, ctx->n, ilog2_(ctx->n), ctx->M, inv2h,
-                0.0, um, um, nullptr, nullptr, nullptr, ctx->uM, 1);
+                0.0, um, um, nullptr, nullptr, nullptr, ctx->uM, 1, DecideArgs{});
         else
             k_grad<3, GRAD_WRITE><<<blocks, threads, 0, ctx->stream>>>(
                 ctx->Ut, ctx->Ut, ctx->G, ctx->F, ctx->Lam, ctx->n, ilog2_(ctx->n), ctx->M, inv2h,
-                0.0, um, um, nullptr, nullptr, nullptr, ctx->uM, 1);
+                0.0, um, um, nullptr, nullptr, nullptr, ctx->uM, 1, DecideArgs{});
         ctx->g_implicit = false;
         ctx->g_buf_valid = true;
     } else {
@@ -2894,7 +2903,7 @@ int mm_slab_res(mm_ctx *ctx, double rho, const double *u_mean, double *sums) {
             if ((rc = mm_ensure_partials(ctx, (int64_t)grid.x * grid.y * grid.z))) return rc;
             k_res_march<<<grid, RT_X * RT_Y, 0, ctx->stream>>>(
                 u_new, ctx->Ut, ctx->F, n, ctx->M, inv2h, um, umo, ctx->partials, ctx->red_out,
-                ctx->red_count, ctx->uM, 0);
+                ctx->red_count, ctx->uM, 0, DecideArgs{});
         } else {
             const int threads = 256;
             const int blocks = (int)std::min<int64_t>((ctx->M + threads - 1) / threads, 148 * 8);
@@ -2902,11 +2911,11 @@ int mm_slab_res(mm_ctx *ctx, double rho, const double *u_mean, double *sums) {
             if (mode == GRAD_RES_IMPL)
                 k_grad<3, GRAD_RES_IMPL><<<blocks, threads, 0, ctx->stream>>>(
                     u_new, ctx->Ut, ctx->G, ctx->F, ctx->Lam, n, lgn, ctx->M, inv2h, rho, um, umo,
-                    ctx->partials, ctx->red_out, ctx->red_count, ctx->uM, 0);
+                    ctx->partials, ctx->red_out, ctx->red_count, ctx->uM, 0, DecideArgs{});
             else
                 k_grad<3, GRAD_RES_EXPL><<<blocks, threads, 0, ctx->stream>>>(
                     u_new, ctx->Ut, ctx->G, ctx->F, ctx->Lam, n, lgn, ctx->M, inv2h, rho, um, umo,
-                    ctx->partials, ctx->red_out, ctx->red_count, ctx->uM, 0);
+                    ctx->partials, ctx->red_out, ctx->red_count, ctx->uM, 0, DecideArgs{});
         }
     }
     MM_LAUNCH_CHECK(ctx);

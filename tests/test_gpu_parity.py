@@ -513,9 +513,10 @@ def test_speculative_projection_front_is_exact(n, K, monkeypatch):
                                        (2, 16, "fraction")])
 def test_library_decision_step_matches_host_loop(dim, n, pol, monkeypatch):
     """mm_residuals_and_step takes the loop's decisions (r_d, r_p, guard,
-    penalty update, convergence, policy tolerance) in the library; fields,
-    history and sweeps equal the host-decided loop (MM_HOST_DECIDE=1) bit for
-    bit, through convergence."""
+    penalty update, convergence, policy tolerance) in the library -- on the
+    device, ahead of the host, when pipelined; fields, history and sweeps
+    equal the host-decided loop (MM_HOST_DECIDE=1) bit for bit, through
+    convergence."""
     grid, mu, kap = _laminate(dim, n, 0)
     Fbar = np.eye(dim)
     Fbar[0, 0] = 0.95
@@ -525,17 +526,20 @@ def test_library_decision_step_matches_host_loop(dim, n, pol, monkeypatch):
               "fraction": mm.FractionConverged(0.9, 2)}[pol]
     params = mm.SolverParams(max_outer=400)
     out = {}
-    # "0": the library loop (mm_solve_fused); "py": the Python loop over
-    # mm_residuals_and_step; "1": the host-decided loop
-    for flag in ("0", "py", "1"):
+    # "0": the library loop (mm_solve_fused; K1, the device-side decision and
+    # the next fused pass queued back to back, MM_OPT_PIPELINE); "nopipe": the
+    # same with the host deciding between K1 and the fused pass; "py": the
+    # Python loop over mm_residuals_and_step; "1": the host-decided loop
+    for flag in ("0", "nopipe", "py", "1"):
         monkeypatch.setenv("MM_HOST_DECIDE", "1" if flag == "1" else "0")
         monkeypatch.setenv("MM_C_LOOP", "0" if flag == "py" else "1")
+        monkeypatch.setenv("MM_PIPELINE", "0" if flag == "nopipe" else "1")
         st = mm.solver.init_state(grid, m, bc, params)
         st.F = st.F + 1e-3 * np.random.default_rng(1).standard_normal(st.F.shape)
         st, conv = mm.solve(grid, m, bc, params, policy=policy, state=st, raise_on_max=False)
         out[flag] = (conv, [np.array(getattr(st, k)) for k in ("F", "lam", "grad_u", "u_tilde")],
                      [r[:5] for r in st.history], st.total_sweeps, st.rho)
-    for other in ("py", "1"):
+    for other in ("nopipe", "py", "1"):
         a, b = out["0"], out[other]
         assert a[0] == b[0] and a[2] == b[2] and a[3] == b[3] and a[4] == b[4]
         for x, y in zip(a[1], b[1]):
