@@ -1909,7 +1909,13 @@ k_grad(const double *__restrict__ Ut, const double *__restrict__ Uold, double *_
 // (plus the ring), instead of seven times through L1/L2 as in k_grad, whose
 // axis-0 neighbours miss in L2 (ncu: 1.5x the algorithmic DRAM bytes).
 // The per-voxel arithmetic is k_grad's, in the same order.
-constexpr int RT_X = 32, RT_Y = 8, RT_ZC = 32;
+#ifndef MM_RES_ZC
+#define MM_RES_ZC 32
+#endif
+#ifndef MM_RES_MINB
+#define MM_RES_MINB 2
+#endif
+constexpr int RT_X = 32, RT_Y = 8, RT_ZC = MM_RES_ZC;
 constexpr int RT_RING = 2 * RT_X + 2 * RT_Y;  // ring cells per plane (no corners needed)
 
 // ring cell r of the tile at plane offset `pl`: rows y0-1 / y0+RT_Y, then
@@ -1932,7 +1938,7 @@ __device__ __forceinline__ void ring_cell(int r, int x0, int y0, int n, int &off
     }
 }
 
-__global__ void __launch_bounds__(RT_X * RT_Y, 2)
+__global__ void __launch_bounds__(RT_X * RT_Y, MM_RES_MINB)
 k_res_march(const double *__restrict__ Un, const double *__restrict__ Uo,
             const double *__restrict__ F, int n, int64_t M, double inv2h, Mean9 um, Mean9 umo,
             double *partials, double *red_out, unsigned int *count, int64_t uM, int wrap0,
