@@ -510,7 +510,7 @@ def test_speculative_projection_front_is_exact(n, K, monkeypatch):
 
 
 @pytest.mark.parametrize("dim,n,pol", [(2, 32, "ratio"), (3, 16, "ratio"), (3, 16, "exact"),
-                                       (2, 16, "fraction")])
+                                       (2, 16, "fraction"), (3, 16, "mixed")])
 def test_library_decision_step_matches_host_loop(dim, n, pol, monkeypatch):
     """mm_residuals_and_step takes the loop's decisions (r_d, r_p, guard,
     penalty update, convergence, policy tolerance) in the library -- on the
@@ -521,9 +521,13 @@ def test_library_decision_step_matches_host_loop(dim, n, pol, monkeypatch):
     Fbar = np.eye(dim)
     Fbar[0, 0] = 0.95
     bc = mm.MacroBC.strain(Fbar)
+    if pol == "mixed":  # F_00 prescribed, the other entries stress-free (u_mean from sum F)
+        bc = mm.MacroBC.mixed({(0, 0): 0.95},
+                              {(i, j): 0.0 for i in range(dim) for j in range(dim)
+                               if (i, j) != (0, 0)}, dim)
     m = mm.MooneyRivlin(mu, kap, dim=dim, mu_rep=1.0)
     policy = {"ratio": mm.RatioToDual(0.3), "exact": mm.ExactAll(),
-              "fraction": mm.FractionConverged(0.9, 2)}[pol]
+              "fraction": mm.FractionConverged(0.9, 2), "mixed": mm.RatioToDual(0.3)}[pol]
     params = mm.SolverParams(max_outer=400)
     out = {}
     # "0": the library loop (mm_solve_fused; K1, the device-side decision and
