@@ -50,6 +50,14 @@ namespace {
 #ifndef MM_ROWFWD_REGS
 #define MM_ROWFWD_REGS 96
 #endif
+#ifndef MM_LM_TWP
+#define MM_LM_TWP 1  // plane row passes: twiddles from 4 loads + products (tile_fft_lm256): 0.475 -> 0.457 ms
+#endif
+#ifndef MM_PLANE_COLSWZ
+// 1: n = 256 column pass on 128-byte swizzled tiles (plane_col_swz): measured
+// 0.51 vs 0.485 ms and it costs the default kernel registers, so not built
+#define MM_PLANE_COLSWZ 0
+#endif
 #ifndef MM_ROWFWD_W
 #define MM_ROWFWD_W 1  // n = 256: the warp-per-task R2C rows (k_row_fwd_w)
 #endif
@@ -1497,7 +1505,7 @@ __device__ __forceinline__ void plane_col_tma(const CUtensorMap *map, int plane,
                                               const double2 *__restrict__ tw, bool swz) {
     using C = PlaneCfg<N1, N2, TK>;
     constexpr int N = C::N, NT = C::NT, IT = C::IT, LD = TK;
-    if constexpr (N == 256 && TK == 8 && NT == 128) {
+    if constexpr (MM_PLANE_COLSWZ && N == 256 && TK == 8 && NT == 128) {
         if (swz) {  // 16 lanes per column on the swizzled tile, no block barrier
             plane_col_swz(map, plane, smem, bars, phase, t0, t1, g, k2, tw);
             return;
@@ -1578,12 +1586,38 @@ __device__ __forceinline__ void tile_fft_lm256(double2 *buf, const double2 *__re
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = L[lm_swz(r, q)];
     __syncwarp();
+#if MM_LM_TWP
+    // W^{q r}: four table loads (r = 1, 2, 4, 8) and products, as
+    // stockham_pass's MM_TW_PROD (fewer dependent loads in the LSU queue)
+    {
+        double2 w[16];
+        w[1] = __ldg(&tw[q]);
+        w[2] = __ldg(&tw[2 * q]);
+        w[4] = __ldg(&tw[4 * q]);
+        w[8] = __ldg(&tw[8 * q]);
+        if (inv) {
+            w[1].y = -w[1].y;
+            w[2].y = -w[2].y;
+            w[4].y = -w[4].y;
+            w[8].y = -w[8].y;
+        }
+        w[3] = cmul(w[1], w[2]);
+        w[5] = cmul(w[1], w[4]);
+        w[6] = cmul(w[2], w[4]);
+        w[7] = cmul(w[3], w[4]);
+#pragma unroll
+        for (int r = 9; r < 16; ++r) w[r] = cmul(w[r - 8], w[8]);
+#pragma unroll
+        for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], w[r]);
+    }
+#else
 #pragma unroll
     for (int r = 1; r < 16; ++r) {
         double2 w = __ldg(&tw[q * r]);
         if (inv) w.y = -w.y;
         v[r] = cmul(v[r], w);
     }
+#endif
     fft_reg_rt<16>(v, inv);
 #pragma unroll
     for (int r = 0; r < 16; ++r) L[q + 16 * r] = v[r];
@@ -2258,9 +2292,6 @@ int run_col(mm_ctx *ctx, const ColGeom &g, int n_outer) {
 #ifndef MM_PLANE_TMA  // 1: pass 2 of the plane FFT through TMA + mbarrier (plane_col_tma);
 #define MM_PLANE_TMA 2  // 2: passes 1 and 3 too at n = 256 (plane_row_tma)
 #endif
-#ifndef MM_PLANE_COLSWZ
-#define MM_PLANE_COLSWZ 0  // 1: n = 256 column pass on 128-byte swizzled tiles (plane_col_swz; measured slower)
-#endif
 
 // Tensor map of the plane-layout spectrum for plane_col_tma: doubles, dims
 // {2N (re/im along axis 1), N (axis 0), planes}, box {2 TK, N, 1}.  Encoded
@@ -2330,10 +2361,8 @@ int run_plane_t(mm_ctx *ctx, const PlaneGeom &g) {
     int use_tma = 0;
     if (C::PPT == 16 && MM_PLANE_TMA) {
         // use_tma == 3 <=> the column map is swizzled (plane_col_swz)
-        // MM_PLANE_COLSWZ in the environment overrides the build default (per call: tests)
-        const char *cs_env = getenv("MM_PLANE_COLSWZ");
-        const bool colswz = cs_env && *cs_env ? atoi(cs_env) != 0 : MM_PLANE_COLSWZ != 0;
-        const bool swz = MM_PLANE_TMA >= 2 && colswz && C::N == 256 && TK == 8 && C::NT == 128;
+        const bool swz =
+            MM_PLANE_TMA >= 2 && MM_PLANE_COLSWZ && C::N == 256 && TK == 8 && C::NT == 128;
         if ((rc = mm_plane_tensor_map(ctx, C::N, TK, swz))) return rc;
         use_tma = ctx->tmap_ok ? 1 : 0;
         if (use_tma && MM_PLANE_TMA >= 2 && C::N == 256 && TK == 8 && C::NT == 128 &&

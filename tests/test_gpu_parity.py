@@ -416,33 +416,6 @@ def test_row_fwd_warp_kernel_matches_tiled():
     np.testing.assert_allclose(out["1"][1][1:], out["0"][1][1:], rtol=1e-11)
 
 
-def test_plane_column_swizzle_variant():
-    """n = 256: the column pass on 128-byte swizzled TMA tiles with the
-    in-warp FFT (MM_PLANE_COLSWZ=1, csrc/mm_project.cu col_fft_solve_256)
-    against the default block-level column FFT: the same transform in another
-    summation order, so whole outer iterations agree to roundoff."""
-    import os
-    grid, mu, kap = _laminate(3, 256, 0)
-    bc = mm.MacroBC.strain(np.diag([0.95, 1.0, 1.0]))
-    m = mm.MooneyRivlin(mu, kap, dim=3, mu_rep=1.0)
-    params = mm.SolverParams(max_outer=2)
-    out = {}
-    for flag in ("1", "0"):
-        os.environ["MM_PLANE_COLSWZ"] = flag
-        try:
-            st = mm.solver.init_state(grid, m, bc, params)
-            st.F = st.F + 1e-4 * np.random.default_rng(0).standard_normal(st.F.shape)
-            st, _ = mm.solve(grid, m, bc, params, policy=mm.RatioToDual(0.3), state=st,
-                             raise_on_max=False)
-        finally:
-            del os.environ["MM_PLANE_COLSWZ"]
-        out[flag] = (st.F.copy(), st.lam.copy(), st.u_tilde.copy(), st.history[-1][:5])
-        del st
-    for a, b in zip(out["1"][:3], out["0"][:3]):
-        assert rel_l2(a, b) < 1e-13
-    np.testing.assert_allclose(out["1"][3][1:], out["0"][3][1:], rtol=1e-11)
-
-
 def test_solve_updates_caller_F_and_lam_in_place():
     """The reference's local step writes F in place (base.py:109-111) and the
     ascent does lam += ... (solver.py:279): arrays the caller handed in as F
