@@ -380,7 +380,7 @@ enum mm_option {
                              * uses them if no other call intervened and rho matches */
     MM_OPT_ROWFWD_WARP = 6, /* default 1: single-GPU n = 256 R2C rows with one warp per
                              * 4-row task (k_row_fwd_w): the block-tiled kernel's four-step
-                             * in the same order (bitwise equal) */
+                             * in the same order (equal to roundoff) */
     MM_OPT_PIPELINE = 7     /* default 1: mm_residuals_and_step queues K1, the decision (on
                              * the device) and the next fused pass back to back; the host
                              * takes the same decision and checks it (bitwise equal loop) */

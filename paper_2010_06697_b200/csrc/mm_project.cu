@@ -50,6 +50,9 @@ namespace {
 #ifndef MM_ROWFWD_REGS
 #define MM_ROWFWD_REGS 96
 #endif
+#ifndef MM_RFW_TWP
+#define MM_RFW_TWP 1  // k_row_fwd_w: twiddles from 4 loads + products (0.375 -> 0.353 ms; 0: bitwise = k_row_fwd)
+#endif
 #ifndef MM_LM_TWP
 #define MM_LM_TWP 1  // plane row passes: twiddles from 4 loads + products (tile_fft_lm256): 0.475 -> 0.457 ms
 #endif
@@ -765,8 +768,24 @@ k_row_fwd_w(const double *__restrict__ T, double2 *__restrict__ spec, RowGeom g,
     // step 1 (tile_fft<16, 8>): n2 = q, 16 points x[8 n1 + q]
     fft_reg<16, false>(v);
     if (q != 0) {
+#if MM_RFW_TWP
+        double2 w[16];  // W^{q k1} from four loads and products (MM_TW_PROD's scheme)
+        w[1] = __ldg(&tw[q]);
+        w[2] = __ldg(&tw[2 * q]);
+        w[4] = __ldg(&tw[4 * q]);
+        w[8] = __ldg(&tw[8 * q]);
+        w[3] = cmul(w[1], w[2]);
+        w[5] = cmul(w[1], w[4]);
+        w[6] = cmul(w[2], w[4]);
+        w[7] = cmul(w[3], w[4]);
+#pragma unroll
+        for (int r = 9; r < 16; ++r) w[r] = cmul(w[r - 8], w[8]);
+#pragma unroll
+        for (int k1 = 1; k1 < 16; ++k1) v[k1] = cmul(v[k1], w[k1]);
+#else
 #pragma unroll
         for (int k1 = 1; k1 < 16; ++k1) v[k1] = cmul(v[k1], __ldg(&tw[q * k1]));
+#endif
     }
     double2 *L = sm[warp][j];
     // element (k1, n2) of the exchange at k1 * 8 + (n2 ^ (k1 & 7))

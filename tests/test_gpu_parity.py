@@ -387,9 +387,10 @@ def test_plane_fft_matches_row_layout(n, monkeypatch):
 def test_row_fwd_warp_kernel_matches_tiled():
     """n = 256: the warp-per-task R2C rows (k_row_fwd_w, MM_OPT_ROWFWD_WARP)
     perform tile_fft<16, 8>'s four-step and k_row_fwd's stencil and split in
-    the same order; whole outer iterations agree with the block-tiled kernel
-    to roundoff (the compiler may contract complex products differently;
-    measured: bit for bit), sweep counts exactly."""
+    the same order, with the step-1 twiddles formed from four table loads and
+    products (MM_RFW_TWP; with table twiddles the two kernels agree bit for
+    bit); whole outer iterations agree with the block-tiled kernel to
+    roundoff, sweep counts exactly."""
     import os
     grid, mu, kap = _laminate(3, 256, 0)
     bc = mm.MacroBC.strain(np.diag([0.95, 1.0, 1.0]))
