@@ -130,9 +130,12 @@ static double gs_threshold(double tol) {
     return x;
 }
 
+#ifndef MM_LOCAL_GRID
+#define MM_LOCAL_GRID 16  // grid-stride blocks per SM (x 128 / LOCAL_THREADS)
+#endif
 inline int local_blocks(int64_t M) {
     int64_t b = (M + LOCAL_THREADS - 1) / LOCAL_THREADS;
-    return (int)std::min<int64_t>(b, 148 * 16 * 128 / LOCAL_THREADS);
+    return (int)std::min<int64_t>(b, 148 * MM_LOCAL_GRID * 128 / LOCAL_THREADS);
 }
 
 // One point of the compiled 2D kernel (mooney_rivlin.py:169-255).
